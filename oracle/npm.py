@@ -1,0 +1,200 @@
+"""The NPM model: encode -> decode -> Table 1 -> pdf / sample, and one
+optimisation step (Fig. 2 stages (1)-(5); §4.1-4.3, §5).
+
+TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.
+
+  NPM(x | Phi) = Theta_hat(x)                                  (Eq. 6)
+  NPM_product(x, w_o | Phi) = Theta_hat(x, w_o)                (Eq. 11)
+  MLP(G(x | Phi_E) | Phi_M) = Theta_hat(x)                     (Eq. 14)
+
+Parameter layout (flat, the C-ABI's NPM_BUF_* layout): the MLP affine layers in
+order, each W [out][in] row-major followed by b [out]; then the grid levels
+coarsest first, each [entries][F].
+
+Product mode (C-O6): z = [G(x), SH4(w_o), SH4(n), roughness].
+RGB targets are reduced by luminance 0.2126/0.7152/0.0722 (C-A11).
+"""
+from dataclasses import dataclass, field
+import numpy as np
+
+from . import grid, mlp, sh, vmf, adam
+
+RADIANCE, PRODUCT = 0, 1
+LUMA = np.array([0.2126, 0.7152, 0.0722])
+
+
+@dataclass
+class Config:
+    mode: int = RADIANCE
+    n_lobes: int = 8
+    n_levels: int = 8
+    n_features: int = 4
+    base_res: int = 8
+    max_res: int = 86
+    log2_hashmap: int = 18
+    mlp_linear_layers: int = 3
+    mlp_width: int = 64
+    sh_bands: int = 4
+    aabb_lo: tuple = (-1.0, -1.0, -1.0)
+    aabb_hi: tuple = (1.0, 1.0, 1.0)
+    lr: float = 5e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    ema_decay: float = 0.99
+    kappa_min: float = 1e-5
+    kappa_max: float = 1e5
+
+    @property
+    def resolutions(self):
+        return grid.level_resolutions(self.base_res, self.max_res, self.n_levels)
+
+    @property
+    def table_sizes(self):
+        return grid.level_table_sizes(self.resolutions, self.log2_hashmap)
+
+    @property
+    def n_in(self):
+        n = self.n_levels * self.n_features
+        if self.mode == PRODUCT:
+            n += 2 * self.sh_bands ** 2 + 1
+        return n
+
+    @property
+    def layer_dims(self):
+        dims = [self.n_in] + [self.mlp_width] * (self.mlp_linear_layers - 1) + [4 * self.n_lobes]
+        return list(zip(dims[:-1], dims[1:]))
+
+    @property
+    def n_mlp(self):
+        return sum(o * i + o for i, o in self.layer_dims)
+
+    @property
+    def n_grid(self):
+        return sum(self.table_sizes) * self.n_features
+
+
+def unpack(cfg, flat):
+    """Flat parameter vector -> (layers [(W, b)], tables [[size_l, F]])."""
+    layers, off = [], 0
+    for i, o in cfg.layer_dims:
+        w = flat[off:off + o * i].reshape(o, i); off += o * i
+        b = flat[off:off + o]; off += o
+        layers.append((w, b))
+    tables = []
+    for s in cfg.table_sizes:
+        tables.append(flat[off:off + s * cfg.n_features].reshape(s, cfg.n_features))
+        off += s * cfg.n_features
+    return layers, tables
+
+
+def pack(cfg, layers, tables):
+    parts = []
+    for w, b in layers:
+        parts += [w.ravel(), b.ravel()]
+    parts += [t.ravel() for t in tables]
+    return np.concatenate(parts)
+
+
+def grid_mask(cfg):
+    m = np.zeros(cfg.n_mlp + cfg.n_grid, bool)
+    m[cfg.n_mlp:] = True
+    return m
+
+
+def encode(cfg, flat, x):
+    """Eq. 13 -> G [L*F, n] (float64)."""
+    _, tables = unpack(cfg, flat)
+    return grid.encode(x, cfg.aabb_lo, cfg.aabb_hi, cfg.resolutions, cfg.table_sizes,
+                       cfg.log2_hashmap, tables)
+
+
+def network_input(cfg, flat, q):
+    """z = G(x) (radiance) or [G, SH(w_o), SH(n), roughness] (product)."""
+    g = encode(cfg, flat, q['x'])
+    if cfg.mode != PRODUCT:
+        return g
+    return np.concatenate([g, sh.sh_encode(q['wo'], cfg.sh_bands), sh.sh_encode(q['n'], cfg.sh_bands),
+                           np.asarray(q['rough'], np.float64)[None, :]], axis=0)
+
+
+def decode(cfg, flat, q):
+    """Eq. 14 + Table 1: returns (raw [4K, n], activated mixture dict)."""
+    layers, _ = unpack(cfg, flat)
+    raw, _, _ = mlp.forward(layers, network_input(cfg, flat, q))
+    return raw, vmf.activate(raw, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
+
+
+def pdf(cfg, flat, q, w):
+    """Eq. 4 at caller directions w [3, n]."""
+    _, act = decode(cfg, flat, q)
+    return vmf.mixture_pdf(np.asarray(w, np.float64), act)
+
+
+def sample(cfg, flat, q, u):
+    """C-O10 with caller uniforms u [3, n] -> (omega [3,n], V(omega) [n], lobe)."""
+    _, act = decode(cfg, flat, q)
+    return vmf.sample(act, np.asarray(u, np.float64), cfg.n_lobes)
+
+
+def scalar_target(target):
+    t = np.asarray(target, np.float64)
+    if t.ndim == 1:
+        return t
+    if t.shape[0] == 1:
+        return t[0]
+    return (LUMA[:, None] * t).sum(axis=0)
+
+
+def gradient(cfg, flat, q, wi, target, sample_pdf, n_global):
+    """Eq. 9 + back propagation: the flat gradient of
+    l = sum_n s_n log max(V_n, 1e-30), s_n = -(D^_n/p~_n)/N_global, with respect
+    to every parameter, plus step statistics."""
+    layers, _ = unpack(cfg, flat)
+    z = network_input(cfg, flat, q)
+    raw, pres, inputs = mlp.forward(layers, z)
+    wi = np.asarray(wi, np.float64)
+    s, dropped, zero = vmf.record_scale(scalar_target(target), np.asarray(sample_pdf, np.float64), n_global)
+    draw, logv = vmf.grad_head(raw, wi, s, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
+    mgrads, dz = mlp.backward(layers, pres, inputs, draw)
+    gl = cfg.n_levels * cfg.n_features
+    ggrads = grid.scatter_grad(q['x'], cfg.aabb_lo, cfg.aabb_hi, cfg.resolutions, cfg.table_sizes,
+                               dz[:gl], cfg.n_features)
+    g = pack(cfg, mgrads, ggrads)
+    stats = dict(loss_proxy=float((s * logv).sum()), n_used=int((~dropped & ~zero).sum()),
+                 n_zero_target=int(zero.sum()), n_dropped=int(dropped.sum()))
+    return g, stats
+
+
+@dataclass
+class State:
+    cfg: Config
+    params: np.ndarray
+    m: np.ndarray = None
+    v: np.ndarray = None
+    ema: np.ndarray = None
+    t: int = 0
+
+    def __post_init__(self):
+        n = self.params.size
+        self.m = np.zeros(n) if self.m is None else self.m
+        self.v = np.zeros(n) if self.v is None else self.v
+        self.ema = self.params.copy() if self.ema is None else self.ema
+
+
+def optimizer_step(state, g):
+    """C-O17 + C-O18 at t := t + 1.  Returns n_nonfinite."""
+    c = state.cfg
+    state.t += 1
+    state.params, state.m, state.v, state.ema, nnf = adam.adam_ema_step(
+        state.params, g, state.m, state.v, state.ema, state.t, grid_mask(c),
+        c.lr, c.beta1, c.beta2, c.adam_eps, c.ema_decay)
+    return nnf
+
+
+def train_step(state, q, wi, target, sample_pdf, n_global=None):
+    n = np.asarray(q['x']).shape[1]
+    g, stats = gradient(state.cfg, state.params, q, wi, target, sample_pdf, n if n_global is None else n_global)
+    stats['grad_norm_sq'] = float(np.sum(np.where(np.isfinite(g), g, 0.0) ** 2))
+    stats['n_nonfinite_grad'] = optimizer_step(state, g)
+    return g, stats
