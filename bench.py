@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark of the NPM hot path (arXiv 2504.04315) on B200.
+
+One STEP = one pass of the whole hot path over one batch of synthetic input
+(DESIGN.md "Measurement"): a guided query wave -- npm_sample with the fused pdf
+at caller directions (encode -> decode -> Table 1 -> sample + pdf) over n
+queries -- followed by one optimisation step -- npm_accumulate_grads (Eq. 9
+head -> backprop -> grid scatter-add) over n records, [gradient allreduce over
+NCCL when N > 1], npm_optimizer_step (Adam + EMA).  n = BASELINE configs[1]
+(c2: 1280 x 720 = 921,600) per GPU; N > 1 is weak scaling with the gradient
+allreduced every step.
+
+value   = (queries + training records) processed by all ranks / device time,
+          i.e. 2 n N / t_step ("samples/s": one query and one record per
+          pixel-sample); train_samples_per_s and queries_per_s are the two
+          phases timed separately inside the same steps.
+e2e     = the same metric through the C ABI with HOST (pinned) buffers, the
+          host<->device copies inside the timed region.
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import synth  # noqa: E402
+from workloads.configs import CONFIGS  # noqa: E402
+
+METRIC = "NPM training samples/sec and guided pdf+sample queries/sec at 1/2/4/8 B200"
+UNIT = "samples/s"
+WORKLOAD = "c2"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_oracle_step(name, n, seed=0):
+    """The float64 oracle as it stands (tests' reference), one step of the
+    hot path on n samples: decode + sample + pdf at caller directions for n
+    queries, gradient over n records, Adam + EMA over all parameters."""
+    from oracle import npm as onpm, vmf as ovmf, philox as ophilox
+    cfg = onpm.Config(**CONFIGS[name]["model"])
+    p = synth.random_params(cfg.layer_dims, cfg.n_grid, cfg.n_lobes, seed=seed).astype(np.float64)
+    state = onpm.State(cfg, p)
+    qb = synth.query_batch(n, seed=seed + 1)
+    tb = synth.training_batch(n, seed=seed + 2)
+    t0 = time.perf_counter()
+    _, act = onpm.decode(cfg, state.ema, dict(x=qb["x"]))
+    u = ophilox.sample_uniforms(n, 1234, 0)
+    ovmf.sample(act, u, cfg.n_lobes)
+    ovmf.mixture_pdf(qb["wq"].astype(np.float64), act)
+    onpm.train_step(state, dict(x=tb["x"]), tb["wi"].astype(np.float64), tb["target"].astype(np.float64),
+                    tb["pdf"].astype(np.float64), n)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(name, target_s=12.0):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        n = 1 << 13
+        dt = cpu_oracle_step(name, n)
+        n2 = int(min(1 << 18, max(n, n * target_s / max(dt, 1e-3))))
+        dt2 = cpu_oracle_step(name, n2)
+    return {"value": 2 * n2 / dt2, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "%s workload, %d queries + %d records, one step (float64 numpy oracle, 1 thread; "
+                      "Adam over all %s params)" % (name, n2, n2, "c2")}
+
+
+def run_reference(args, rank):
+    """--impl reference: the oracle on host cores, same metric/config."""
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    n = 1 << 14
+    with threadpool_limits(limits=1):
+        for _ in range(args.warmup):
+            cpu_oracle_step(WORKLOAD, n)
+        ts = [cpu_oracle_step(WORKLOAD, n, seed=i) for i in range(args.steps)]
+    t = float(np.sum(ts))
+    v = 2 * n * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD + " (bounded sample: %d queries + %d records "
+                                                           "per step)" % (n, n), "n_per_gpu": n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": "%d queries + %d records per step of the %s workload" % (n, n, WORKLOAD)},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=WORKLOAD, choices=list(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2504_04315_b200 import npm
+    from paper_2504_04315_b200.dp import DataParallel
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    name = args.workload
+    cfg = CONFIGS[name]
+    n = cfg["n"] if name != "c3" else cfg["n_global"] // world
+    m = npm.Model(local, **cfg["model"])
+    dp = DataParallel(m, world)
+    # inputs resident in HBM (device-timed value)
+    qb = synth.query_batch(n, seed=100 + rank, product=m.product)
+    tb = synth.training_batch(n, seed=200 + rank, product=m.product)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    qx, wq = T(qb["x"]), T(qb["wq"])
+    tx, twi, ttg, tpd = T(tb["x"]), T(tb["wi"]), T(tb["target"]), T(tb["pdf"])
+    extra_q = [T(qb["wo"]), T(qb["nrm"]), T(qb["rough"])] if m.product else [None, None, None]
+    extra_t = [T(tb["wo"]), T(tb["nrm"]), T(tb["rough"])] if m.product else [None, None, None]
+    qq = m.query(qx, *extra_q)
+    qt = m.query(tx, *extra_t)
+    wi_o, pdf_o, pdfq_o = (torch.empty(3, n, device=dev), torch.empty(n, device=dev),
+                           torch.empty(n, device=dev))
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(i, ev=None):
+        npm.npm_sample(m.h, qq, None, 0xC0FFEE, i * n, True, wi_o[0], wi_o[1], wi_o[2], pdf_o, wq[0], wq[1],
+                       wq[2], pdfq_o, stream=stream)
+        if ev is not None:
+            ev.record()
+        dp.train_step(qt, twi, ttg, tpd, n_local=n)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    launches0 = m.launches
+    npm.npm_profile_reset(m.h)
+    npm.npm_profile_enable(m.h, True)
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                     # L2 flush between timed steps (not timed)
+            e0[i].record()
+            step(args.warmup + i, e1[i])
+            e2[i].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = m.launches - launches0
+    npm.npm_profile_enable(m.h, False)
+    prof = npm.npm_profile_read(m.h)
+    t_q = sum(a.elapsed_time(b) for a, b in zip(e0, e1)) / 1e3
+    t_t = sum(a.elapsed_time(b) for a, b in zip(e1, e2)) / 1e3
+    tt = torch.tensor([t_q + t_t, t_q, t_t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_tot, t_q, t_t = tt.tolist()
+    K = args.steps
+    value = 2 * n * world * K / t_tot
+
+    # ---- e2e: same step through the C ABI with pinned HOST buffers ------------------------
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hqx, hwq = pin(qb["x"]), pin(qb["wq"])
+    htx, htwi, httg, htpd = pin(tb["x"]), pin(tb["wi"]), pin(tb["target"]), pin(tb["pdf"])
+    hex_q = [pin(qb["wo"]), pin(qb["nrm"]), pin(qb["rough"])] if m.product else [None, None, None]
+    hex_t = [pin(tb["wo"]), pin(tb["nrm"]), pin(tb["rough"])] if m.product else [None, None, None]
+    hq = npm.make_query(n, hqx[0], hqx[1], hqx[2], *(
+        [hex_q[0][0], hex_q[0][1], hex_q[0][2], hex_q[1][0], hex_q[1][1], hex_q[1][2], hex_q[2]] if m.product else []))
+    ht = npm.make_query(n, htx[0], htx[1], htx[2], *(
+        [hex_t[0][0], hex_t[0][1], hex_t[0][2], hex_t[1][0], hex_t[1][1], hex_t[1][2], hex_t[2]] if m.product else []))
+    hwi, hpdf, hpdfq = pin(np.zeros((3, n), np.float32)), pin(np.zeros(n, np.float32)), pin(np.zeros(n, np.float32))
+    n_in_f = 3 + (7 if m.product else 0)
+    h2d = n * 4 * (n_in_f + 3) + n * 4 * (n_in_f + 3 + ttg.shape[0] + 1)
+    d2h = n * 4 * 5 + 8 * 6
+
+    def e2e_step(i):
+        npm.npm_sample(m.h, hq, None, 0xC0FFEE, i * n, True, hwi[0], hwi[1], hwi[2], hpdf, hwq[0], hwq[1], hwq[2],
+                       hpdfq, stream=stream)
+        return dp.train_step(ht, htwi, httg, htpd, n_local=n, want_stats=True)   # stats: D2H of the loss
+
+    for i in range(2):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record()
+    for i in range(K):
+        e2e_step(i)
+    ee1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([ee0.elapsed_time(ee1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = 2 * n * world * K / te.item()
+
+    # ---- roofline of the dominant kernel -----------------------------------------------------
+    hbm, bf16, bf16s, src = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    kname, (kl, kms) = dom
+    L, F = m.L, m.F
+    gather = 8 * L * F * 4
+    per_unit = {  # algorithmic bytes per sample
+        "query": 12 + 12 + gather + 12 + 4 + 4,          # x, caller dir, gathers, sample w + pdf, pdf_q
+        "train_forward": 12 + 12 + 4 * ttg.shape[0] + 4 + gather,
+        "train_backward": 12 + gather,                   # x (re-derive corners) + scatter-add
+        "weight_grad": 0, "adam": 0, "encode": 12 + gather + 4 * L * F,
+    }
+    units = n * K
+    if kname == "adam":
+        algo = 40 * m.n_params * kl
+    else:
+        algo = per_unit.get(kname, 0) * units
+    achieved = algo / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "kernel": kname, "kernel_ms_per_launch": kms / max(kl, 1),
+            "kernel_share_of_step": (kms / 1e3) / t_tot if t_tot > 0 else None, "peak_source": src,
+            "per_unit_bytes": per_unit.get(kname), "units_per_launch": n}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(name)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+                "ms_per_step": 1e3 * t_tot / K, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "%s: %s" % (name, "per-frame batch 1280x720 queries + records per GPU, "
+                                                   "K=8, L=8 (D 8..86, T=2^18), 3x64 MLP" if name == "c2" else name),
+                           "n_per_gpu": n, "l2": "flushed between timed steps (512 MB write)",
+                           "parallelism": "dp%d" % world},
+                "train_samples_per_s": n * world * K / t_t, "queries_per_s": n * world * K / t_q,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches, "gpu_launches_per_step": launches / K,
+                "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
+                "clocks": clk.summary(), "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

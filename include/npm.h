@@ -1,0 +1,237 @@
+/*
+ * npm.h -- C ABI of the B200-native Neural Parametric Mixtures hot path.
+ *
+ * Paper: Dong, Wang, Li, "Neural Parametric Mixtures for Path Guiding",
+ * arXiv 2504.04315.  Citations: P:n = line n of the paper's LaTeX source
+ * with the section / equation named; C-xx = the reading recorded in
+ * DESIGN.md ("Readings of the paper").
+ *
+ * The library evaluates and trains
+ *
+ *     NPM(x | Phi) = Theta_hat(x)                 (Eq. 6,  P:152-154)
+ *     NPM_product(x, w_o | Phi) = Theta_hat(x, w_o) (Eq. 11)
+ *     MLP(G(x | Phi_E) | Phi_M) = Theta_hat(x)    (Eq. 14)
+ *
+ * with G the multi-resolution grid embedding (Eq. 13), Theta_hat a
+ * K-lobe vMF mixture (Eq. 3/4) after the Table 1 mappings
+ * (P:166-179), trained with the Monte Carlo KL gradient (Eq. 9)
+ * back-propagated through decoder and grid into Adam + EMA.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions common to every call
+ *   - Batches are structure-of-arrays ("structure-of-arrays (SoA) memory
+ *     layout"): one float32 array per component, length n.
+ *   - POINTERS MAY BE HOST OR DEVICE.  The library inspects every array
+ *     pointer (cudaPointerGetAttributes).  Device (or managed) pointers are used
+ *     in place.  Host pointers (pinned or pageable) are staged through
+ *     library-owned device scratch: inputs copied host->device, outputs
+ *     device->host, all on `stream`; the call then returns only after the
+ *     output copies completed (pageable) or after they were enqueued (pinned
+ *     host memory, still ordered on `stream`: synchronise `stream` before
+ *     reading them).  Device pointers never cause a host synchronisation
+ *     except where a host out-parameter (stats) is requested.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  All work is enqueued on it, in call order.
+ *   - Ownership: every array is caller-owned; outputs must not alias inputs.
+ *     The model owns parameters, gradients, Adam moments, EMA shadow and
+ *     scratch.
+ *   - Errors: a bad argument returns NPM_ERR_INVALID with nothing enqueued; a
+ *     CUDA failure returns NPM_ERR_CUDA (the model may then be unusable).
+ *     npm_last_error() gives a thread-local message.  n == 0 is a no-op
+ *     returning NPM_OK.  Data problems are NOT errors (see npm_train_step).
+ *   - Concurrency: queries (encode/decode/pdf/sample) only read the model and
+ *     may run concurrently with each other; a training call must not overlap
+ *     queries on the same model (training happens between render waves).
+ *
+ * Supported configurations (validated by npm_create): n_features = 4;
+ * 1 <= n_levels <= 16; 1 <= n_lobes <= 16 ; decoder shapes
+ * {n_in 16, width 32, 2 layers}, {n_in 32, width 64, 3 layers},
+ * {n_in 64, width 64, 3 layers}, {product: n_in 65, width 64, 3 layers};
+ * 4*n_lobes must be 32 or 64.
+ */
+#ifndef NPM_H
+#define NPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NPM_VERSION 1
+
+typedef struct npm_model npm_model; /* opaque */
+
+typedef enum {
+  NPM_OK = 0,
+  NPM_ERR_INVALID = 1, /* bad config / argument; nothing was enqueued */
+  NPM_ERR_CUDA = 2,    /* CUDA runtime failure */
+  NPM_ERR_NCCL = 3,    /* collective failure (multi-GPU) */
+  NPM_ERR_OOM = 4,     /* device allocation failed */
+  NPM_ERR_STATE = 5    /* call not valid in the model's current state */
+} npm_status;
+
+typedef enum { NPM_RADIANCE = 0, NPM_PRODUCT = 1 } npm_mode;
+
+/* Parameter-sized buffers, all in the same flat float32 layout:
+ * the decoder's affine layers in order, each W[out][in] row-major then b[out];
+ * then the grid levels coarsest first, each [entries][F] (entry index as in
+ * npm_encode_debug). Total length n_mlp + n_grid (npm_param_count). */
+typedef enum {
+  NPM_BUF_PARAMS = 0, /* live trainable parameters Phi = Phi_M u Phi_E (Eq. 14) */
+  NPM_BUF_GRADS = 1,  /* gradient accumulator (sum over records, already / N_global) */
+  NPM_BUF_ADAM_M = 2, /* Adam first moment */
+  NPM_BUF_ADAM_V = 3, /* Adam second moment */
+  NPM_BUF_EMA = 4     /* EMA shadow used by queries with use_ema = 1 */
+} npm_buffer;
+
+typedef struct {
+  int32_t mode;              /* npm_mode; PRODUCT conditions on w_o, n, roughness (§4.3) */
+  int32_t n_lobes;           /* K vMF components (K = 8) */
+  int32_t n_levels;          /* L grid levels (L = 8) */
+  int32_t n_features;        /* F features per lattice point (F = 4) */
+  int32_t base_res;          /* D_1 lattice points per axis (8) */
+  int32_t max_res;           /* D_L (86); D_l = ceil(D_1 b^(l-1) - 1e-9), C-A3 */
+  int32_t log2_hashmap;      /* T = 2^log2_hashmap entries cap per level; levels with
+                                D^3 > T are spatially hashed (C-A4); 0 = all dense */
+  int32_t mlp_linear_layers; /* affine layers incl. output ("3 linear layers") */
+  int32_t mlp_width;         /* hidden width (64) */
+  int32_t sh_bands;          /* SH bands for w_o and n in product mode (C-A20: 4) */
+  float aabb_lo[3], aabb_hi[3]; /* scene bounds mapped onto the grids (C-O1) */
+  float lr;                  /* Adam learning rate (0.005) */
+  float beta1, beta2, adam_eps; /* 0.9, 0.999, 1e-8 (C-A14) */
+  float ema_decay;           /* 0.99 (C-A15) */
+  float kappa_min, kappa_max;/* clamp of kappa = exp(kappa') (C-A8): 1e-5, 1e5 */
+  uint64_t init_seed;        /* parameter initialisation seed (C-A21) */
+} npm_config;
+
+/* One SoA queue of shading points. px/py/pz: world-space x.
+ * wox.., nx.., rough: product mode only (w_o unit outgoing direction, n unit
+ * normal, roughness in [0,1]); ignored (may be NULL) in radiance mode. */
+typedef struct {
+  int64_t n;
+  const float *px, *py, *pz;
+  const float *wox, *woy, *woz;
+  const float *nx, *ny, *nz;
+  const float *rough;
+} npm_query;
+
+/* Training statistics of one step. loss_proxy = sum_n s_n log max(V_n,
+ * 1e-30) with s_n = -(D^_n / p~_n) / N_global: the Theta-dependent part of the
+ * Eq. 8 estimate. */
+typedef struct {
+  double loss_proxy;
+  double grad_norm_sq;        /* ||g||^2 of the (reduced) gradient, finite entries */
+  int64_t n_used;             /* records with finite, non-zero D^/p~ */
+  int64_t n_zero_target;      /* records with D^ = 0 (zero gradient) */
+  int64_t n_dropped;          /* non-finite D^ or p~ <= 0 / non-finite */
+  int64_t n_nonfinite_grad;   /* gradient entries zeroed before Adam */
+} npm_step_stats;
+
+/* Defaults of the paper's model + readings C-A3..C-A15. */
+void npm_default_config(npm_config* cfg);
+
+/* Validate cfg, allocate all model state on `cuda_device`, initialise
+ * parameters (features U(-1e-2, 1e-2), Xavier-uniform weights, zero biases;
+ * C-A21), Adam moments 0, EMA := params, step t = 0.  Synchronous. */
+npm_status npm_create(const npm_config* cfg, int cuda_device, npm_model** out);
+npm_status npm_destroy(npm_model* model);
+
+/* n_mlp = sum over layers of out*in + out; n_grid = F * sum_l entries_l. */
+npm_status npm_param_count(const npm_model* model, int64_t* n_grid, int64_t* n_mlp);
+/* Per-level lattice resolution D_l and table entries (min(D^3, T)). */
+npm_status npm_level_info(const npm_model* model, int32_t* res, int64_t* entries);
+
+/* Copy a whole parameter-sized buffer out of / into the model (count must be
+ * n_mlp + n_grid). Used for checkpoints and for parity (identical params on
+ * both sides). src/dst host or device. */
+npm_status npm_get_buffer(npm_model* model, npm_buffer which, float* dst, int64_t count, void* stream);
+npm_status npm_set_buffer(npm_model* model, npm_buffer which, const float* src, int64_t count, void* stream);
+/* Adam step counter t (bias correction uses the global t, C-A14). */
+npm_status npm_get_step(const npm_model* model, int64_t* t);
+npm_status npm_set_step(npm_model* model, int64_t t);
+
+/* Eq. 13: feat = G(x) as [L*F][n] (feature-major SoA, level-major,
+ * coarsest level first, C-O5). use_ema selects the EMA shadow. */
+npm_status npm_encode(npm_model* model, const npm_query* q, int use_ema, float* feat, void* stream);
+
+/* Parity/debug view of Eq. 13: the 8 corner entry indices per level
+ * (uint32 [L][8][n]; corner c = cx + 2cy + 4cz; dense index Px + D(Py + D Pz),
+ * hashed levels (Px ^ Py*2654435761 ^ Pz*805459861) & (T-1), C-O4) and the
+ * trilinear weights (float [L][8][n]). The cell index is the pinned fp32
+ * sequence C-O1/C-O3 (bit-exact with the oracle). Either output may be NULL. */
+npm_status npm_encode_debug(npm_model* model, const npm_query* q, uint32_t* idx, float* w, void* stream);
+
+/* Eq. 14 + Table 1. feat: optional [L*F][n] encoding to decode instead of
+ * G(x) (radiance mode only; NULL = encode internally). Outputs (each may be
+ * NULL): raw [4K][n] in the block layout [lambda' | kappa' | theta' | phi']
+ * (C-A6); lambda [K][n]; kappa [K][n]; mu [3][K][n] (C-A7 convention). */
+npm_status npm_decode(npm_model* model, const npm_query* q, const float* feat, int use_ema,
+                      float* raw, float* lambda, float* kappa, float* mu, void* stream);
+
+/* Eq. 4 mixture pdf V(w | Theta_hat(x)) at caller unit directions w. */
+npm_status npm_pdf(npm_model* model, const npm_query* q, const float* wix, const float* wiy,
+                   const float* wiz, int use_ema, float* pdf, void* stream);
+
+/* Guided direction sampled from V(. | Theta_hat(x)) with the numerically
+ * stable vMF inversion (Jakob 2012; C-O10) and the FULL mixture pdf at
+ * it. u: [3][n] uniforms in [0,1) or NULL => Philox4x32-10 with key = seed,
+ * counter = (i + offset) (C-O11). Optional fused query: if qx/qy/qz/pdf_q are
+ * all non-NULL, V is also evaluated at the caller directions q for the same
+ * x (one encode + decode serves both: the "pdf + sample" query). */
+npm_status npm_sample(npm_model* model, const npm_query* q, const float* u, uint64_t seed,
+                      uint64_t offset, int use_ema, float* wix, float* wiy, float* wiz,
+                      float* pdf, const float* qx, const float* qy, const float* qz,
+                      float* pdf_q, void* stream);
+
+/* One optimisation step ("optimization step is performed for each spp"):
+ * Eq. 9 gradient over the batch, back propagation through decoder and grid
+ * (P:216), [allreduce if a communicator is attached], Adam + EMA.
+ * Records: directions wi (unit), target = D^ as [C][n] with C = 1 or 3 (RGB
+ * reduced by luminance, C-A11), sample_pdf = p~ the direction was drawn from
+ * (stop-gradient, C-A12). n_global = records across all ranks (the 1/N of
+ * Eq. 9, C-A13); pass n on one GPU. Data problems are not errors: D^ = 0 gives
+ * no gradient; non-finite D^ or p~ <= 0 drops the record (still counted in N);
+ * non-finite gradient entries are zeroed; V is floored at 1e-30. stats may be
+ * NULL (no host synchronisation); otherwise the call synchronises `stream`. */
+npm_status npm_train_step(npm_model* model, const npm_query* q, const float* wix, const float* wiy,
+                          const float* wiz, const float* target, int target_channels,
+                          const float* sample_pdf, int64_t n_global, npm_step_stats* stats,
+                          void* stream);
+
+/* Split form: npm_train_step == npm_accumulate_grads + npm_optimizer_step.
+ * accumulate_grads ADDS the batch's gradient into NPM_BUF_GRADS (no update);
+ * optimizer_step [allreduces GRADS,] applies Adam + EMA at t := t + 1 and
+ * zeroes GRADS. */
+npm_status npm_accumulate_grads(npm_model* model, const npm_query* q, const float* wix,
+                                const float* wiy, const float* wiz, const float* target,
+                                int target_channels, const float* sample_pdf, int64_t n_global,
+                                npm_step_stats* stats, void* stream);
+npm_status npm_optimizer_step(npm_model* model, npm_step_stats* stats, void* stream);
+
+/* Raw device pointer of a model buffer (for zero-copy collectives by the
+ * caller's process group). */
+npm_status npm_buffer_device_ptr(npm_model* model, npm_buffer which, float** ptr, int64_t* count);
+
+/* Number of library kernels launched on this model since creation (the
+ * bench's gpu_launches evidence). */
+int64_t npm_launch_count(const npm_model* model);
+
+/* Kernel timing: when enabled, every library kernel launch is bracketed by
+ * CUDA events recorded on its launch stream (used by bench.py for the
+ * per-kernel roofline). Kinds are 0 .. npm_profile_kinds()-1; npm_profile_read
+ * synchronises on the recorded events and returns the kind's name, launches
+ * and total device milliseconds since the last reset. */
+int npm_profile_kinds(void);
+npm_status npm_profile_enable(npm_model* model, int enable);
+npm_status npm_profile_reset(npm_model* model);
+npm_status npm_profile_read(npm_model* model, int kind, const char** name, int64_t* launches,
+                            double* total_ms);
+
+const char* npm_last_error(void);
+int npm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NPM_H */

@@ -154,7 +154,10 @@ def gradient(cfg, flat, q, wi, target, sample_pdf, n_global):
     z = network_input(cfg, flat, q)
     raw, pres, inputs = mlp.forward(layers, z)
     wi = np.asarray(wi, np.float64)
-    s, dropped, zero = vmf.record_scale(scalar_target(target), np.asarray(sample_pdf, np.float64), n_global)
+    tgt = np.asarray(target, np.float64)
+    is_zero = (tgt == 0).all(axis=0) if tgt.ndim == 2 else (tgt == 0)
+    s, dropped, zero = vmf.record_scale(scalar_target(target), np.asarray(sample_pdf, np.float64), n_global,
+                                        is_zero)
     draw, logv = vmf.grad_head(raw, wi, s, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
     mgrads, dz = mlp.backward(layers, pres, inputs, draw)
     gl = cfg.n_levels * cfg.n_features

@@ -88,15 +88,17 @@ def sample(act, u, k):
     return omega, mixture_pdf(omega, act), lobe
 
 
-def record_scale(target, sample_pdf, n_global):
+def record_scale(target, sample_pdf, n_global, is_zero=None):
     """C-O12: a = D^/p~; the record is dropped (a := 0) if a is non-finite or
     p~ <= 0 or p~ is non-finite; s = -a / N_global (N counts every record,
-    C-A13).  Returns (s [n], dropped bool [n], zero_target bool [n])."""
+    C-A13).  ``is_zero``: the D^ = 0 decision (for RGB targets: every channel
+    is 0, C-A11); default target == 0.
+    Returns (s [n], dropped bool [n], zero_target bool [n])."""
     with np.errstate(divide='ignore', invalid='ignore'):
         a = target / sample_pdf
     dropped = ~np.isfinite(a) | ~np.isfinite(sample_pdf) | (sample_pdf <= 0)
     a = np.where(dropped, 0.0, a)
-    zero = (~dropped) & (target == 0)
+    zero = (~dropped) & ((target == 0) if is_zero is None else is_zero)
     return -a / n_global, dropped, zero
 
 

@@ -1,0 +1,734 @@
+// npm_capi.cu -- the C ABI (include/npm.h) and the model runtime: config
+// validation, level schedule, device state, host/device pointer staging,
+// kernel orchestration for encode / decode / pdf / sample / train.
+#include "../../include/npm.h"
+#include "npm_kernels.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace npm;
+
+namespace {
+
+thread_local std::string g_err;
+
+npm_status fail(npm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return fail(NPM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct npm_model {
+  npm_config cfg;
+  int device = 0;
+  int num_sms = 148;
+  NetShape shape{};
+  GridDesc grid{};
+  int res[kMaxLevels] = {};
+  int64_t entries[kMaxLevels] = {};
+  int64_t n_mlp = 0, n_grid = 0, n_total = 0;
+  float* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // params, grads, m, v, ema
+  int64_t t = 0;
+  // device statistics: [0] loss, [1] grad norm^2 ; counters [0] used [1] zero [2] dropped [3] nonfinite
+  double* dstats = nullptr;
+  unsigned long long* dcount = nullptr;
+  DevBuf scratch_train;            // act / delta rows
+  DevBuf stage[24];                // host-pointer staging slots
+  std::mutex stage_mu;
+  int64_t launches = 0;
+  // kernel timing (npm_profile_*): CUDA events around each launch, on its stream
+  bool prof = false;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  int64_t prof_launches[16] = {};
+  double prof_ms[16] = {};
+};
+
+namespace {
+
+struct Pending {
+  void* host;
+  const void* dev;
+  size_t bytes;
+  bool pageable;
+};
+
+// Host/device pointer resolution (npm.h "POINTERS MAY BE HOST OR DEVICE").
+struct Stager {
+  npm_model* m;
+  cudaStream_t st;
+  int next = 0;
+  std::vector<Pending> outs;
+  bool any_pageable = false;
+  cudaError_t err = cudaSuccess;
+
+  static int kind(const void* p) {  // 0 host-pageable, 1 host-pinned, 2 device/managed
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return 2;
+    if (at.type == cudaMemoryTypeHost) return 1;
+    return 0;
+  }
+  template <class T>
+  const T* in(const T* p, size_t count) {
+    if (!p || count == 0) return p;
+    const int k = kind(p);
+    if (k == 2) return p;
+    if (next >= 24) { err = cudaErrorMemoryAllocation; return nullptr; }
+    DevBuf& b = m->stage[next++];
+    err = b.ensure(count * sizeof(T));
+    if (err != cudaSuccess) return nullptr;
+    err = cudaMemcpyAsync(b.p, p, count * sizeof(T), cudaMemcpyHostToDevice, st);
+    return static_cast<const T*>(b.p);
+  }
+  template <class T>
+  T* out(T* p, size_t count) {
+    if (!p || count == 0) return p;
+    const int k = kind(p);
+    if (k == 2) return p;
+    if (next >= 24) { err = cudaErrorMemoryAllocation; return nullptr; }
+    DevBuf& b = m->stage[next++];
+    err = b.ensure(count * sizeof(T));
+    if (err != cudaSuccess) return nullptr;
+    outs.push_back({p, b.p, count * sizeof(T), k == 0});
+    any_pageable |= (k == 0);
+    return static_cast<T*>(b.p);
+  }
+  cudaError_t finish() {
+    for (auto& o : outs) {
+      cudaError_t e = cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return e;
+    }
+    if (any_pageable) return cudaStreamSynchronize(st);
+    return cudaSuccess;
+  }
+};
+
+bool query_ok(const npm_model* m, const npm_query* q) {
+  if (!q || q->n < 0) return false;
+  if (q->n == 0) return true;
+  if (!q->px || !q->py || !q->pz) return false;
+  if (m->cfg.mode == NPM_PRODUCT &&
+      (!q->wox || !q->woy || !q->woz || !q->nx || !q->ny || !q->nz || !q->rough))
+    return false;
+  return true;
+}
+
+// Stage all query inputs (x, and product-mode conditioning).
+void stage_query(Stager& s, const npm_model* m, const npm_query* q, npm_query& d) {
+  d = *q;
+  const size_t n = (size_t)q->n;
+  d.px = s.in(q->px, n); d.py = s.in(q->py, n); d.pz = s.in(q->pz, n);
+  if (m->cfg.mode == NPM_PRODUCT) {
+    d.wox = s.in(q->wox, n); d.woy = s.in(q->woy, n); d.woz = s.in(q->woz, n);
+    d.nx = s.in(q->nx, n); d.ny = s.in(q->ny, n); d.nz = s.in(q->nz, n);
+    d.rough = s.in(q->rough, n);
+  } else {
+    d.wox = d.woy = d.woz = d.nx = d.ny = d.nz = d.rough = nullptr;
+  }
+}
+
+void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryArgs& a) {
+  memset(&a, 0, sizeof(a));
+  a.n = d.n;
+  a.px = d.px; a.py = d.py; a.pz = d.pz;
+  a.wox = d.wox; a.woy = d.woy; a.woz = d.woz; a.nx = d.nx; a.ny = d.ny; a.nz = d.nz; a.rough = d.rough;
+  a.params = use_ema ? m->buf[NPM_BUF_EMA] : m->buf[NPM_BUF_PARAMS];
+  a.grid = m->grid;
+  a.log_kmin = logf(m->cfg.kappa_min);
+  a.log_kmax = logf(m->cfg.kappa_max);
+}
+
+const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward", "weight_grad", "adam"};
+enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKinds };
+
+cudaEvent_t take_event(npm_model* m) {
+  if (!m->pool.empty()) { cudaEvent_t e = m->pool.back(); m->pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Timed launch: records events around `f()` when profiling is on.
+template <class F>
+int timed(npm_model* m, int kind, cudaStream_t st, F&& f) {
+  if (!m->prof) return f();
+  cudaEvent_t a = take_event(m), b = take_event(m);
+  cudaEventRecord(a, st);
+  const int r = f();
+  cudaEventRecord(b, st);
+  m->pending.push_back({kind, a, b});
+  return r;
+}
+
+npm_status check_launch(npm_model* m, int r) {
+  if (r < 0) return fail(NPM_ERR_INVALID, "unsupported decoder shape");
+  m->launches += r;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(NPM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return NPM_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int npm_version(void) { return NPM_VERSION; }
+const char* npm_last_error(void) { return g_err.c_str(); }
+
+void npm_default_config(npm_config* c) {
+  memset(c, 0, sizeof(*c));
+  c->mode = NPM_RADIANCE;
+  c->n_lobes = 8;
+  c->n_levels = 8;
+  c->n_features = 4;
+  c->base_res = 8;
+  c->max_res = 86;
+  c->log2_hashmap = 18;      // C-A4
+  c->mlp_linear_layers = 3;
+  c->mlp_width = 64;
+  c->sh_bands = 4;           // C-A20
+  for (int a = 0; a < 3; ++a) { c->aabb_lo[a] = -1.0f; c->aabb_hi[a] = 1.0f; }
+  c->lr = 5e-3f;
+  c->beta1 = 0.9f; c->beta2 = 0.999f; c->adam_eps = 1e-8f;  // C-A14
+  c->ema_decay = 0.99f;      // C-A15
+  c->kappa_min = 1e-5f; c->kappa_max = 1e5f;                 // C-A8
+  c->init_seed = 0x4E504DULL;
+}
+
+npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
+  if (!cfg || !out) return fail(NPM_ERR_INVALID, "null argument");
+  const npm_config& c = *cfg;
+  if (c.mode != NPM_RADIANCE && c.mode != NPM_PRODUCT) return fail(NPM_ERR_INVALID, "bad mode");
+  if (c.n_features != 4) return fail(NPM_ERR_INVALID, "n_features must be 4");
+  if (c.n_levels < 1 || c.n_levels > kMaxLevels) return fail(NPM_ERR_INVALID, "n_levels out of range [1,16]");
+  if (c.n_lobes < 1 || c.n_lobes > kMaxLobes) return fail(NPM_ERR_INVALID, "n_lobes out of range [1,16]");
+  if (c.base_res < 2 || c.max_res < c.base_res || (c.n_levels > 1 && c.max_res <= c.base_res))
+    return fail(NPM_ERR_INVALID, "need 2 <= D_1 < D_L");
+  if (c.log2_hashmap < 0 || c.log2_hashmap > 30) return fail(NPM_ERR_INVALID, "log2_hashmap out of range");
+  for (int a = 0; a < 3; ++a)
+    if (!(c.aabb_hi[a] > c.aabb_lo[a]) || !std::isfinite(c.aabb_lo[a]) || !std::isfinite(c.aabb_hi[a]))
+      return fail(NPM_ERR_INVALID, "degenerate AABB");
+  if (c.mode == NPM_PRODUCT && c.sh_bands != 4) return fail(NPM_ERR_INVALID, "product mode needs sh_bands = 4");
+  if (!(c.kappa_min > 0) || !(c.kappa_max > c.kappa_min)) return fail(NPM_ERR_INVALID, "bad kappa range");
+  if (!(c.ema_decay >= 0 && c.ema_decay < 1)) return fail(NPM_ERR_INVALID, "ema_decay must be in [0,1)");
+
+  NetShape s;
+  s.n_in = c.n_levels * c.n_features + (c.mode == NPM_PRODUCT ? 2 * c.sh_bands * c.sh_bands + 1 : 0);
+  s.width = c.mlp_width;
+  s.n_layers = c.mlp_linear_layers;
+  s.n_out = 4 * c.n_lobes;
+  s.product = c.mode == NPM_PRODUCT;
+  if (!shape_supported(s)) return fail(NPM_ERR_INVALID, "unsupported decoder shape (see npm.h)");
+
+  DeviceGuard g(dev);
+  auto* m = new npm_model();
+  m->cfg = c;
+  m->device = dev;
+  m->shape = s;
+  if (cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    delete m;
+    return fail(NPM_ERR_CUDA, "no CUDA device");
+  }
+  // Level schedule (C-O2 / C-A3) and table sizes (C-A4).
+  const int L = c.n_levels;
+  if (L == 1) {
+    m->res[0] = c.max_res;
+  } else {
+    const double b = std::pow((double)c.max_res / (double)c.base_res, 1.0 / (L - 1));
+    for (int l = 0; l < L; ++l) m->res[l] = (int)std::ceil((double)c.base_res * std::pow(b, (double)l) - 1e-9);
+    m->res[L - 1] = c.max_res;
+  }
+  GridDesc& gd = m->grid;
+  gd.L = L;
+  gd.hashed_mask = 0;
+  int64_t off = 0;
+  const int64_t T = c.log2_hashmap ? (int64_t(1) << c.log2_hashmap) : 0;
+  for (int l = 0; l < L; ++l) {
+    const int64_t d3 = (int64_t)m->res[l] * m->res[l] * m->res[l];
+    int64_t e = d3;
+    if (T && d3 > T) { e = T; gd.hashed_mask |= 1u << l; }
+    if (e > 0xFFFFFFFFLL) { delete m; return fail(NPM_ERR_INVALID, "level too large for 32-bit indices"); }
+    m->entries[l] = e;
+    gd.res[l] = m->res[l];
+    gd.tsize[l] = (uint32_t)e;
+    gd.off[l] = off;
+    off += e;
+  }
+  for (int a = 0; a < 3; ++a) {
+    gd.lo[a] = c.aabb_lo[a];
+    gd.inv[a] = (float)(1.0 / ((double)c.aabb_hi[a] - (double)c.aabb_lo[a]));  // C-O1
+  }
+  m->n_grid = off * c.n_features;
+  int64_t nm = 0;
+  {
+    int dims[4] = {s.n_in, s.width, s.width, s.n_out};
+    if (s.n_layers == 2) dims[2] = s.n_out;
+    for (int k = 0; k < s.n_layers; ++k) nm += (int64_t)dims[k] * dims[k + 1] + dims[k + 1];
+  }
+  m->n_mlp = nm;
+  if (nm % 4) { delete m; return fail(NPM_ERR_INVALID, "internal: MLP size not 16B aligned"); }
+  m->n_total = m->n_mlp + m->n_grid;
+  for (int b = 0; b < 5; ++b) {
+    if (cudaMalloc(&m->buf[b], m->n_total * sizeof(float)) != cudaSuccess) {
+      npm_destroy(m);
+      return fail(NPM_ERR_OOM, "parameter buffers");
+    }
+  }
+  if (cudaMalloc(&m->dstats, 2 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&m->dcount, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    npm_destroy(m);
+    return fail(NPM_ERR_OOM, "stats");
+  }
+  cudaStream_t st = 0;
+  launch_init_params(m->buf[NPM_BUF_PARAMS], m->n_mlp, m->n_total, s, c.init_seed, st);
+  m->launches += 1;
+  cudaMemsetAsync(m->buf[NPM_BUF_GRADS], 0, m->n_total * sizeof(float), st);
+  cudaMemsetAsync(m->buf[NPM_BUF_ADAM_M], 0, m->n_total * sizeof(float), st);
+  cudaMemsetAsync(m->buf[NPM_BUF_ADAM_V], 0, m->n_total * sizeof(float), st);
+  cudaMemcpyAsync(m->buf[NPM_BUF_EMA], m->buf[NPM_BUF_PARAMS], m->n_total * sizeof(float),
+                  cudaMemcpyDeviceToDevice, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    npm_destroy(m);
+    return fail(NPM_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return NPM_OK;
+}
+
+npm_status npm_destroy(npm_model* m) {
+  if (!m) return NPM_OK;
+  DeviceGuard g(m->device);
+  for (auto& b : m->buf) if (b) cudaFree(b);
+  if (m->dstats) cudaFree(m->dstats);
+  if (m->dcount) cudaFree(m->dcount);
+  m->scratch_train.release();
+  for (auto& s : m->stage) s.release();
+  for (auto& r : m->pending) { m->pool.push_back(r.a); m->pool.push_back(r.b); }
+  for (auto e : m->pool) cudaEventDestroy(e);
+  delete m;
+  return NPM_OK;
+}
+
+npm_status npm_param_count(const npm_model* m, int64_t* n_grid, int64_t* n_mlp) {
+  if (!m) return fail(NPM_ERR_INVALID, "null model");
+  if (n_grid) *n_grid = m->n_grid;
+  if (n_mlp) *n_mlp = m->n_mlp;
+  return NPM_OK;
+}
+
+npm_status npm_level_info(const npm_model* m, int32_t* res, int64_t* entries) {
+  if (!m) return fail(NPM_ERR_INVALID, "null model");
+  for (int l = 0; l < m->cfg.n_levels; ++l) {
+    if (res) res[l] = m->res[l];
+    if (entries) entries[l] = m->entries[l];
+  }
+  return NPM_OK;
+}
+
+npm_status npm_get_step(const npm_model* m, int64_t* t) {
+  if (!m || !t) return fail(NPM_ERR_INVALID, "null argument");
+  *t = m->t;
+  return NPM_OK;
+}
+npm_status npm_set_step(npm_model* m, int64_t t) {
+  if (!m || t < 0) return fail(NPM_ERR_INVALID, "bad argument");
+  m->t = t;
+  return NPM_OK;
+}
+
+npm_status npm_buffer_device_ptr(npm_model* m, npm_buffer which, float** ptr, int64_t* count) {
+  if (!m || (int)which < 0 || (int)which > 4 || !ptr) return fail(NPM_ERR_INVALID, "bad argument");
+  *ptr = m->buf[which];
+  if (count) *count = m->n_total;
+  return NPM_OK;
+}
+
+int64_t npm_launch_count(const npm_model* m) { return m ? m->launches : 0; }
+
+static void prof_drain(npm_model* m) {
+  for (auto& r : m->pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    m->prof_ms[r.kind] += ms;
+    m->prof_launches[r.kind] += 1;
+    m->pool.push_back(r.a);
+    m->pool.push_back(r.b);
+  }
+  m->pending.clear();
+}
+
+int npm_profile_kinds(void) { return kKinds; }
+
+npm_status npm_profile_enable(npm_model* m, int enable) {
+  if (!m) return fail(NPM_ERR_INVALID, "null model");
+  DeviceGuard g(m->device);
+  prof_drain(m);
+  m->prof = enable != 0;
+  return NPM_OK;
+}
+
+npm_status npm_profile_reset(npm_model* m) {
+  if (!m) return fail(NPM_ERR_INVALID, "null model");
+  DeviceGuard g(m->device);
+  prof_drain(m);
+  for (int k = 0; k < 16; ++k) { m->prof_ms[k] = 0; m->prof_launches[k] = 0; }
+  return NPM_OK;
+}
+
+npm_status npm_profile_read(npm_model* m, int kind, const char** name, int64_t* launches, double* total_ms) {
+  if (!m || kind < 0 || kind >= kKinds) return fail(NPM_ERR_INVALID, "bad argument");
+  DeviceGuard g(m->device);
+  prof_drain(m);
+  if (name) *name = kKindNames[kind];
+  if (launches) *launches = m->prof_launches[kind];
+  if (total_ms) *total_ms = m->prof_ms[kind];
+  return NPM_OK;
+}
+
+npm_status npm_get_buffer(npm_model* m, npm_buffer which, float* dst, int64_t count, void* stream) {
+  if (!m || (int)which < 0 || (int)which > 4 || !dst) return fail(NPM_ERR_INVALID, "bad argument");
+  if (count != m->n_total) return fail(NPM_ERR_INVALID, "count must equal n_mlp + n_grid");
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(dst, m->buf[which], count * sizeof(float), cudaMemcpyDefault, st));
+  if (Stager::kind(dst) != 2) CUDA_TRY(cudaStreamSynchronize(st));
+  return NPM_OK;
+}
+
+npm_status npm_set_buffer(npm_model* m, npm_buffer which, const float* src, int64_t count, void* stream) {
+  if (!m || (int)which < 0 || (int)which > 4 || !src) return fail(NPM_ERR_INVALID, "bad argument");
+  if (count != m->n_total) return fail(NPM_ERR_INVALID, "count must equal n_mlp + n_grid");
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(m->buf[which], src, count * sizeof(float), cudaMemcpyDefault, st));
+  if (Stager::kind(src) != 2) CUDA_TRY(cudaStreamSynchronize(st));
+  return NPM_OK;
+}
+
+// ---------------------------------------------------------------------------
+npm_status npm_encode(npm_model* m, const npm_query* q, int use_ema, float* feat, void* stream) {
+  if (!m || !query_ok(m, q) || (q->n > 0 && !feat)) return fail(NPM_ERR_INVALID, "bad argument");
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const int LF = m->cfg.n_levels * m->cfg.n_features;
+  float* f = s.out(feat, (size_t)LF * q->n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  QueryArgs a;
+  fill_query_args(m, d, use_ema, a);
+  a.params += m->n_mlp;  // grid section
+  a.feat = f;
+  npm_status r = check_launch(m, timed(m, kKEncode, st, [&] { return launch_encode(m->cfg.n_levels, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+npm_status npm_encode_debug(npm_model* m, const npm_query* q, uint32_t* idx, float* w, void* stream) {
+  if (!m || !query_ok(m, q)) return fail(NPM_ERR_INVALID, "bad argument");
+  if (q->n == 0 || (!idx && !w)) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const size_t cnt = (size_t)m->cfg.n_levels * 8 * q->n;
+  uint32_t* di = s.out(idx, cnt);
+  float* dw = s.out(w, cnt);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  QueryArgs a;
+  fill_query_args(m, d, 0, a);
+  a.params += m->n_mlp;
+  a.dbg_idx = di;
+  a.dbg_w = dw;
+  npm_status r = check_launch(m, timed(m, kKEncode, st, [&] { return launch_encode(m->cfg.n_levels, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+npm_status npm_decode(npm_model* m, const npm_query* q, const float* feat, int use_ema, float* raw,
+                      float* lambda, float* kappa, float* mu, void* stream) {
+  if (!m || !query_ok(m, q)) return fail(NPM_ERR_INVALID, "bad argument");
+  if (feat && m->cfg.mode == NPM_PRODUCT) return fail(NPM_ERR_INVALID, "feat input is radiance-mode only");
+  if (q->n == 0 || (!raw && !lambda && !kappa && !mu)) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const size_t n = (size_t)q->n, K = (size_t)m->cfg.n_lobes;
+  const float* fi = s.in(feat, (size_t)m->cfg.n_levels * m->cfg.n_features * n);
+  QueryArgs a;
+  fill_query_args(m, d, use_ema, a);
+  a.feat_in = fi;
+  a.raw = s.out(raw, 4 * K * n);
+  a.lambda = s.out(lambda, K * n);
+  a.kappa = s.out(kappa, K * n);
+  a.mu = s.out(mu, 3 * K * n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query(m->shape, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+npm_status npm_pdf(npm_model* m, const npm_query* q, const float* wix, const float* wiy, const float* wiz,
+                   int use_ema, float* pdf, void* stream) {
+  if (!m || !query_ok(m, q) || (q->n > 0 && (!wix || !wiy || !wiz || !pdf)))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const size_t n = (size_t)q->n;
+  QueryArgs a;
+  fill_query_args(m, d, use_ema, a);
+  a.wx = s.in(wix, n); a.wy = s.in(wiy, n); a.wz = s.in(wiz, n);
+  a.pdf = s.out(pdf, n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query(m->shape, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t seed, uint64_t offset,
+                      int use_ema, float* wix, float* wiy, float* wiz, float* pdf, const float* qx,
+                      const float* qy, const float* qz, float* pdf_q, void* stream) {
+  if (!m || !query_ok(m, q) || (q->n > 0 && (!wix || !wiy || !wiz || !pdf)))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  const bool fused = qx && qy && qz && pdf_q;
+  if ((qx || qy || qz || pdf_q) && !fused) return fail(NPM_ERR_INVALID, "fused query needs qx, qy, qz, pdf_q");
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const size_t n = (size_t)q->n;
+  QueryArgs a;
+  fill_query_args(m, d, use_ema, a);
+  a.do_sample = 1;
+  a.u = s.in(u, 3 * n);
+  a.seed = seed;
+  a.offset = offset;
+  if (fused) {
+    a.wx = s.in(qx, n); a.wy = s.in(qy, n); a.wz = s.in(qz, n);
+    a.pdf = s.out(pdf_q, n);
+  }
+  a.sx = s.out(wix, n); a.sy = s.out(wiy, n); a.sz = s.out(wiz, n); a.spdf = s.out(pdf, n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query(m->shape, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+// ---------------------------------------------------------------------------
+static npm_status read_stats(npm_model* m, cudaStream_t st, npm_step_stats* out, bool train_part, bool opt_part) {
+  double ds[2];
+  unsigned long long dc[4];
+  CUDA_TRY(cudaMemcpyAsync(ds, m->dstats, sizeof(ds), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(dc, m->dcount, sizeof(dc), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (train_part) {
+    out->loss_proxy = ds[0];
+    out->n_used = (int64_t)dc[0];
+    out->n_zero_target = (int64_t)dc[1];
+    out->n_dropped = (int64_t)dc[2];
+  }
+  if (opt_part) {
+    out->grad_norm_sq = ds[1];
+    out->n_nonfinite_grad = (int64_t)dc[3];
+  }
+  return NPM_OK;
+}
+
+static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
+                             const float* wiz, const float* target, int channels, const float* spdf,
+                             int64_t n_global, cudaStream_t st, Stager& s) {
+  const size_t n = (size_t)q->n;
+  npm_query d;
+  stage_query(s, m, q, d);
+  TrainArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n = q->n;
+  a.px = d.px; a.py = d.py; a.pz = d.pz;
+  a.wox = d.wox; a.woy = d.woy; a.woz = d.woz; a.nx = d.nx; a.ny = d.ny; a.nz = d.nz; a.rough = d.rough;
+  a.wx = s.in(wix, n); a.wy = s.in(wiy, n); a.wz = s.in(wiz, n);
+  a.target = s.in(target, (size_t)channels * n);
+  a.channels = channels;
+  a.spdf = s.in(spdf, n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  a.inv_n_global = 1.0 / (double)n_global;
+  a.params = m->buf[NPM_BUF_PARAMS];
+  a.grads = m->buf[NPM_BUF_GRADS];
+  a.grid = m->grid;
+  a.log_kmin = logf(m->cfg.kappa_min);
+  a.log_kmax = logf(m->cfg.kappa_max);
+  a.stats = m->dstats;
+  a.counters = m->dcount;
+  // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
+  const NetShape& sh = m->shape;
+  const size_t rows = (size_t)sh.n_in + (size_t)(sh.n_layers - 1) * sh.width  // acts
+                      + (size_t)(sh.n_layers - 1) * sh.width + sh.n_out;       // deltas
+  CUDA_TRY(m->scratch_train.ensure(rows * n * sizeof(float)));
+  float* p = static_cast<float*>(m->scratch_train.p);
+  a.act[0] = p; p += (size_t)sh.n_in * n;
+  for (int k = 1; k < sh.n_layers; ++k) { a.act[k] = p; p += (size_t)sh.width * n; }
+  for (int k = 0; k < sh.n_layers - 1; ++k) { a.delta[k] = p; p += (size_t)sh.width * n; }
+  a.delta[sh.n_layers - 1] = p;
+  CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
+  CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+  npm_status r;
+  if ((r = check_launch(m, timed(m, kKTrainFwd, st, [&] { return launch_train_forward(sh, a, m->num_sms, st); }))) != NPM_OK) return r;
+  if ((r = check_launch(m, timed(m, kKTrainBwd, st, [&] { return launch_train_backward(sh, a, m->num_sms, st); }))) != NPM_OK) return r;
+  if ((r = check_launch(m, timed(m, kKWgrad, st, [&] { return launch_weight_grads(sh, a, m->num_sms, st); }))) != NPM_OK) return r;
+  return NPM_OK;
+}
+
+static bool train_args_ok(const npm_model* m, const npm_query* q, const float* wix, const float* wiy,
+                          const float* wiz, const float* target, int channels, const float* spdf, int64_t n_global) {
+  if (!m || !query_ok(m, q)) return false;
+  if (channels != 1 && channels != 3) return false;
+  if (q->n > 0 && (!wix || !wiy || !wiz || !target || !spdf)) return false;
+  if (n_global < q->n || n_global <= 0) return false;
+  return true;
+}
+
+npm_status npm_accumulate_grads(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
+                                const float* wiz, const float* target, int channels, const float* spdf,
+                                int64_t n_global, npm_step_stats* stats, void* stream) {
+  if (!train_args_ok(m, q, wix, wiy, wiz, target, channels, spdf, n_global))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_status r = accumulate(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st, s);
+  if (r != NPM_OK) return r;
+  if (stats) return read_stats(m, st, stats, true, false);
+  return NPM_OK;
+}
+
+static npm_status optimizer(npm_model* m, cudaStream_t st) {
+  m->t += 1;
+  const npm_config& c = m->cfg;
+  AdamArgs a;
+  a.n_mlp = m->n_mlp;
+  a.n_total = m->n_total;
+  a.p = m->buf[NPM_BUF_PARAMS]; a.g = m->buf[NPM_BUF_GRADS]; a.m = m->buf[NPM_BUF_ADAM_M];
+  a.v = m->buf[NPM_BUF_ADAM_V]; a.e = m->buf[NPM_BUF_EMA];
+  a.lr = c.lr; a.beta1 = c.beta1; a.beta2 = c.beta2; a.eps = c.adam_eps; a.decay = c.ema_decay;
+  a.c1 = (float)(1.0 / (1.0 - std::pow((double)c.beta1, (double)m->t)));
+  a.c2 = (float)(1.0 / (1.0 - std::pow((double)c.beta2, (double)m->t)));
+  a.gnorm = m->dstats + 1;
+  a.nonfinite = m->dcount + 3;
+  CUDA_TRY(cudaMemsetAsync(m->dstats + 1, 0, sizeof(double), st));
+  CUDA_TRY(cudaMemsetAsync(m->dcount + 3, 0, sizeof(unsigned long long), st));
+  return check_launch(m, timed(m, kKAdam, st, [&] { return launch_adam(a, m->num_sms, st); }));
+}
+
+npm_status npm_optimizer_step(npm_model* m, npm_step_stats* stats, void* stream) {
+  if (!m) return fail(NPM_ERR_INVALID, "null model");
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  npm_status r = optimizer(m, st);
+  if (r != NPM_OK) return r;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    return read_stats(m, st, stats, false, true);
+  }
+  return NPM_OK;
+}
+
+npm_status npm_train_step(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
+                          const float* wiz, const float* target, int channels, const float* spdf,
+                          int64_t n_global, npm_step_stats* stats, void* stream) {
+  if (!train_args_ok(m, q, wix, wiy, wiz, target, channels, spdf, n_global))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (stats) memset(stats, 0, sizeof(*stats));
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (q->n > 0) {
+    std::lock_guard<std::mutex> lk(m->stage_mu);
+    Stager s{m, st};
+    npm_status r = accumulate(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st, s);
+    if (r != NPM_OK) return r;
+  } else {
+    CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+  }
+  npm_status r = optimizer(m, st);
+  if (r != NPM_OK) return r;
+  if (stats) return read_stats(m, st, stats, true, true);
+  return NPM_OK;
+}
+
+}  // extern "C"

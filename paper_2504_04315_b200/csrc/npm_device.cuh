@@ -1,0 +1,253 @@
+// npm_device.cuh -- device building blocks of the NPM hot path (sm_100a).
+//
+// Citations: P:n = PAPER.md line n (equation / section named); C-xx = reading
+// in DESIGN.md.  Nothing here is shared with oracle/ (independent code).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace npm {
+
+constexpr int kMaxLevels = 16;
+constexpr int kMaxLobes = 16;
+constexpr float kPi = 3.14159265358979323846f;
+constexpr float kTwoPi = 6.28318530717958647692f;
+constexpr float kUMax = (float)(1.0 - 1e-6);  // S:163 clamp, C-O1
+constexpr float kVFloor = 1e-30f;             // S:125, C-O13
+
+// Grid embedding descriptor (Eq. 13; C-A3/C-A4).
+struct GridDesc {
+  int L;
+  uint32_t hashed_mask;        // bit l set: level l uses the spatial hash (C-A4)
+  int res[kMaxLevels];         // D_l lattice points per axis
+  uint32_t tsize[kMaxLevels];  // entries in level l (D^3 or T)
+  int64_t off[kMaxLevels];     // first entry of level l (entries of F = 4 floats)
+  float lo[3], inv[3];         // AABB min, fl32(1/(hi - lo)) (C-O1)
+};
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11), C-O11.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k.x += W0; k.y += W1; }
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+// u_j = (out_j >> 8) * 2^-24, counter = (lo32(i+offset), hi32(i+offset), 0, 0).
+__device__ __forceinline__ float3 philox_uniforms(uint64_t seed, uint64_t ctr) {
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), 0u, 0u),
+                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const float s = 5.9604644775390625e-08f;  // 2^-24
+  return make_float3((float)(o.x >> 8) * s, (float)(o.y >> 8) * s, (float)(o.z >> 8) * s);
+}
+
+// ---------------------------------------------------------------------------
+// Pinned fp32 cell-index sequence (C-O1, C-O3; C-A1): no FMA contraction.
+__device__ __forceinline__ float normalize_axis(float x, float lo, float inv) {
+  const float u = __fmul_rn(__fsub_rn(x, lo), inv);
+  return fminf(fmaxf(u, 0.0f), kUMax);
+}
+
+__device__ __forceinline__ void cell_axis(float u, int d, int& i, float& f) {
+  const float s = __fmul_rn(u, (float)(d - 1));
+  int ii = (int)floorf(s);
+  const int hi = d > 2 ? d - 2 : 0;
+  ii = ii < 0 ? 0 : (ii > hi ? hi : ii);
+  i = ii;
+  f = __fsub_rn(s, (float)ii);
+}
+
+// Corner entry index (C-O4): dense Px + D(Py + D Pz); hashed (C-A4 convention,
+// not in the paper) (Px*1 ^ Py*2654435761 ^ Pz*805459861) & (T - 1).
+__device__ __forceinline__ uint32_t corner_index(uint32_t px, uint32_t py, uint32_t pz, int d,
+                                                 uint32_t tsize, bool hashed) {
+  if (!hashed) return px + (uint32_t)d * (py + (uint32_t)d * pz);
+  return (px ^ (py * 2654435761u) ^ (pz * 805459861u)) & (tsize - 1u);
+}
+
+// The 8 corners + trilinear weights of level l (Eq. 13 "eight corners",
+// trilinear per C-A2), corner c = cx + 2 cy + 4 cz.
+struct LevelCorners {
+  uint32_t idx[8];
+  float w[8];
+};
+
+__device__ __forceinline__ void level_corners(const GridDesc& g, int l, float ux, float uy, float uz,
+                                              LevelCorners& lc) {
+  const int d = g.res[l];
+  int ix, iy, iz;
+  float fx, fy, fz;
+  cell_axis(ux, d, ix, fx);
+  cell_axis(uy, d, iy, fy);
+  cell_axis(uz, d, iz, fz);
+  const bool hashed = (g.hashed_mask >> l) & 1u;
+  const float gx[2] = {1.0f - fx, fx}, gy[2] = {1.0f - fy, fy}, gz[2] = {1.0f - fz, fz};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+    lc.idx[c] = corner_index((uint32_t)(ix + cx), (uint32_t)(iy + cy), (uint32_t)(iz + cz), d, g.tsize[l], hashed);
+    lc.w[c] = gx[cx] * gy[cy] * gz[cz];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Real orthonormal SH, 4 bands, l-major / m ascending, no Condon-Shortley
+// phase (C-A20, C-O6).  Cartesian polynomial forms.
+__device__ __forceinline__ void sh4(float x, float y, float z, float* o) {
+  const float xx = x * x, yy = y * y, zz = z * z;
+  o[0] = 0.28209479177387814f;
+  o[1] = 0.48860251190291992f * y;
+  o[2] = 0.48860251190291992f * z;
+  o[3] = 0.48860251190291992f * x;
+  o[4] = 1.0925484305920792f * x * y;
+  o[5] = 1.0925484305920792f * y * z;
+  o[6] = 0.31539156525252005f * (3.0f * zz - 1.0f);
+  o[7] = 1.0925484305920792f * x * z;
+  o[8] = 0.54627421529603959f * (xx - yy);
+  o[9] = 0.59004358992664352f * y * (3.0f * xx - yy);
+  o[10] = 2.8906114426405538f * x * y * z;
+  o[11] = 0.45704579946446572f * y * (5.0f * zz - 1.0f);
+  o[12] = 0.3731763325901154f * z * (5.0f * zz - 3.0f);
+  o[13] = 0.45704579946446572f * x * (5.0f * zz - 1.0f);
+  o[14] = 1.4453057213202769f * z * (xx - yy);
+  o[15] = 0.59004358992664352f * x * (xx - 3.0f * yy);
+}
+
+// ---------------------------------------------------------------------------
+// Table 1 mappings, C-O8: raw block layout [l' | k' | t' | p'] (C-A6).
+template <int K>
+struct Mixture {
+  float lam[K], kap[K], mx[K], my[K], mz[K];
+};
+
+template <int K>
+__device__ __forceinline__ void activate(const float* raw, float log_kmin, float log_kmax, Mixture<K>& m) {
+  float mx = raw[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) mx = fmaxf(mx, raw[i]);
+  float sum = 0.0f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) { m.lam[i] = expf(raw[i] - mx); sum += m.lam[i]; }
+  const float inv = 1.0f / sum;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    m.lam[i] *= inv;
+    m.kap[i] = expf(fminf(fmaxf(raw[K + i], log_kmin), log_kmax));
+    const float th = 1.0f / (1.0f + expf(-raw[2 * K + i]));
+    const float ph = 1.0f / (1.0f + expf(-raw[3 * K + i]));
+    float st, ct, sp, cp;
+    sincospif(th, &st, &ct);          // sin(pi theta), cos(pi theta)
+    sincospif(2.0f * ph, &sp, &cp);   // sin(2 pi phi), cos(2 pi phi)
+    m.mx[i] = st * cp;                // C-A7: polar angle from +z, azimuth from +x
+    m.my[i] = st * sp;
+    m.mz[i] = ct;
+  }
+}
+
+// Stable Eq. 3 (C-O9): kappa / (2 pi (1 - e^{-2 kappa})) exp(-kappa |mu - w|^2 / 2).
+__device__ __forceinline__ float lobe_pdf(float kap, float mx, float my, float mz, float wx, float wy, float wz) {
+  const float dx = mx - wx, dy = my - wy, dz = mz - wz;
+  const float d2 = dx * dx + dy * dy + dz * dz;
+  return kap / (kTwoPi * (-expm1f(-2.0f * kap))) * expf(-0.5f * kap * d2);
+}
+
+template <int K>
+__device__ __forceinline__ float mixture_pdf(const Mixture<K>& m, float wx, float wy, float wz) {
+  float v = 0.0f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) v += m.lam[i] * lobe_pdf(m.kap[i], m.mx[i], m.my[i], m.mz[i], wx, wy, wz);
+  return v;
+}
+
+// Jakob 2012 stable vMF inversion in the Duff et al. ONB (C-O10).
+template <int K>
+__device__ __forceinline__ void mixture_sample(const Mixture<K>& m, float u1, float u2, float u3,
+                                               float& wx, float& wy, float& wz) {
+  // i* = min{i : u1 < C_i}, C_i = sum_{j<=i} lambda_j; K-1 if none (C-A17)
+  int sel = K - 1;
+  bool found = false;
+  float cdf = 0.0f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    cdf += m.lam[i];
+    if (!found && u1 < cdf) { sel = i; found = true; }
+  }
+  float kap = m.kap[0], mux = m.mx[0], muy = m.my[0], muz = m.mz[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i)
+    if (sel == i) { kap = m.kap[i]; mux = m.mx[i]; muy = m.my[i]; muz = m.mz[i]; }
+  // delta = -log(u2 + (1 - u2) e^{-2 kappa}) / kappa  (Jakob 2012, C-O10), evaluated in fp32
+  // in whichever of two equal forms is well conditioned: log1p of
+  // x = (1 - u2) expm1(-2 kappa) while 1 + x >= 1/2, else log of 1 + x formed
+  // directly as u2 + (1 - u2) e^{-2 kappa} (keeps full precision when u2 -> 0).
+  const float x = (1.0f - u2) * expm1f(-2.0f * kap);
+  const float lg = x > -0.5f ? log1pf(x) : logf(u2 + (1.0f - u2) * expf(-2.0f * kap));
+  const float delta = fminf(-lg / kap, 2.0f);
+  // 2 - delta = log1p(u2 expm1(2 kappa)) / kappa, the same quantity evaluated so
+  // that it stays accurate where delta -> 2 (u2 -> 0): r = sqrt(delta (2 - delta))
+  // has an infinite derivative there.  expm1(2 kappa) overflows only for
+  // kappa > ~44, where delta is near 2 only at u2 = 0 (then 2 - delta = 0).
+  const float e2k = expm1f(2.0f * kap);
+  const float eps = isfinite(e2k) ? fminf(log1pf(u2 * e2k) / kap, 2.0f) : 2.0f - delta;
+  const float w = 1.0f - delta;
+  const float r = sqrtf(fmaxf(delta * eps, 0.0f));
+  const float s = copysignf(1.0f, muz);
+  const float a = -1.0f / (s + muz);
+  const float b = mux * muy * a;
+  const float t1x = 1.0f + s * mux * mux * a, t1y = s * b, t1z = -s * mux;
+  const float t2x = b, t2y = s + muy * muy * a, t2z = -muy;
+  float sp, cp;
+  sincospif(2.0f * u3, &sp, &cp);
+  wx = w * mux + r * (cp * t1x + sp * t2x);
+  wy = w * muy + r * (cp * t1y + sp * t2y);
+  wz = w * muz + r * (cp * t1z + sp * t2z);
+}
+
+// Eq. 9 head (C-O13): d loss / d raw for one record, multiplied by s.
+// Returns log max(V, 1e-30).
+template <int K>
+__device__ __forceinline__ float grad_head(const float* raw, float log_kmin, float log_kmax,
+                                           float wx, float wy, float wz, float s, float* draw) {
+  Mixture<K> m;
+  activate<K>(raw, log_kmin, log_kmax, m);
+  float v[K];
+  float V = 0.0f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    v[i] = lobe_pdf(m.kap[i], m.mx[i], m.my[i], m.mz[i], wx, wy, wz);
+    V += m.lam[i] * v[i];
+  }
+  const float Vb = fmaxf(V, kVFloor);
+  const float invV = 1.0f / Vb;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const float gam = m.lam[i] * v[i] * invV;
+    draw[i] = s * (gam - m.lam[i]);
+    const float kap = m.kap[i];
+    const float kr = raw[K + i];
+    const float dx = m.mx[i] - wx, dy = m.my[i] - wy, dz = m.mz[i] - wz;
+    const float d2 = dx * dx + dy * dy + dz * dz;
+    const float em = -expm1f(-2.0f * kap);
+    float dk = s * gam * (1.0f - kap * 0.5f * d2 - 2.0f * kap * expf(-2.0f * kap) / em);
+    draw[K + i] = (kr < log_kmin || kr > log_kmax) ? 0.0f : dk;
+    const float th = 1.0f / (1.0f + expf(-raw[2 * K + i]));
+    const float ph = 1.0f / (1.0f + expf(-raw[3 * K + i]));
+    float st, ct, sp, cp;
+    sincospif(th, &st, &ct);
+    sincospif(2.0f * ph, &sp, &cp);
+    const float wdth = kPi * (ct * cp * wx + ct * sp * wy - st * wz);
+    const float wdph = kTwoPi * (-st * sp * wx + st * cp * wy);
+    const float sgk = s * gam * kap;
+    draw[2 * K + i] = sgk * wdth * th * (1.0f - th);
+    draw[3 * K + i] = sgk * wdph * ph * (1.0f - ph);
+  }
+  return logf(Vb);
+}
+
+}  // namespace npm

@@ -1,0 +1,79 @@
+// npm_kernels.cuh -- launch interface between the C ABI (npm_capi.cu) and the
+// sm_100a kernels.  Internal header: not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "npm_device.cuh"
+
+namespace npm {
+
+// Decoder shape (C-A5): n_in -> width (x n_layers-1) -> 4K.
+struct NetShape {
+  int n_in, width, n_layers, n_out;  // n_out = 4K
+  bool product;
+};
+
+struct QueryArgs {
+  int64_t n;
+  const float *px, *py, *pz, *wox, *woy, *woz, *nx, *ny, *nz, *rough;
+  const float* params;      // live or EMA flat parameter buffer
+  GridDesc grid;
+  float log_kmin, log_kmax;
+  // encode-only outputs
+  float* feat;              // [L*F][n]
+  uint32_t* dbg_idx;        // [L][8][n]
+  float* dbg_w;             // [L][8][n]
+  // decode
+  const float* feat_in;     // optional [L*F][n] input instead of G(x)
+  float *raw, *lambda, *kappa, *mu;
+  // pdf at caller directions
+  const float *wx, *wy, *wz;
+  float* pdf;
+  // sampling
+  int do_sample;
+  const float* u;           // [3][n] or NULL -> Philox
+  uint64_t seed, offset;
+  float *sx, *sy, *sz, *spdf;
+};
+
+struct TrainArgs {
+  int64_t n;
+  const float *px, *py, *pz, *wox, *woy, *woz, *nx, *ny, *nz, *rough;
+  const float *wx, *wy, *wz;
+  const float* target;      // [C][n]
+  int channels;
+  const float* spdf;        // p~
+  double inv_n_global;
+  const float* params;
+  float* grads;
+  GridDesc grid;
+  float log_kmin, log_kmax;
+  // scratch, feature-major [rows][n]
+  float* act[3];            // inputs of layer k: z, h1, h2
+  float* delta[3];          // d loss / d pre-activation of layer k
+  double* stats;            // [0] loss, [1] unused, then int counters as double
+  unsigned long long* counters;  // [0] used, [1] zero, [2] dropped
+};
+
+struct AdamArgs {
+  int64_t n_mlp, n_total;
+  float *p, *g, *m, *v, *e;
+  float lr, beta1, beta2, eps, decay, c1, c2;  // c1 = 1/(1-b1^t), c2 = 1/(1-b2^t)
+  double* gnorm;
+  unsigned long long* nonfinite;
+};
+
+bool shape_supported(const NetShape& s);
+size_t weight_smem_bytes(const NetShape& s);
+
+// Every launcher returns the number of kernels launched (>= 1) or -1 on error.
+int launch_query(const NetShape& s, const QueryArgs& a, int num_sms, cudaStream_t st);
+int launch_encode(int L, const QueryArgs& a, int num_sms, cudaStream_t st);  // a.params = grid section
+int launch_train_forward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
+int launch_train_backward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
+int launch_weight_grads(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
+int launch_adam(const AdamArgs& a, int num_sms, cudaStream_t st);
+int launch_init_params(float* p, int64_t n_mlp, int64_t n_total, const NetShape& s, uint64_t seed,
+                       cudaStream_t st);
+
+}  // namespace npm

@@ -1,0 +1,87 @@
+"""Data-parallel training driver (BASELINE north_star).
+
+Training shards the record batch contiguously over ranks; every rank scales
+its records by 1/N_global (Eq. 9's 1/N over the whole batch, C-A13) so the
+global gradient is the plain SUM of the per-rank gradients -- the only
+exchange step of the method.  One optimisation step:
+
+    accumulate_grads(local shard, N_global)   # Eq. 9 -> backprop -> scatter (CUDA)
+    all_reduce(GRADS, SUM)                    # NCCL over NVLink/NVSwitch (world > 1)
+    optimizer_step()                          # Adam + EMA (CUDA), identical on every rank
+
+Every rank receives the same reduced bytes and runs the same deterministic
+optimiser kernel, so the replicas stay bitwise identical (no parameter
+broadcast needed after initialisation).  Queries (encode/decode/pdf/sample)
+shard trivially and need no collective.
+
+The driver is backend-agnostic: ``model`` is any object exposing
+``accumulate_grads_ptrs`` / ``optimizer_step`` / ``grad_tensor`` (the CUDA
+``npm.Model`` via ``NpmTrainer`` below; the CPU tests plug in an oracle-backed
+stand-in to exercise the sharding and reduction logic over gloo).
+"""
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_global, rank, world):
+    """Contiguous shard [start, end) of rank in a batch of n_global records;
+    the first n_global % world ranks get one extra record."""
+    base, rem = divmod(int(n_global), int(world))
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+class NpmTrainer:
+    """Adapter of the C-ABI model to the DataParallel protocol."""
+
+    def __init__(self, model):
+        from . import npm
+        self.npm = npm
+        self.m = model
+        self._grads = None
+
+    def accumulate(self, q, wi, target, spdf, n_global, want_stats):
+        npm = self.npm
+        channels = target.shape[0] if target.dim() == 2 else 1
+        return npm.npm_accumulate_grads(self.m.h, q, wi[0], wi[1], wi[2], target, channels, spdf, n_global,
+                                        want_stats, self.m._stream())
+
+    def optimizer_step(self, want_stats):
+        return self.npm.npm_optimizer_step(self.m.h, want_stats, self.m._stream())
+
+    def grad_tensor(self):
+        if self._grads is None:
+            self._grads = self.m.buffer_view(self.npm.BUF_GRADS)
+        return self._grads
+
+
+class DataParallel:
+    def __init__(self, model, world=None, group=None):
+        self.t = model if hasattr(model, "accumulate") else NpmTrainer(model)
+        self.world = world if world is not None else (dist.get_world_size() if dist.is_initialized() else 1)
+        self.group = group
+
+    def allreduce_grads(self):
+        if self.world > 1:
+            dist.all_reduce(self.t.grad_tensor(), op=dist.ReduceOp.SUM, group=self.group)
+
+    def train_step(self, q, wi, target, spdf, n_local=None, n_global=None, want_stats=False):
+        """One data-parallel optimisation step on this rank's shard.
+        n_global defaults to world * n_local (equal shards)."""
+        if n_global is None:
+            n_global = self.world * (n_local if n_local is not None else q.n)
+        st = self.t.accumulate(q, wi, target, spdf, n_global, want_stats)
+        self.allreduce_grads()
+        st2 = self.t.optimizer_step(want_stats)
+        if not want_stats:
+            return None
+        st = dict(st)
+        st["grad_norm_sq"] = st2["grad_norm_sq"]
+        st["n_nonfinite_grad"] = st2["n_nonfinite_grad"]
+        if self.world > 1:
+            v = torch.tensor([st["loss_proxy"], st["n_used"], st["n_zero_target"], st["n_dropped"]],
+                             dtype=torch.float64, device=self.t.grad_tensor().device)
+            dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
+            st["loss_proxy"], st["n_used"], st["n_zero_target"], st["n_dropped"] = (
+                v[0].item(), int(v[1].item()), int(v[2].item()), int(v[3].item()))
+        return st

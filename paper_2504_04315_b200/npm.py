@@ -1,0 +1,421 @@
+"""Thin Python binding of the C ABI in include/npm.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels of libnpm.so; this module
+only converts arrays to pointers.  The functions keep the C names
+(npm_create, npm_encode, npm_decode, npm_pdf, npm_sample, npm_train_step, ...);
+``Model`` is a small convenience wrapper over them that allocates outputs with
+torch (device memory and streams are PyTorch's job, nothing else is).
+
+Arrays may be torch tensors (CUDA or CPU) or numpy arrays: float32,
+C-contiguous.  CPU arrays are staged by the library itself (npm.h "POINTERS MAY
+BE HOST OR DEVICE").  There is no CPU fallback: if libnpm.so is missing or
+fails to load, importing this module raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnpm.so")
+
+RADIANCE, PRODUCT = 0, 1
+BUF_PARAMS, BUF_GRADS, BUF_ADAM_M, BUF_ADAM_V, BUF_EMA = range(5)
+STATUS = {0: "NPM_OK", 1: "NPM_ERR_INVALID", 2: "NPM_ERR_CUDA", 3: "NPM_ERR_NCCL", 4: "NPM_ERR_OOM",
+          5: "NPM_ERR_STATE"}
+
+
+class NpmError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+
+
+class npm_config(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("n_lobes", ctypes.c_int32), ("n_levels", ctypes.c_int32),
+                ("n_features", ctypes.c_int32), ("base_res", ctypes.c_int32), ("max_res", ctypes.c_int32),
+                ("log2_hashmap", ctypes.c_int32), ("mlp_linear_layers", ctypes.c_int32),
+                ("mlp_width", ctypes.c_int32), ("sh_bands", ctypes.c_int32),
+                ("aabb_lo", ctypes.c_float * 3), ("aabb_hi", ctypes.c_float * 3),
+                ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("adam_eps", ctypes.c_float), ("ema_decay", ctypes.c_float),
+                ("kappa_min", ctypes.c_float), ("kappa_max", ctypes.c_float),
+                ("init_seed", ctypes.c_uint64)]
+
+
+_FP = ctypes.POINTER(ctypes.c_float)
+
+
+class npm_query(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64)] + [(k, ctypes.c_void_p) for k in
+                                          ("px", "py", "pz", "wox", "woy", "woz", "nx", "ny", "nz", "rough")]
+
+
+class npm_step_stats(ctypes.Structure):
+    _fields_ = [("loss_proxy", ctypes.c_double), ("grad_norm_sq", ctypes.c_double),
+                ("n_used", ctypes.c_int64), ("n_zero_target", ctypes.c_int64),
+                ("n_dropped", ctypes.c_int64), ("n_nonfinite_grad", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libnpm.so not built (run __graft_entry__.build() or "
+                          "python paper_2504_04315_b200/build.py): %s" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH)
+    V, I64, I32, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64
+    M = ctypes.c_void_p
+    sig = {
+        "npm_default_config": (None, [ctypes.POINTER(npm_config)]),
+        "npm_create": (I32, [ctypes.POINTER(npm_config), I32, ctypes.POINTER(M)]),
+        "npm_destroy": (I32, [M]),
+        "npm_param_count": (I32, [M, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "npm_level_info": (I32, [M, V, V]),
+        "npm_get_buffer": (I32, [M, I32, V, I64, V]),
+        "npm_set_buffer": (I32, [M, I32, V, I64, V]),
+        "npm_get_step": (I32, [M, ctypes.POINTER(I64)]),
+        "npm_set_step": (I32, [M, I64]),
+        "npm_encode": (I32, [M, ctypes.POINTER(npm_query), I32, V, V]),
+        "npm_encode_debug": (I32, [M, ctypes.POINTER(npm_query), V, V, V]),
+        "npm_decode": (I32, [M, ctypes.POINTER(npm_query), V, I32, V, V, V, V, V]),
+        "npm_pdf": (I32, [M, ctypes.POINTER(npm_query), V, V, V, I32, V, V]),
+        "npm_sample": (I32, [M, ctypes.POINTER(npm_query), V, U64, U64, I32, V, V, V, V, V, V, V, V, V]),
+        "npm_train_step": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
+                                 ctypes.POINTER(npm_step_stats), V]),
+        "npm_accumulate_grads": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
+                                       ctypes.POINTER(npm_step_stats), V]),
+        "npm_optimizer_step": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
+        "npm_buffer_device_ptr": (I32, [M, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(I64)]),
+        "npm_launch_count": (I64, [M]),
+        "npm_profile_kinds": (I32, []),
+        "npm_profile_enable": (I32, [M, I32]),
+        "npm_profile_reset": (I32, [M]),
+        "npm_profile_read": (I32, [M, I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(I64),
+                                   ctypes.POINTER(ctypes.c_double)]),
+        "npm_last_error": (ctypes.c_char_p, []),
+        "npm_version": (I32, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+
+# ---------------------------------------------------------------------------
+# raw C-name wrappers
+
+
+def _check(st):
+    if st != 0:
+        raise NpmError(st, _lib.npm_last_error().decode())
+
+
+def _ptr(x):
+    """Pointer of a float32/uint32 C-contiguous torch tensor or numpy array."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    if not x.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return x.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    return ctypes.c_void_p(stream)
+
+
+def npm_default_config(**overrides):
+    c = npm_config()
+    _lib.npm_default_config(ctypes.byref(c))
+    for k, v in overrides.items():
+        if k in ("aabb_lo", "aabb_hi"):
+            setattr(c, k, (ctypes.c_float * 3)(*v))
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def npm_create(cfg, device=0):
+    h = ctypes.c_void_p()
+    _check(_lib.npm_create(ctypes.byref(cfg), int(device), ctypes.byref(h)))
+    return h
+
+
+def npm_destroy(h):
+    _check(_lib.npm_destroy(h))
+
+
+def make_query(n, px, py, pz, wox=None, woy=None, woz=None, nx=None, ny=None, nz=None, rough=None):
+    q = npm_query()
+    q.n = int(n)
+    for k, v in zip(("px", "py", "pz", "wox", "woy", "woz", "nx", "ny", "nz", "rough"),
+                    (px, py, pz, wox, woy, woz, nx, ny, nz, rough)):
+        setattr(q, k, _ptr(v))
+    return q
+
+
+def npm_encode(h, q, use_ema, feat, stream=None):
+    _check(_lib.npm_encode(h, ctypes.byref(q), int(use_ema), _ptr(feat), _stream(stream)))
+
+
+def npm_encode_debug(h, q, idx, w, stream=None):
+    _check(_lib.npm_encode_debug(h, ctypes.byref(q), _ptr(idx), _ptr(w), _stream(stream)))
+
+
+def npm_decode(h, q, feat, use_ema, raw, lam, kappa, mu, stream=None):
+    _check(_lib.npm_decode(h, ctypes.byref(q), _ptr(feat), int(use_ema), _ptr(raw), _ptr(lam), _ptr(kappa),
+                           _ptr(mu), _stream(stream)))
+
+
+def npm_pdf(h, q, wx, wy, wz, use_ema, pdf, stream=None):
+    _check(_lib.npm_pdf(h, ctypes.byref(q), _ptr(wx), _ptr(wy), _ptr(wz), int(use_ema), _ptr(pdf),
+                        _stream(stream)))
+
+
+def npm_sample(h, q, u, seed, offset, use_ema, wx, wy, wz, pdf, qx=None, qy=None, qz=None, pdf_q=None,
+               stream=None):
+    _check(_lib.npm_sample(h, ctypes.byref(q), _ptr(u), int(seed), int(offset), int(use_ema), _ptr(wx),
+                           _ptr(wy), _ptr(wz), _ptr(pdf), _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q),
+                           _stream(stream)))
+
+
+def npm_train_step(h, q, wx, wy, wz, target, channels, spdf, n_global, want_stats=True, stream=None):
+    st = npm_step_stats() if want_stats else None
+    _check(_lib.npm_train_step(h, ctypes.byref(q), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(target), int(channels),
+                               _ptr(spdf), int(n_global), ctypes.byref(st) if st is not None else None,
+                               _stream(stream)))
+    return st.as_dict() if st is not None else None
+
+
+def npm_accumulate_grads(h, q, wx, wy, wz, target, channels, spdf, n_global, want_stats=True, stream=None):
+    st = npm_step_stats() if want_stats else None
+    _check(_lib.npm_accumulate_grads(h, ctypes.byref(q), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(target),
+                                     int(channels), _ptr(spdf), int(n_global),
+                                     ctypes.byref(st) if st is not None else None, _stream(stream)))
+    return st.as_dict() if st is not None else None
+
+
+def npm_optimizer_step(h, want_stats=True, stream=None):
+    st = npm_step_stats() if want_stats else None
+    _check(_lib.npm_optimizer_step(h, ctypes.byref(st) if st is not None else None, _stream(stream)))
+    return st.as_dict() if st is not None else None
+
+
+def npm_param_count(h):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.npm_param_count(h, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def npm_level_info(h, n_levels):
+    res = np.zeros(n_levels, np.int32)
+    ent = np.zeros(n_levels, np.int64)
+    _check(_lib.npm_level_info(h, res.ctypes.data, ent.ctypes.data))
+    return res, ent
+
+
+def npm_get_buffer(h, which, dst, stream=None):
+    _check(_lib.npm_get_buffer(h, int(which), _ptr(dst), int(dst.numel() if hasattr(dst, "numel") else dst.size),
+                               _stream(stream)))
+
+
+def npm_set_buffer(h, which, src, stream=None):
+    _check(_lib.npm_set_buffer(h, int(which), _ptr(src), int(src.numel() if hasattr(src, "numel") else src.size),
+                               _stream(stream)))
+
+
+def npm_get_step(h):
+    t = ctypes.c_int64()
+    _check(_lib.npm_get_step(h, ctypes.byref(t)))
+    return t.value
+
+
+def npm_set_step(h, t):
+    _check(_lib.npm_set_step(h, int(t)))
+
+
+def npm_buffer_device_ptr(h, which):
+    p, n = ctypes.c_void_p(), ctypes.c_int64()
+    _check(_lib.npm_buffer_device_ptr(h, int(which), ctypes.byref(p), ctypes.byref(n)))
+    return p.value, n.value
+
+
+def npm_launch_count(h):
+    return int(_lib.npm_launch_count(h))
+
+
+def npm_profile_enable(h, on):
+    _check(_lib.npm_profile_enable(h, int(on)))
+
+
+def npm_profile_reset(h):
+    _check(_lib.npm_profile_reset(h))
+
+
+def npm_profile_read(h):
+    """{kernel kind: (launches, total_ms)} since the last reset."""
+    out = {}
+    for k in range(_lib.npm_profile_kinds()):
+        name, n, ms = ctypes.c_char_p(), ctypes.c_int64(), ctypes.c_double()
+        _check(_lib.npm_profile_read(h, k, ctypes.byref(name), ctypes.byref(n), ctypes.byref(ms)))
+        out[name.value.decode()] = (n.value, ms.value)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Convenience wrapper with torch-allocated outputs.
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a library-owned device buffer."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+
+class Model:
+    def __init__(self, device=0, **cfg):
+        import torch
+        self.torch = torch
+        self.cfg = npm_default_config(**cfg)
+        self.device = torch.device("cuda", device)
+        self.h = npm_create(self.cfg, device)
+        self.n_grid, self.n_mlp = npm_param_count(self.h)
+        self.n_params = self.n_grid + self.n_mlp
+        self.K = self.cfg.n_lobes
+        self.L = self.cfg.n_levels
+        self.F = self.cfg.n_features
+        self.product = self.cfg.mode == PRODUCT
+
+    def close(self):
+        if self.h:
+            npm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def _f32(self, x):
+        t = self.torch
+        if x is None:
+            return None
+        if isinstance(x, np.ndarray):
+            x = t.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        return x.to(device=self.device, dtype=t.float32).contiguous()
+
+    def _empty(self, *shape, dtype=None):
+        return self.torch.empty(*shape, device=self.device, dtype=dtype or self.torch.float32)
+
+    def query(self, x, wo=None, nrm=None, rough=None):
+        """x: [3, n]; product mode also wo [3, n], nrm [3, n], rough [n]."""
+        x = self._f32(x)
+        keep = [x]
+        if self.product:
+            wo, nrm, rough = self._f32(wo), self._f32(nrm), self._f32(rough)
+            keep += [wo, nrm, rough]
+            q = make_query(x.shape[1], x[0], x[1], x[2], wo[0], wo[1], wo[2], nrm[0], nrm[1], nrm[2], rough)
+        else:
+            q = make_query(x.shape[1], x[0], x[1], x[2])
+        q._keep = keep
+        return q
+
+    def buffer_view(self, which):
+        """Zero-copy torch view of a model buffer (e.g. GRADS for a collective)."""
+        p, n = npm_buffer_device_ptr(self.h, which)
+        return self.torch.as_tensor(_CudaArray(p, n), device=self.device)
+
+    def get(self, which=BUF_PARAMS):
+        out = self._empty(self.n_params)
+        npm_get_buffer(self.h, which, out, self._stream())
+        return out
+
+    def set(self, which, values):
+        v = self._f32(values)
+        npm_set_buffer(self.h, which, v, self._stream())
+
+    def encode(self, q, use_ema=False):
+        feat = self._empty(self.L * self.F, q.n)
+        npm_encode(self.h, q, use_ema, feat, self._stream())
+        return feat
+
+    def encode_debug(self, q):
+        idx = self._empty(self.L, 8, q.n, dtype=self.torch.int32)
+        w = self._empty(self.L, 8, q.n)
+        npm_encode_debug(self.h, q, idx, w, self._stream())
+        return idx, w
+
+    def decode(self, q, use_ema=False, feat=None):
+        n = q.n
+        raw, lam, kap, mu = (self._empty(4 * self.K, n), self._empty(self.K, n), self._empty(self.K, n),
+                             self._empty(3, self.K, n))
+        npm_decode(self.h, q, self._f32(feat), use_ema, raw, lam, kap, mu, self._stream())
+        return raw, lam, kap, mu
+
+    def pdf(self, q, w, use_ema=False):
+        w = self._f32(w)
+        out = self._empty(q.n)
+        npm_pdf(self.h, q, w[0], w[1], w[2], use_ema, out, self._stream())
+        return out
+
+    def sample(self, q, u=None, seed=0, offset=0, use_ema=False, wq=None):
+        n = q.n
+        wi, pdf = self._empty(3, n), self._empty(n)
+        u = self._f32(u)
+        if wq is not None:
+            wq = self._f32(wq)
+            pdf_q = self._empty(n)
+            npm_sample(self.h, q, u, seed, offset, use_ema, wi[0], wi[1], wi[2], pdf, wq[0], wq[1], wq[2], pdf_q,
+                       stream=self._stream())
+            return wi, pdf, pdf_q
+        npm_sample(self.h, q, u, seed, offset, use_ema, wi[0], wi[1], wi[2], pdf, stream=self._stream())
+        return wi, pdf
+
+    def _train_args(self, wi, target, spdf):
+        wi, target, spdf = self._f32(wi), self._f32(target), self._f32(spdf)
+        if target.dim() == 1:
+            target = target[None]
+        return wi, target, spdf
+
+    def train_step(self, q, wi, target, spdf, n_global=None, want_stats=True):
+        wi, target, spdf = self._train_args(wi, target, spdf)
+        return npm_train_step(self.h, q, wi[0], wi[1], wi[2], target, target.shape[0], spdf,
+                              q.n if n_global is None else n_global, want_stats, self._stream())
+
+    def accumulate_grads(self, q, wi, target, spdf, n_global=None, want_stats=True):
+        wi, target, spdf = self._train_args(wi, target, spdf)
+        return npm_accumulate_grads(self.h, q, wi[0], wi[1], wi[2], target, target.shape[0], spdf,
+                                    q.n if n_global is None else n_global, want_stats, self._stream())
+
+    def optimizer_step(self, want_stats=True):
+        return npm_optimizer_step(self.h, want_stats, self._stream())
+
+    @property
+    def step(self):
+        return npm_get_step(self.h)
+
+    @step.setter
+    def step(self, t):
+        npm_set_step(self.h, t)
+
+    @property
+    def launches(self):
+        return npm_launch_count(self.h)
+
+    def level_info(self):
+        return npm_level_info(self.h, self.L)
