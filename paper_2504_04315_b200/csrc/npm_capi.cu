@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -75,6 +76,7 @@ struct npm_model {
   std::vector<cudaEvent_t> pool;
   int64_t prof_launches[16] = {};
   double prof_ms[16] = {};
+  bool use_tc = true;  // fused tcgen05 decoder (NPM_CUDACORE=1 selects the CUDA-core debug path)
 };
 
 namespace {
@@ -175,8 +177,9 @@ void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryA
   a.log_kmax = logf(m->cfg.kappa_max);
 }
 
-const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward", "weight_grad", "adam"};
-enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKinds };
+const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward", "weight_grad", "adam",
+                            "train_fused"};
+enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKTrainFused, kKinds };
 
 cudaEvent_t take_event(npm_model* m) {
   if (!m->pool.empty()) { cudaEvent_t e = m->pool.back(); m->pool.pop_back(); return e; }
@@ -276,6 +279,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   m->cfg = c;
   m->device = dev;
   m->shape = s;
+  if (const char* e = getenv("NPM_CUDACORE")) m->use_tc = !(e[0] == '1');
   if (cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     delete m;
     return fail(NPM_ERR_CUDA, "no CUDA device");
@@ -526,7 +530,7 @@ npm_status npm_decode(npm_model* m, const npm_query* q, const float* feat, int u
   a.kappa = s.out(kappa, K * n);
   a.mu = s.out(mu, 3 * K * n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
-  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query(m->shape, a, m->num_sms, st); }));
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return (m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st)); }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -549,7 +553,7 @@ npm_status npm_pdf(npm_model* m, const npm_query* q, const float* wix, const flo
   a.wx = s.in(wix, n); a.wy = s.in(wiy, n); a.wz = s.in(wiz, n);
   a.pdf = s.out(pdf, n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
-  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query(m->shape, a, m->num_sms, st); }));
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return (m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st)); }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -582,7 +586,7 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   }
   a.sx = s.out(wix, n); a.sy = s.out(wiy, n); a.sz = s.out(wiz, n); a.spdf = s.out(pdf, n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
-  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query(m->shape, a, m->num_sms, st); }));
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return (m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st)); }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -634,6 +638,11 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.counters = m->dcount;
   // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
   const NetShape& sh = m->shape;
+  if (m->use_tc) {
+    CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+    return check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
+  }
   const size_t rows = (size_t)sh.n_in + (size_t)(sh.n_layers - 1) * sh.width  // acts
                       + (size_t)(sh.n_layers - 1) * sh.width + sh.n_out;       // deltas
   CUDA_TRY(m->scratch_train.ensure(rows * n * sizeof(float)));

@@ -67,7 +67,9 @@ using namespace detail;
   int net_train_fwd_##TAG(const TrainArgs&, int, cudaStream_t);                    \
   int net_train_bwd_##TAG(const TrainArgs&, int, cudaStream_t);                    \
   int net_dw_##TAG(const TrainArgs&, int, cudaStream_t);                           \
-  int net_smem_##TAG();
+  int net_smem_##TAG();                                                             \
+  int net_query_tc_##TAG(const QueryArgs&, int, cudaStream_t);                     \
+  int net_train_tc_##TAG(const TrainArgs&, int, cudaStream_t);
 NPM_DECLARE_NET(c1)
 NPM_DECLARE_NET(c2)
 NPM_DECLARE_NET(c5)
@@ -75,7 +77,7 @@ NPM_DECLARE_NET(p16)
 #undef NPM_DECLARE_NET
 
 namespace {
-enum Op { kQuery, kTrainFwd, kTrainBwd, kDw, kSmem };
+enum Op { kQuery, kTrainFwd, kTrainBwd, kDw, kSmem, kQueryTc, kTrainTc };
 
 template <class Args>
 int call(const NetShape& s, Op op, const Args* a, int sms, cudaStream_t st) {
@@ -83,10 +85,12 @@ int call(const NetShape& s, Op op, const Args* a, int sms, cudaStream_t st) {
   if (s.n_in == NIN && s.width == W && s.n_layers == NL && s.n_out == NOUT && s.product == PROD) {     \
     if constexpr (std::is_same<Args, QueryArgs>::value) {                                              \
       if (op == kQuery) return net_query_##TAG(*a, sms, st);                                           \
+      if (op == kQueryTc) return net_query_tc_##TAG(*a, sms, st);                                      \
     } else if constexpr (std::is_same<Args, TrainArgs>::value) {                                       \
       if (op == kTrainFwd) return net_train_fwd_##TAG(*a, sms, st);                                    \
       if (op == kTrainBwd) return net_train_bwd_##TAG(*a, sms, st);                                    \
       if (op == kDw) return net_dw_##TAG(*a, sms, st);                                                 \
+      if (op == kTrainTc) return net_train_tc_##TAG(*a, sms, st);                                      \
     }                                                                                                  \
     if (op == kSmem) return net_smem_##TAG();                                                          \
     return -1;                                                                                         \
@@ -109,6 +113,14 @@ size_t weight_smem_bytes(const NetShape& s) {
 int launch_query(const NetShape& s, const QueryArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return 0;
   return call(s, kQuery, &a, sms, st);
+}
+int launch_query_tc(const NetShape& s, const QueryArgs& a, int sms, cudaStream_t st) {
+  if (a.n == 0) return 0;
+  return call(s, kQueryTc, &a, sms, st);
+}
+int launch_train_tc(const NetShape& s, const TrainArgs& a, int sms, cudaStream_t st) {
+  if (a.n == 0) return 0;
+  return call(s, kTrainTc, &a, sms, st);
 }
 int launch_train_forward(const NetShape& s, const TrainArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return 0;

@@ -73,6 +73,9 @@ int launch_train_forward(const NetShape& s, const TrainArgs& a, int num_sms, cud
 int launch_train_backward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_weight_grads(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_adam(const AdamArgs& a, int num_sms, cudaStream_t st);
+// Fused tcgen05/TMEM decoder paths (npm_tc_kernels.cuh).
+int launch_query_tc(const NetShape& s, const QueryArgs& a, int num_sms, cudaStream_t st);
+int launch_train_tc(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_init_params(float* p, int64_t n_mlp, int64_t n_total, const NetShape& s, uint64_t seed,
                        cudaStream_t st);
 

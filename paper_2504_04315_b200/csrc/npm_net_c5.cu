@@ -1,7 +1,7 @@
-// npm_net_c5.cu -- instantiation of the CUDA-core decoder kernels for the
-// decoder shape n_in=64, width=64, layers=3, 4K=32 (one TU per shape so the
-// heavily unrolled kernels compile in parallel).
-#include "npm_kernels_impl.cuh"
+// npm_net_c5.cu -- instantiation of the decoder kernels for the decoder shape
+// n_in=64, width=64, layers=3, 4K=32 (one TU per shape so the heavily
+// unrolled kernels compile in parallel).
+#include "npm_tc_kernels.cuh"
 
 namespace npm {
 using NetT = detail::Net<64, 64, 3, 32>;
@@ -10,4 +10,6 @@ int net_train_fwd_c5(const TrainArgs& a, int sms, cudaStream_t st) { return deta
 int net_train_bwd_c5(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::train_bwd(a, sms, st); }
 int net_dw_c5(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::dw(a, sms, st); }
 int net_smem_c5() { return NetT::SMEM_FLOATS * (int)sizeof(float); }
+int net_query_tc_c5(const QueryArgs& a, int sms, cudaStream_t st) { return tck::TcLaunch<NetT>::query(a, sms, st); }
+int net_train_tc_c5(const TrainArgs& a, int sms, cudaStream_t st) { return tck::TcLaunch<NetT>::train(a, sms, st); }
 }  // namespace npm
