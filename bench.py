@@ -274,6 +274,7 @@ def main():
     gather = 8 * L * F * 4
     per_unit = {  # algorithmic bytes per sample
         "query": 12 + 12 + gather + 12 + 4 + 4,          # x, caller dir, gathers, sample w + pdf, pdf_q
+        "train_fused": 12 + 12 + 4 * ttg.shape[0] + 4 + 2 * gather,   # records + gathers + scatter-add
         "train_forward": 12 + 12 + 4 * ttg.shape[0] + 4 + gather,
         "train_backward": 12 + gather,                   # x (re-derive corners) + scatter-add
         "weight_grad": 0, "adam": 0, "encode": 12 + gather + 4 * L * F,
@@ -289,13 +290,26 @@ def main():
             "kernel_share_of_step": (kms / 1e3) / t_tot if t_tot > 0 else None, "peak_source": src,
             "per_unit_bytes": per_unit.get(kname), "units_per_launch": n}
 
+    # decoder tensor-core work (algorithmic MACs of the 64-wide MLP; split-bf16 issues 3x)
+    dims = [(m.cfg.n_levels * m.F + (33 if m.product else 0), m.cfg.mlp_width)]
+    dims += [(m.cfg.mlp_width, m.cfg.mlp_width)] * (m.cfg.mlp_linear_layers - 2)
+    dims += [(m.cfg.mlp_width, 4 * m.K)]
+    fwd_flop = 2 * sum(i * o for i, o in dims)
+    t_dec = {k: v for k, v in prof.items() if k in ("query", "train_fused")}
+    tens = {}
+    for k, (kl2, kms2) in t_dec.items():
+        fl = (fwd_flop if k == "query" else 3 * fwd_flop) * n * kl2
+        tens[k] = {"algorithmic_tflops": fl / (kms2 / 1e3) / 1e12 if kms2 else None,
+                   "issued_tflops_split_bf16x3": 3 * fl / (kms2 / 1e3) / 1e12 if kms2 else None,
+                   "peak_bf16_tflops": bf16, "flop_per_sample": fl / (n * kl2)}
+    roof["decoder_tensor"] = tens
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(name)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
                 "ms_per_step": 1e3 * t_tot / K, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f32 (decoder MMAs split-bf16x3, f32 accumulate)", "data": "synthetic",
                 "config": {"workload": "%s: %s" % (name, "per-frame batch 1280x720 queries + records per GPU, "
                                                    "K=8, L=8 (D 8..86, T=2^18), 3x64 MLP" if name == "c2" else name),
                            "n_per_gpu": n, "l2": "flushed between timed steps (512 MB write)",

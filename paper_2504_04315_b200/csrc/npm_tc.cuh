@@ -108,6 +108,39 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+template <int NC>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
+  static_assert(NC == 1 || NC == 2 || NC == 4 || NC == 8 || NC == 16 || NC % 16 == 0, "columns");
+  if constexpr (NC % 16 == 0 && NC > 16) {
+#pragma unroll
+    for (int c = 0; c < NC; c += 16) tmem_ld16(taddr + (uint32_t)c, v + c);
+  } else if constexpr (NC == 16) {
+    tmem_ld16(taddr, v);
+  } else if constexpr (NC == 8) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  } else if constexpr (NC == 4) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+  } else if constexpr (NC == 2) {
+    uint32_t r[2];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+    v[0] = __uint_as_float(r[0]);
+    v[1] = __uint_as_float(r[1]);
+  } else {
+    uint32_t r0;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r0) : "r"(taddr));
+    v[0] = __uint_as_float(r0);
+  }
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -136,6 +169,29 @@ __device__ __forceinline__ void store_chunk(uint32_t hi_base, uint32_t lo_base, 
   const uint32_t off = (uint32_t)(j * rows * 16 + row * 16);
   st_shared_v4(hi_base + off, h[0], h[1], h[2], h[3]);
   st_shared_v4(lo_base + off, l[0], l[1], l[2], l[3]);
+}
+
+// Write CNT consecutive features [f0, f0 + CNT) of one row (split hi/lo);
+// CNT in {2, 4, 8k}; f0 aligned to min(CNT, 8).
+template <int CNT>
+__device__ __forceinline__ void store_feats(uint32_t hi_base, uint32_t lo_base, int rows, int row, int f0,
+                                            const float* v) {
+  if constexpr (CNT >= 8) {
+#pragma unroll
+    for (int j = 0; j < CNT / 8; ++j) store_chunk(hi_base, lo_base, rows, row, f0 / 8 + j, v + 8 * j);
+  } else {
+    uint32_t h[CNT / 2], l[CNT / 2];
+#pragma unroll
+    for (int q = 0; q < CNT / 2; ++q) split_pack(v[2 * q], v[2 * q + 1], h[q], l[q]);
+    const uint32_t off = (uint32_t)((f0 / 8) * rows * 16 + row * 16 + (f0 % 8) * 2);
+    if constexpr (CNT == 4) {
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" :: "r"(hi_base + off), "r"(h[0]), "r"(h[1]) : "memory");
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" :: "r"(lo_base + off), "r"(l[0]), "r"(l[1]) : "memory");
+    } else {
+      asm volatile("st.shared.b32 [%0], %1;" :: "r"(hi_base + off), "r"(h[0]) : "memory");
+      asm volatile("st.shared.b32 [%0], %1;" :: "r"(lo_base + off), "r"(l[0]) : "memory");
+    }
+  }
 }
 
 }  // namespace tc

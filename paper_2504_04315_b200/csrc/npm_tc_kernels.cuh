@@ -38,8 +38,9 @@ template <class N>
 struct TC {
   static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN;
   static constexpr int KIN = r16(NIN);          // layer-0 MMA K
-  static constexpr int ZF = r16(NIN + 1);       // train X0 features (ones at NIN)
-  static constexpr int HF = r16(W + 1);         // train hidden features (ones at W)
+  // train X0 features: ones at NIN (bias row of dW_0^T), >= KIN for the forward K
+  static constexpr int ZF = KIN > ((NIN + 8) & ~7) ? KIN : ((NIN + 8) & ~7);
+  static constexpr int HF = W + 8;              // train hidden features (ones at W)
   __host__ __device__ static constexpr int in_p(int k) { return k == 0 ? KIN : W; }   // padded MMA K of layer k
   __host__ __device__ static constexpr int out(int k) { return k == NL - 1 ? NOUT : W; }
   __host__ __device__ static constexpr int in(int k) { return k == 0 ? NIN : W; }
@@ -64,7 +65,8 @@ struct TC {
   static constexpr uint32_t DOFF = xoff(NL);
   static constexpr uint32_t WOFF_T = DOFF + 2u * (NOUT / 8) * CH;
   static constexpr uint32_t BOFF_T = WOFF_T + WBYTES;
-  static constexpr uint32_t MISC_T = (BOFF_T + BBYTES + 127u) & ~127u;
+  static constexpr uint32_t RED_T = (BOFF_T + BBYTES + 127u) & ~127u;   // head reductions [3][4][R] f32
+  static constexpr uint32_t MISC_T = RED_T + 3u * 4u * R * 4u;
   // every X_k^T MMA reads 16 chunks from its lo base: keep them inside the allocation
   __host__ __device__ static constexpr uint32_t overread(int k) {
     return xoff(k) + (xfeat(k) / 8) * CH + 16u * CH;
@@ -313,14 +315,26 @@ __global__ void __launch_bounds__(R, 1) tc_query_kernel(QueryArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused training kernel: encode -> forward -> Eq. 9 head -> backward (dX, dW^T)
-// -> grid scatter; dW/db flushed once per CTA.
+// Fused training kernel, 4 threads per sample row (512 threads, 16 warps):
+// thread (q, r): quarter q = warp / 4 in [0, 4), row r = 32 (warp % 4) + lane,
+// i.e. TMEM lane r.  Quarter q owns grid levels [q L/4, (q+1) L/4) in the
+// encode and the scatter, columns [q C/4, (q+1) C/4) of every accumulator in
+// the epilogues, and lobes [q K/4, (q+1) K/4) in the Eq. 9 head (cross-quarter
+// softmax / mixture sums through smem).  Phases per 128-sample tile:
+//   encode -> X0;  forward k: MMA, epilogue -> X_{k+1};  head -> delta_L;
+//   backward k = L..0: MMA batch {dX, dW_k^T += X_k^T delta_k}, epilogue
+//   delta_{k-1} (or dz -> red.global.add.v4.f32 on the grid gradient).
 template <class N>
-__global__ void __launch_bounds__(R, 1) tc_train_kernel(TrainArgs a) {
+__global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
   using T = TC<N>;
-  constexpr int NL = N::NL;
+  constexpr int NL = N::NL, K = N::K, W = N::W, NOUT = N::NOUT;
+  constexpr int KQ = K / 4, WQ = W / 4, LQ = N::L / 4, GQ = 4 * LQ;
+  static_assert(K % 4 == 0 && N::L % 4 == 0 && W % 32 == 0, "quartered kernel shape");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = tc::smem_u32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, q = warp >> 2;
+  const int r = ((warp & 3) << 5) | (tid & 31);
+  const uint32_t lane_addr = (uint32_t)((warp & 3) << 21);   // (32 * (warp % 4)) << 16
   uint64_t* mbar;
   uint32_t tbase;
   setup_cta<N>(smem, T::MISC_T, T::TCOLS_TRAIN, mbar, tbase);
@@ -328,45 +342,89 @@ __global__ void __launch_bounds__(R, 1) tc_train_kernel(TrainArgs a) {
   const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
   float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
   const float* bias = reinterpret_cast<const float*>(smem + T::BOFF_T);
-  const int r = threadIdx.x;
+  float* red = reinterpret_cast<float*>(smem + T::RED_T);   // [3][4][R]
   const int64_t n = a.n;
   const int64_t ntiles = (n + R - 1) / R;
   uint32_t phase = 0, first = 1;
   double loss = 0.0;
   unsigned c_used = 0, c_zero = 0, c_drop = 0;
-  // smem addresses of X_k (hi) and its lo offset
   uint32_t xhi[NL], xlo[NL];
 #pragma unroll
   for (int k = 0; k < NL; ++k) {
     xhi[k] = sb + T::xoff(k);
     xlo[k] = xhi[k] + (T::xfeat(k) / 8) * CH;
   }
-  const uint32_t dlast_hi = sb + T::DOFF, dlast_lo = dlast_hi + (N::NOUT / 8) * CH;
+  const uint32_t dlast_hi = sb + T::DOFF, dlast_lo = dlast_hi + (NOUT / 8) * CH;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * R + r;
     const bool valid = i < n;
-    uint64_t mask[NL];   // ReLU masks of X_1..X_{NL-1} (bit j: feature j > 0)
-    // ---- encode -> X_0 (features [0, NIN), ones at NIN, zeros to ZF)
+    const int64_t ic = valid ? i : 0;
+    uint32_t mask[NL];   // ReLU mask bits of this quarter's WQ columns of X_1..X_{NL-1}
+    float ux = 0.f, uy = 0.f, uz = 0.f;
+    // ---- encode: levels [q LQ, (q+1) LQ) -> features [q GQ, (q+1) GQ) of X0
     {
-      float z[T::ZF];
+      float g[GQ];
       if (valid) {
-        network_input<N>(a.grid, tab, a.px, a.py, a.pz, a.wox, a.woy, a.woz, a.nx, a.ny, a.nz, a.rough, i, z,
-                         nullptr, nullptr, n);
+        ux = normalize_axis(__ldg(a.px + i), a.grid.lo[0], a.grid.inv[0]);
+        uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
+        uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
+#pragma unroll
+        for (int ll = 0; ll < LQ; ++ll) {
+          const int l = q * LQ + ll;
+          LevelCorners lc;
+          level_corners(a.grid, l, ux, uy, uz, lc);
+          const float4* t = tab + a.grid.off[l];
+          float4 v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = __ldg(t + lc.idx[c]);
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
+            a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
+          }
+          g[4 * ll] = a0; g[4 * ll + 1] = a1; g[4 * ll + 2] = a2; g[4 * ll + 3] = a3;
+        }
       } else {
 #pragma unroll
-        for (int j = 0; j < N::NINP; ++j) z[j] = 0.0f;
+        for (int j = 0; j < GQ; ++j) g[j] = 0.0f;
       }
+      tc::store_feats<GQ>(xhi[0], xlo[0], R, r, q * GQ, g);
+      // conditioning / ones features [NGRID, ZF)
+      if constexpr (N::PRODUCT) {
+        float e[16];
+        if (q == 0 || q == 1) {
+          if (valid) {
+            if (q == 0) sh4(__ldg(a.wox + i), __ldg(a.woy + i), __ldg(a.woz + i), e);
+            else sh4(__ldg(a.nx + i), __ldg(a.ny + i), __ldg(a.nz + i), e);
+          } else {
 #pragma unroll
-      for (int j = N::NIN; j < T::ZF; ++j) z[j] = j == N::NIN ? 1.0f : 0.0f;
+            for (int j = 0; j < 16; ++j) e[j] = 0.0f;
+          }
+          tc::store_feats<16>(xhi[0], xlo[0], R, r, 32 + 16 * q, e);
+        } else if (q == 2) {
 #pragma unroll
-      for (int j = 0; j < T::ZF / 8; ++j) tc::store_chunk(xhi[0], xlo[0], R, r, j, z + 8 * j);
+          for (int j = 0; j < 16; ++j) e[j] = 0.0f;
+          e[0] = valid ? __ldg(a.rough + i) : 0.0f;   // feature 64
+          e[1] = 1.0f;                                  // feature 65 = NIN: ones (bias row)
+          tc::store_feats<16>(xhi[0], xlo[0], R, r, 64, e);
+        }
+      } else {
+        if (q == 3) {
+          float e[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int f = N::NGRID; f < T::ZF; f += 8) {
+            tc::store_chunk(xhi[0], xlo[0], R, r, f / 8, e);
+            e[0] = 0.f;
+          }
+        }
+      }
     }
     // ---- forward
-    float draw[N::NOUT];
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       handoff_to_mma();
-      if (r == 0) {
+      if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF_T + T::woff(k);
         issue_fwd(tbase, xhi[k], xlo[k], w, w + T::wbytes(k), T::in_p(k), T::out(k));
@@ -375,55 +433,111 @@ __global__ void __launch_bounds__(R, 1) tc_train_kernel(TrainArgs a) {
       wait_mma(mbar, phase);
       const float* b = bias + T::boff(k) / 4;
       if (k < NL - 1) {
-        float h[T::HF];
-        tmem_row<N::W>(tbase, 0, h);
-        uint64_t mk = 0;
+        float h[WQ];
+        tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), h);
+        tc::tmem_wait_ld();
+        uint32_t mk = 0;
 #pragma unroll
-        for (int j = 0; j < N::W; ++j) {
-          h[j] = fmaxf(h[j] + b[j], 0.0f);
-          mk |= (h[j] > 0.0f ? 1ull : 0ull) << j;
+        for (int j = 0; j < WQ; ++j) {
+          h[j] = fmaxf(h[j] + b[q * WQ + j], 0.0f);
+          mk |= (h[j] > 0.0f ? 1u : 0u) << j;
         }
         mask[k + 1] = mk;
-#pragma unroll
-        for (int j = N::W; j < T::HF; ++j) h[j] = j == N::W ? 1.0f : 0.0f;
-#pragma unroll
-        for (int j = 0; j < T::HF / 8; ++j) tc::store_chunk(xhi[k + 1], xlo[k + 1], R, r, j, h + 8 * j);
+        tc::store_feats<WQ>(xhi[k + 1], xlo[k + 1], R, r, q * WQ, h);
+        if (q == 3) {   // ones feature at W (bias row of dW_{k+1}^T)
+          const float e[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          tc::store_chunk(xhi[k + 1], xlo[k + 1], R, r, W / 8, e);
+        }
       } else {
-        float raw[N::NOUT];
-        tmem_row<N::NOUT>(tbase, 0, raw);
+        // ---- Eq. 9 head, lobes [q KQ, (q+1) KQ) (C-O12, C-O13)
+        float lp[KQ], kp[KQ], tp[KQ], pp[KQ];
+        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(q * KQ), lp);
+        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(K + q * KQ), kp);
+        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(2 * K + q * KQ), tp);
+        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(3 * K + q * KQ), pp);
+        tc::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < N::NOUT; ++j) raw[j] += b[j];
-        // ---- Eq. 9 head (C-O12, C-O13)
-        bool use = false;
-        float s = 0.0f;
-        if (valid) {
-          float t = __ldg(a.target + i);
-          bool all_zero = t == 0.0f;
-          if (a.channels == 3) {
-            const float tg = __ldg(a.target + n + i), tb = __ldg(a.target + 2 * n + i);
-            all_zero = all_zero && tg == 0.0f && tb == 0.0f;
-            t = 0.2126f * t + 0.7152f * tg + 0.0722f * tb;
-          }
-          const float p = __ldg(a.spdf + i);
-          const float ratio = t / p;
-          const bool drop = !isfinite(ratio) || !isfinite(p) || !(p > 0.0f);
-          const bool zero = !drop && all_zero;
-          c_drop += drop;
-          c_zero += zero;
-          use = !drop && !zero;
-          s = (float)(-(double)ratio * a.inv_n_global);
+        for (int j = 0; j < KQ; ++j) {
+          lp[j] += b[q * KQ + j]; kp[j] += b[K + q * KQ + j];
+          tp[j] += b[2 * K + q * KQ + j]; pp[j] += b[3 * K + q * KQ + j];
         }
-        if (use) {
-          const float logv = grad_head<N::K>(raw, a.log_kmin, a.log_kmax, __ldg(a.wx + i), __ldg(a.wy + i),
-                                             __ldg(a.wz + i), s, draw);
-          loss += (double)s * (double)logv;
-          c_used += 1;
-        } else {
-#pragma unroll
-          for (int j = 0; j < N::NOUT; ++j) draw[j] = 0.0f;
+        // record scale (every quarter evaluates it for its row)
+        float t = __ldg(a.target + ic);
+        bool all_zero = t == 0.0f;
+        if (a.channels == 3) {
+          const float tg = __ldg(a.target + n + ic), tb = __ldg(a.target + 2 * n + ic);
+          all_zero = all_zero && tg == 0.0f && tb == 0.0f;
+          t = 0.2126f * t + 0.7152f * tg + 0.0722f * tb;
         }
+        const float p = __ldg(a.spdf + ic);
+        const float ratio = t / p;
+        const bool drop = valid && (!isfinite(ratio) || !isfinite(p) || !(p > 0.0f));
+        const bool zero = valid && !drop && all_zero;
+        const bool use = valid && !drop && !zero;
+        const float s = use ? (float)(-(double)ratio * a.inv_n_global) : 0.0f;
+        const float wx = __ldg(a.wx + ic), wy = __ldg(a.wy + ic), wz = __ldg(a.wz + ic);
+        // own lobes: kappa, mu, v_i(w)
+        float kap[KQ], mx[KQ], my[KQ], mz[KQ], th[KQ], ph[KQ], v[KQ];
+        float mloc = lp[0];
 #pragma unroll
-        for (int j = 0; j < N::NOUT / 8; ++j) tc::store_chunk(dlast_hi, dlast_lo, R, r, j, draw + 8 * j);
+        for (int j = 0; j < KQ; ++j) {
+          mloc = fmaxf(mloc, lp[j]);
+          kap[j] = expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
+          th[j] = 1.0f / (1.0f + expf(-tp[j]));
+          ph[j] = 1.0f / (1.0f + expf(-pp[j]));
+          float st, ct, sp, cp;
+          sincospif(th[j], &st, &ct);
+          sincospif(2.0f * ph[j], &sp, &cp);
+          mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
+          v[j] = lobe_pdf(kap[j], mx[j], my[j], mz[j], wx, wy, wz);
+        }
+        // softmax max over all K lambda' (cross-quarter)
+        red[(0 * 4 + q) * R + r] = mloc;
+        __syncthreads();
+        const float M = fmaxf(fmaxf(red[0 * R + r], red[1 * R + r]), fmaxf(red[2 * R + r], red[3 * R + r]));
+        float e[KQ], S = 0.0f, P = 0.0f;
+#pragma unroll
+        for (int j = 0; j < KQ; ++j) {
+          e[j] = expf(lp[j] - M);
+          S += e[j];
+          P += e[j] * v[j];
+        }
+        red[(1 * 4 + q) * R + r] = S;
+        red[(2 * 4 + q) * R + r] = P;
+        __syncthreads();
+        const float Ssum = red[4 * R + r] + red[5 * R + r] + red[6 * R + r] + red[7 * R + r];
+        const float Psum = red[8 * R + r] + red[9 * R + r] + red[10 * R + r] + red[11 * R + r];
+        const float invS = 1.0f / Ssum;
+        const float Vb = fmaxf(Psum * invS, kVFloor);
+        const float invV = 1.0f / Vb;
+        float dl[KQ], dk[KQ], dt[KQ], dp[KQ];
+#pragma unroll
+        for (int j = 0; j < KQ; ++j) {
+          const float lam = e[j] * invS;
+          const float gam = lam * v[j] * invV;
+          dl[j] = s * (gam - lam);
+          const float dx = mx[j] - wx, dy = my[j] - wy, dz = mz[j] - wz;
+          const float d2 = dx * dx + dy * dy + dz * dz;
+          const float em = -expm1f(-2.0f * kap[j]);
+          const float dkk = s * gam * (1.0f - kap[j] * 0.5f * d2 - 2.0f * kap[j] * expf(-2.0f * kap[j]) / em);
+          dk[j] = (kp[j] < a.log_kmin || kp[j] > a.log_kmax) ? 0.0f : dkk;
+          float st, ct, sp, cp;
+          sincospif(th[j], &st, &ct);
+          sincospif(2.0f * ph[j], &sp, &cp);
+          const float wdth = kPi * (ct * cp * wx + ct * sp * wy - st * wz);
+          const float wdph = kTwoPi * (-st * sp * wx + st * cp * wy);
+          const float sgk = s * gam * kap[j];
+          dt[j] = sgk * wdth * th[j] * (1.0f - th[j]);
+          dp[j] = sgk * wdph * ph[j] * (1.0f - ph[j]);
+        }
+        if (q == 0) {
+          c_drop += drop; c_zero += zero;
+          if (use) { loss += (double)s * (double)logf(Vb); c_used += 1; }
+        }
+        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, q * KQ, dl);
+        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, K + q * KQ, dk);
+        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, 2 * K + q * KQ, dt);
+        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, 3 * K + q * KQ, dp);
       }
     }
     // ---- backward
@@ -431,74 +545,74 @@ __global__ void __launch_bounds__(R, 1) tc_train_kernel(TrainArgs a) {
 #pragma unroll
     for (int k = NL - 1; k >= 0; --k) {
       handoff_to_mma();
-      const int nin = k > 0 ? N::W : N::NGRID;
-      if (r == 0) {
+      if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF_T + T::woff(k);
-        issue_dx(tbase, dhi, dlo, w, w + T::wbytes(k), T::out(k), nin);
+        issue_dx(tbase, dhi, dlo, w, w + T::wbytes(k), T::out(k), k > 0 ? W : N::NGRID);
         issue_dw(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, T::out(k), first);
         tc::mma_commit(mbar);
       }
       wait_mma(mbar, phase);
       if (k > 0) {
-        float d[N::W];
-        tmem_row<N::W>(tbase, 0, d);
-        const uint64_t mk = mask[k];
+        float d[WQ];
+        tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), d);
+        tc::tmem_wait_ld();
+        const uint32_t mk = mask[k];
 #pragma unroll
-        for (int j = 0; j < N::W; ++j) d[j] = ((mk >> j) & 1ull) ? d[j] : 0.0f;
-        // delta_{k-1} overwrites X_k (dead once its dW MMA completed)
-        dhi = xhi[k];
-        dlo = xhi[k] + (N::W / 8) * CH;
-#pragma unroll
-        for (int j = 0; j < N::W / 8; ++j) tc::store_chunk(dhi, dlo, R, r, j, d + 8 * j);
+        for (int j = 0; j < WQ; ++j) d[j] = ((mk >> j) & 1u) ? d[j] : 0.0f;
+        dhi = xhi[k];                       // delta_{k-1} overwrites X_k (its dW MMA completed)
+        dlo = xhi[k] + (W / 8) * CH;
+        tc::store_feats<WQ>(dhi, dlo, R, r, q * WQ, d);
       } else {
-        float dz[N::NGRID];
-        tmem_row<N::NGRID>(tbase, 0, dz);   // warp-collective: before the validity branch
-        if (!valid) continue;
-        const float ux = normalize_axis(__ldg(a.px + i), a.grid.lo[0], a.grid.inv[0]);
-        const float uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
-        const float uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
+        float dz[GQ];
+        tc::tmem_ldn<GQ>(tbase + lane_addr + (uint32_t)(q * GQ), dz);
+        tc::tmem_wait_ld();
+        if (valid) {
 #pragma unroll
-        for (int l = 0; l < N::L; ++l) {
-          const float g0 = dz[4 * l], g1 = dz[4 * l + 1], g2 = dz[4 * l + 2], g3 = dz[4 * l + 3];
-          if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f && g3 == 0.0f) continue;
-          LevelCorners lc;
-          level_corners(a.grid, l, ux, uy, uz, lc);
-          float4* t = gtab + a.grid.off[l];
+          for (int ll = 0; ll < LQ; ++ll) {
+            const int l = q * LQ + ll;
+            const float g0 = dz[4 * ll], g1 = dz[4 * ll + 1], g2 = dz[4 * ll + 2], g3 = dz[4 * ll + 3];
+            if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f && g3 == 0.0f) continue;
+            LevelCorners lc;
+            level_corners(a.grid, l, ux, uy, uz, lc);
+            float4* t = gtab + a.grid.off[l];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float w = lc.w[c];
-            atomicAdd(t + lc.idx[c], make_float4(w * g0, w * g1, w * g2, w * g3));
+            for (int c = 0; c < 8; ++c) {
+              const float w = lc.w[c];
+              atomicAdd(t + lc.idx[c], make_float4(w * g0, w * g1, w * g2, w * g3));
+            }
           }
         }
       }
     }
     first = 0;
   }
-  // ---- flush dW^T / db accumulators: lane r = input feature r (r == in: bias)
+  // ---- flush dW^T / db: lane r = input feature r (r == in: bias); quarter q
+  // takes columns [q out/4, (q+1) out/4)
   if (!first) {
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
-      constexpr int MAXO = N::NOUT > N::W ? N::NOUT : N::W;
+      constexpr int MAXO = (NOUT > W ? NOUT : W) / 4;
       float v[MAXO];
-      const int out = T::out(k), in = T::in(k);
-      if (out == N::NOUT) tmem_row<N::NOUT>(tbase, T::dwcol(k), v);
-      else tmem_row<N::W>(tbase, T::dwcol(k), v);
+      const int out = T::out(k), in = T::in(k), oq = out / 4;
+      if (out == NOUT) tc::tmem_ldn<NOUT / 4>(tbase + lane_addr + (uint32_t)(T::dwcol(k) + q * (NOUT / 4)), v);
+      else tc::tmem_ldn<W / 4>(tbase + lane_addr + (uint32_t)(T::dwcol(k) + q * (W / 4)), v);
+      tc::tmem_wait_ld();
       if (r < in) {
         float* g = a.grads + N::gw_off(k) + r;
-        for (int o = 0; o < out; ++o) atomicAdd(g + o * in, v[o]);
+        for (int o = 0; o < oq; ++o) atomicAdd(g + (q * oq + o) * in, v[o]);
       } else if (r == in) {
         float* g = a.grads + N::gb_off(k);
-        for (int o = 0; o < out; ++o) atomicAdd(g + o, v[o]);
+        for (int o = 0; o < oq; ++o) atomicAdd(g + q * oq + o, v[o]);
       }
     }
   }
   loss = warp_sum_d(loss);
   c_used = warp_sum_u(c_used); c_zero = warp_sum_u(c_zero); c_drop = warp_sum_u(c_drop);
-  if ((threadIdx.x & 31) == 0) {
+  if ((threadIdx.x & 31) == 0 && q == 0) {
     atomicAdd(a.stats, loss);
     atomicAdd(a.counters + 0, (unsigned long long)c_used);
     atomicAdd(a.counters + 1, (unsigned long long)c_zero);
@@ -526,7 +640,7 @@ struct TcLaunch {
     const int per_sm = (int)((227u * 1024u) / (T::SMEM_TRAIN + 1024u));
     const int64_t cap = (int64_t)sms * (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm));
     const int blocks = (int)(ntiles < cap ? ntiles : cap);
-    tc_train_kernel<N><<<blocks, R, T::SMEM_TRAIN, st>>>(a);
+    tc_train_kernel<N><<<blocks, 4 * R, T::SMEM_TRAIN, st>>>(a);
     return 1;
   }
 };
