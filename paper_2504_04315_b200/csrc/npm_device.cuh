@@ -165,6 +165,9 @@ __device__ __forceinline__ float mixture_pdf(const Mixture<K>& m, float wx, floa
   return v;
 }
 
+__device__ __forceinline__ void lobe_sample(float kap, float mux, float muy, float muz, float u2, float u3,
+                                            float& wx, float& wy, float& wz);
+
 // Jakob 2012 stable vMF inversion in the Duff et al. ONB (C-O10).
 template <int K>
 __device__ __forceinline__ void mixture_sample(const Mixture<K>& m, float u1, float u2, float u3,
@@ -182,6 +185,13 @@ __device__ __forceinline__ void mixture_sample(const Mixture<K>& m, float u1, fl
 #pragma unroll
   for (int i = 1; i < K; ++i)
     if (sel == i) { kap = m.kap[i]; mux = m.mx[i]; muy = m.my[i]; muz = m.mz[i]; }
+  lobe_sample(kap, mux, muy, muz, u2, u3, wx, wy, wz);
+}
+
+// One vMF lobe sampled from (u2, u3): Jakob 2012 inversion of the cosine to
+// mu + azimuth 2 pi u3 in the Duff et al. ONB (C-O10).
+__device__ __forceinline__ void lobe_sample(float kap, float mux, float muy, float muz, float u2, float u3,
+                                            float& wx, float& wy, float& wz) {
   // delta = -log(u2 + (1 - u2) e^{-2 kappa}) / kappa  (Jakob 2012, C-O10), evaluated in fp32
   // in whichever of two equal forms is well conditioned: log1p of
   // x = (1 - u2) expm1(-2 kappa) while 1 + x >= 1/2, else log of 1 + x formed

@@ -63,7 +63,19 @@ struct TC {
     return k == 0 ? 0u : xoff(k - 1) + 2u * (xfeat(k - 1) / 8) * CH;
   }
   static constexpr uint32_t DOFF = xoff(NL);
-  static constexpr uint32_t WOFF_T = DOFF + 2u * (NOUT / 8) * CH;
+  // hidden-layer deltas D_0..D_{NL-2} get their own buffers when smem allows
+  // (SEP_D): each dW_k^T MMA batch then runs behind the next dX while the
+  // threads compute the next delta; otherwise D_{k-1} overwrites X_k.
+  static constexpr uint32_t DHOFF = DOFF + 2u * (NOUT / 8) * CH;
+  static constexpr uint32_t DH_ONE = 2u * (W / 8) * CH;
+  // Measured on B200 (c2): the deferred-dW overlap (SEP_D) costs +64 KB smem,
+  // which shrinks L1 (unified with smem) and the gathers' L1 hit rate (28 % of
+  // sectors at 150 KB smem): 0.97 ms vs 0.82 ms per train step. Kept off; the
+  // code path stays for configurations with small activation tiles.
+  static constexpr bool SEP_D = false &&
+      DHOFF + (NL - 1) * DH_ONE + WBYTES + BBYTES + 3u * 4u * R * 4u + 512u <= 227u * 1024u;
+  __host__ __device__ static constexpr uint32_t dhoff(int k) { return DHOFF + (uint32_t)k * DH_ONE; }
+  static constexpr uint32_t WOFF_T = DHOFF + (SEP_D ? (NL - 1) * DH_ONE : 0u);
   static constexpr uint32_t BOFF_T = WOFF_T + WBYTES;
   static constexpr uint32_t RED_T = (BOFF_T + BBYTES + 127u) & ~127u;   // head reductions [3][4][R] f32
   static constexpr uint32_t MISC_T = RED_T + 3u * 4u * R * 4u;
@@ -82,7 +94,8 @@ struct TC {
   static constexpr uint32_t QA = 0, QB = 2u * (QAF / 8) * CH;
   static constexpr uint32_t WOFF_Q = QB + 2u * (W / 8) * CH;
   static constexpr uint32_t BOFF_Q = WOFF_Q + WBYTES;
-  static constexpr uint32_t MISC_Q = (BOFF_Q + BBYTES + 127u) & ~127u;
+  static constexpr uint32_t RED_Q = (BOFF_Q + BBYTES + 127u) & ~127u;   // head reductions [5][4][R] f32
+  static constexpr uint32_t MISC_Q = RED_Q + 5u * 4u * R * 4u;
   static constexpr uint32_t SMEM_QUERY = MISC_Q + 64;
 };
 
@@ -185,10 +198,11 @@ __device__ __forceinline__ void wait_mma(uint64_t* mbar, uint32_t& phase) {
 template <class N>
 __device__ __forceinline__ void setup_cta(uint8_t* smem, uint32_t misc, int tcols, uint64_t*& mbar,
                                           uint32_t& tbase) {
-  mbar = reinterpret_cast<uint64_t*>(smem + misc);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + misc + 8);
+  mbar = reinterpret_cast<uint64_t*>(smem + misc);           // mbar[0]: waited MMA batches
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + misc + 16);   // mbar[1]: deferred dW batches
   if (threadIdx.x == 0) {
     tc::mbar_init(mbar, 1);
+    tc::mbar_init(mbar + 1, 1);
     tc::fence_mbar_init();
   }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, (uint32_t)tcols);
@@ -206,109 +220,223 @@ __device__ __forceinline__ void teardown_cta(uint32_t tbase, int tcols) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused query kernel: encode -> decoder (tcgen05) -> Table 1 -> outputs.
+// Fused query kernel: encode -> decoder (tcgen05) -> Table 1 -> outputs, with
+// the train kernel's mapping: 4 threads per sample row (512 threads), quarter q
+// owning grid levels [q L/4, ...), accumulator columns [q C/4, ...) and lobes
+// [q K/4, ...); softmax, mixture sums and the lobe choice cross quarters
+// through smem.  Lobe choice (C-O10, C-A17): quarter boundaries
+// B_q = sum_{q'<q} S_q' (S_q = sum of the quarter's e^{lambda'-M}) are
+// computed identically by the 4 threads of a row, so exactly one quarter owns
+// u1 and picks its first lobe with u1 < C_i (its last lobe at C = B_{q+1}).
 template <class N>
-__global__ void __launch_bounds__(R, 1) tc_query_kernel(QueryArgs a) {
+__global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
   using T = TC<N>;
+  constexpr int NL = N::NL, K = N::K, W = N::W;
+  constexpr int KQ = K / 4, WQ = W / 4, LQ = N::L / 4, GQ = 4 * LQ;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = tc::smem_u32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, q = warp >> 2;
+  const int r = ((warp & 3) << 5) | (tid & 31);
+  const uint32_t lane_addr = (uint32_t)((warp & 3) << 21);
   uint64_t* mbar;
   uint32_t tbase;
   setup_cta<N>(smem, T::MISC_Q, T::TCOLS_QUERY, mbar, tbase);
   stage_weights_tc<N>(a.params, smem, T::WOFF_Q, T::BOFF_Q);
   const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
   const float* bias = reinterpret_cast<const float*>(smem + T::BOFF_Q);
-  const int r = threadIdx.x;
+  float* red = reinterpret_cast<float*>(smem + T::RED_Q);   // [slot][4][R]
+  auto RS = [&](int slot, int qq) -> float& { return red[(slot * 4 + qq) * R + r]; };
   const int64_t n = a.n;
   const int64_t ntiles = (n + R - 1) / R;
   uint32_t phase = 0;
   const uint32_t xbuf[2] = {sb + T::QA, sb + T::QB};
-  const uint32_t xlo[2] = {(uint32_t)(T::QAF / 8) * CH, (uint32_t)(N::W / 8) * CH};
+  const uint32_t xlo[2] = {(uint32_t)(T::QAF / 8) * CH, (uint32_t)(W / 8) * CH};
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * R + r;
     const bool valid = i < n;
-    // ---- encode (Eq. 13) + conditioning -> buffer A
+    const int64_t ic = valid ? i : 0;
+    // ---- encode (Eq. 13): levels [q LQ, (q+1) LQ) + conditioning -> buffer A
     {
-      float z[T::KIN];
-      if (valid) {
-        if (a.feat_in) {
+      float g[GQ];
+      if (valid && a.feat_in) {
 #pragma unroll
-          for (int j = 0; j < N::NGRID; ++j) z[j] = __ldg(a.feat_in + (int64_t)j * n + i);
+        for (int j = 0; j < GQ; ++j) g[j] = __ldg(a.feat_in + (int64_t)(q * GQ + j) * n + i);
+      } else if (valid) {
+        const float ux = normalize_axis(__ldg(a.px + i), a.grid.lo[0], a.grid.inv[0]);
+        const float uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
+        const float uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
 #pragma unroll
-          for (int j = N::NGRID; j < N::NINP; ++j) z[j] = 0.0f;
-        } else {
-          network_input<N>(a.grid, tab, a.px, a.py, a.pz, a.wox, a.woy, a.woz, a.nx, a.ny, a.nz, a.rough, i,
-                           z, nullptr, nullptr, n);
+        for (int ll = 0; ll < LQ; ++ll) {
+          const int l = q * LQ + ll;
+          LevelCorners lc;
+          level_corners(a.grid, l, ux, uy, uz, lc);
+          const float4* t = tab + a.grid.off[l];
+          float4 v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = __ldg(t + lc.idx[c]);
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
+            a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
+          }
+          g[4 * ll] = a0; g[4 * ll + 1] = a1; g[4 * ll + 2] = a2; g[4 * ll + 3] = a3;
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < N::NINP; ++j) z[j] = 0.0f;
+        for (int j = 0; j < GQ; ++j) g[j] = 0.0f;
       }
+      tc::store_feats<GQ>(xbuf[0], xbuf[0] + xlo[0], R, r, q * GQ, g);
+      if constexpr (N::PRODUCT) {
+        float e[16];
 #pragma unroll
-      for (int j = N::NINP; j < T::KIN; ++j) z[j] = 0.0f;
-#pragma unroll
-      for (int j = 0; j < T::KIN / 8; ++j) tc::store_chunk(xbuf[0], xbuf[0] + xlo[0], R, r, j, z + 8 * j);
+        for (int j = 0; j < 16; ++j) e[j] = 0.0f;
+        if (valid) {
+          if (q == 0) sh4(__ldg(a.wox + i), __ldg(a.woy + i), __ldg(a.woz + i), e);
+          else if (q == 1) sh4(__ldg(a.nx + i), __ldg(a.ny + i), __ldg(a.nz + i), e);
+          else if (q == 2) e[0] = __ldg(a.rough + i);
+        }
+        if (q < 3) tc::store_feats<16>(xbuf[0], xbuf[0] + xlo[0], R, r, 32 + 16 * q, e);
+      }
     }
-    float raw[N::NOUT];
+    // ---- decoder
 #pragma unroll
-    for (int k = 0; k < N::NL; ++k) {
+    for (int k = 0; k < NL - 1; ++k) {
       const int src = k & 1, dst = (k + 1) & 1;
       handoff_to_mma();
-      if (r == 0) {
+      if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF_Q + T::woff(k);
         issue_fwd(tbase, xbuf[src], xbuf[src] + xlo[src], w, w + T::wbytes(k), T::in_p(k), T::out(k));
         tc::mma_commit(mbar);
       }
       wait_mma(mbar, phase);
-      if (k < N::NL - 1) {
-        float h[N::W];
-        tmem_row<N::W>(tbase, 0, h);
-        const float* b = bias + T::boff(k) / 4;
+      float h[WQ];
+      tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), h);
+      tc::tmem_wait_ld();
+      const float* b = bias + T::boff(k) / 4;
 #pragma unroll
-        for (int j = 0; j < N::W; ++j) h[j] = fmaxf(h[j] + b[j], 0.0f);
+      for (int j = 0; j < WQ; ++j) h[j] = fmaxf(h[j] + b[q * WQ + j], 0.0f);
+      tc::store_feats<WQ>(xbuf[dst], xbuf[dst] + xlo[dst], R, r, q * WQ, h);
+    }
+    {
+      constexpr int k = NL - 1, src = k & 1;
+      handoff_to_mma();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t w = sb + T::WOFF_Q + T::woff(k);
+        issue_fwd(tbase, xbuf[src], xbuf[src] + xlo[src], w, w + T::wbytes(k), T::in_p(k), T::out(k));
+        tc::mma_commit(mbar);
+      }
+      wait_mma(mbar, phase);
+    }
+    // ---- Table 1 on this quarter's lobes
+    float lp[KQ], kp[KQ], tp[KQ], pp[KQ];
+    tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(q * KQ), lp);
+    tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(K + q * KQ), kp);
+    tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(2 * K + q * KQ), tp);
+    tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(3 * K + q * KQ), pp);
+    tc::tmem_wait_ld();
+    const float* b = bias + T::boff(NL - 1) / 4;
 #pragma unroll
-        for (int j = 0; j < N::W / 8; ++j) tc::store_chunk(xbuf[dst], xbuf[dst] + xlo[dst], R, r, j, h + 8 * j);
-      } else {
-        tmem_row<N::NOUT>(tbase, 0, raw);
-        const float* b = bias + T::boff(k) / 4;
+    for (int j = 0; j < KQ; ++j) {
+      lp[j] += b[q * KQ + j]; kp[j] += b[K + q * KQ + j];
+      tp[j] += b[2 * K + q * KQ + j]; pp[j] += b[3 * K + q * KQ + j];
+    }
+    if (a.raw && valid) {
 #pragma unroll
-        for (int j = 0; j < N::NOUT; ++j) raw[j] += b[j];
+      for (int j = 0; j < KQ; ++j) {
+        const int l = q * KQ + j;
+        a.raw[(int64_t)l * n + i] = lp[j];
+        a.raw[(int64_t)(K + l) * n + i] = kp[j];
+        a.raw[(int64_t)(2 * K + l) * n + i] = tp[j];
+        a.raw[(int64_t)(3 * K + l) * n + i] = pp[j];
       }
     }
-    if (!valid) continue;
-    // ---- Table 1 + outputs (thread per sample)
-    if (a.raw) {
+    float kap[KQ], mx[KQ], my[KQ], mz[KQ];
+    float mloc = lp[0];
 #pragma unroll
-      for (int j = 0; j < N::NOUT; ++j) a.raw[(int64_t)j * n + i] = raw[j];
+    for (int j = 0; j < KQ; ++j) {
+      mloc = fmaxf(mloc, lp[j]);
+      kap[j] = expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
+      const float th = 1.0f / (1.0f + expf(-tp[j]));
+      const float ph = 1.0f / (1.0f + expf(-pp[j]));
+      float st, ct, sp, cp;
+      sincospif(th, &st, &ct);
+      sincospif(2.0f * ph, &sp, &cp);
+      mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
     }
-    Mixture<N::K> m;
-    activate<N::K>(raw, a.log_kmin, a.log_kmax, m);
-    if (a.lambda) {
+    if (valid && a.kappa) {
 #pragma unroll
-      for (int j = 0; j < N::K; ++j) a.lambda[(int64_t)j * n + i] = m.lam[j];
+      for (int j = 0; j < KQ; ++j) a.kappa[(int64_t)(q * KQ + j) * n + i] = kap[j];
     }
-    if (a.kappa) {
+    if (valid && a.mu) {
 #pragma unroll
-      for (int j = 0; j < N::K; ++j) a.kappa[(int64_t)j * n + i] = m.kap[j];
-    }
-    if (a.mu) {
-#pragma unroll
-      for (int j = 0; j < N::K; ++j) {
-        a.mu[(int64_t)(0 * N::K + j) * n + i] = m.mx[j];
-        a.mu[(int64_t)(1 * N::K + j) * n + i] = m.my[j];
-        a.mu[(int64_t)(2 * N::K + j) * n + i] = m.mz[j];
+      for (int j = 0; j < KQ; ++j) {
+        a.mu[(int64_t)(q * KQ + j) * n + i] = mx[j];
+        a.mu[(int64_t)(K + q * KQ + j) * n + i] = my[j];
+        a.mu[(int64_t)(2 * K + q * KQ + j) * n + i] = mz[j];
       }
     }
-    if (a.pdf) a.pdf[i] = mixture_pdf<N::K>(m, __ldg(a.wx + i), __ldg(a.wy + i), __ldg(a.wz + i));
+    RS(0, q) = mloc;
+    __syncthreads();
+    const float M = fmaxf(fmaxf(RS(0, 0), RS(0, 1)), fmaxf(RS(0, 2), RS(0, 3)));
+    float e[KQ], S = 0.0f, P = 0.0f;
+    const bool want_pdf = a.pdf != nullptr;
+    float qx = 0.f, qy = 0.f, qz = 0.f;
+    if (want_pdf) { qx = __ldg(a.wx + ic); qy = __ldg(a.wy + ic); qz = __ldg(a.wz + ic); }
+#pragma unroll
+    for (int j = 0; j < KQ; ++j) {
+      e[j] = expf(lp[j] - M);
+      S += e[j];
+      if (want_pdf) P += e[j] * lobe_pdf(kap[j], mx[j], my[j], mz[j], qx, qy, qz);
+    }
+    RS(1, q) = S;
+    RS(2, q) = P;
+    __syncthreads();
+    float B[5];
+    B[0] = 0.0f;
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) B[qq + 1] = B[qq] + RS(1, qq);
+    const float invS = 1.0f / B[4];
+    if (valid && a.lambda) {
+#pragma unroll
+      for (int j = 0; j < KQ; ++j) a.lambda[(int64_t)(q * KQ + j) * n + i] = e[j] * invS;
+    }
+    if (want_pdf && q == 0 && valid) a.pdf[i] = (RS(2, 0) + RS(2, 1) + RS(2, 2) + RS(2, 3)) * invS;
     if (a.do_sample) {
       float3 u;
-      if (a.u) u = make_float3(__ldg(a.u + i), __ldg(a.u + n + i), __ldg(a.u + 2 * n + i));
-      else u = philox_uniforms(a.seed, (uint64_t)i + a.offset);
-      float wx, wy, wz;
-      mixture_sample<N::K>(m, u.x, u.y, u.z, wx, wy, wz);
-      a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
-      a.spdf[i] = mixture_pdf<N::K>(m, wx, wy, wz);
+      if (a.u) u = make_float3(__ldg(a.u + ic), __ldg(a.u + n + ic), __ldg(a.u + 2 * n + ic));
+      else u = philox_uniforms(a.seed, (uint64_t)ic + a.offset);
+      const bool before = u.x < B[q] * invS;                 // an earlier quarter owns u1
+      const bool after = u.x >= B[q + 1] * invS && q < 3;    // a later quarter owns u1
+      if (!before && !after) {
+        int sel = KQ - 1;
+        float cum = B[q];
+#pragma unroll
+        for (int j = 0; j < KQ - 1; ++j) {
+          cum += e[j];
+          if (sel == KQ - 1 && u.x < cum * invS) sel = j;
+        }
+        float kk = kap[0], mmx = mx[0], mmy = my[0], mmz = mz[0];
+#pragma unroll
+        for (int j = 1; j < KQ; ++j)
+          if (sel == j) { kk = kap[j]; mmx = mx[j]; mmy = my[j]; mmz = mz[j]; }
+        float wx, wy, wz;
+        lobe_sample(kk, mmx, mmy, mmz, u.y, u.z, wx, wy, wz);
+        RS(3, 0) = wx; RS(3, 1) = wy; RS(3, 2) = wz;
+      }
+      __syncthreads();
+      const float wx = RS(3, 0), wy = RS(3, 1), wz = RS(3, 2);
+      float P2 = 0.0f;
+#pragma unroll
+      for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_pdf(kap[j], mx[j], my[j], mz[j], wx, wy, wz);
+      RS(4, q) = P2;
+      __syncthreads();
+      if (q == 0 && valid) {
+        a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
+        a.spdf[i] = (RS(4, 0) + RS(4, 1) + RS(4, 2) + RS(4, 3)) * invS;
+      }
     }
   }
   teardown_cta(tbase, T::TCOLS_QUERY);
@@ -345,7 +473,7 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
   float* red = reinterpret_cast<float*>(smem + T::RED_T);   // [3][4][R]
   const int64_t n = a.n;
   const int64_t ntiles = (n + R - 1) / R;
-  uint32_t phase = 0, first = 1;
+  uint32_t phase = 0, phase_dw = 0, first = 1;
   double loss = 0.0;
   unsigned c_used = 0, c_zero = 0, c_drop = 0;
   uint32_t xhi[NL], xlo[NL];
@@ -388,6 +516,11 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
       } else {
 #pragma unroll
         for (int j = 0; j < GQ; ++j) g[j] = 0.0f;
+      }
+      // SEP_D: the previous tile's deferred dW batch reads X_0 .. X_{NL-1} and the
+      // deltas; the gathers above overlapped it, wait before overwriting.
+      if constexpr (T::SEP_D) {
+        if (!first) wait_mma(mbar + 1, phase_dw);
       }
       tc::store_feats<GQ>(xhi[0], xlo[0], R, r, q * GQ, g);
       // conditioning / ones features [NGRID, ZF)
@@ -549,8 +682,15 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF_T + T::woff(k);
         issue_dx(tbase, dhi, dlo, w, w + T::wbytes(k), T::out(k), k > 0 ? W : N::NGRID);
-        issue_dw(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, T::out(k), first);
-        tc::mma_commit(mbar);
+        if constexpr (T::SEP_D) {
+          // commit the dX alone; dW_k^T runs behind it while the threads build delta_{k-1}
+          tc::mma_commit(mbar);
+          issue_dw(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, T::out(k), first);
+          if (k == 0) tc::mma_commit(mbar + 1);
+        } else {
+          issue_dw(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, T::out(k), first);
+          tc::mma_commit(mbar);
+        }
       }
       wait_mma(mbar, phase);
       if (k > 0) {
@@ -560,8 +700,12 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
         const uint32_t mk = mask[k];
 #pragma unroll
         for (int j = 0; j < WQ; ++j) d[j] = ((mk >> j) & 1u) ? d[j] : 0.0f;
-        dhi = xhi[k];                       // delta_{k-1} overwrites X_k (its dW MMA completed)
-        dlo = xhi[k] + (W / 8) * CH;
+        if constexpr (T::SEP_D) {
+          dhi = sb + T::dhoff(k - 1);
+        } else {
+          dhi = xhi[k];                     // delta_{k-1} overwrites X_k (its dW MMA completed)
+        }
+        dlo = dhi + (W / 8) * CH;
         tc::store_feats<WQ>(dhi, dlo, R, r, q * WQ, d);
       } else {
         float dz[GQ];
@@ -590,6 +734,7 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
   // ---- flush dW^T / db: lane r = input feature r (r == in: bias); quarter q
   // takes columns [q out/4, (q+1) out/4)
   if (!first) {
+    if constexpr (T::SEP_D) wait_mma(mbar + 1, phase_dw);   // last tile's deferred dW batch
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -627,18 +772,18 @@ struct TcLaunch {
     using T = TC<N>;
     cudaFuncSetAttribute(tc_query_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
     const int64_t ntiles = (a.n + R - 1) / R;
-    const int per_sm = (int)((227u * 1024u) / (T::SMEM_QUERY + 1024u));
-    const int64_t cap = (int64_t)sms * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));
+    // 512 threads x ~112 registers: one CTA per SM (persistent over tiles)
+    const int64_t cap = (int64_t)sms;
     const int blocks = (int)(ntiles < cap ? ntiles : cap);
-    tc_query_kernel<N><<<blocks, R, T::SMEM_QUERY, st>>>(a);
+    tc_query_kernel<N><<<blocks, 4 * R, T::SMEM_QUERY, st>>>(a);
     return 1;
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
     using T = TC<N>;
     cudaFuncSetAttribute(tc_train_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_TRAIN);
     const int64_t ntiles = (a.n + R - 1) / R;
-    const int per_sm = (int)((227u * 1024u) / (T::SMEM_TRAIN + 1024u));
-    const int64_t cap = (int64_t)sms * (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm));
+    // 512 threads, ~150 KB smem: one CTA per SM
+    const int64_t cap = (int64_t)sms;
     const int blocks = (int)(ntiles < cap ? ntiles : cap);
     tc_train_kernel<N><<<blocks, 4 * R, T::SMEM_TRAIN, st>>>(a);
     return 1;
