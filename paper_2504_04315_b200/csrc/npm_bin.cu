@@ -1,0 +1,129 @@
+// npm_bin.cu -- spatial binning of a sample batch: counting sort by the Morton
+// code of the sample's cell in a 16^3 grid over the scene AABB.  Not part of
+// the method: it only reorders the processing of independent samples so that
+// the 32 samples of a warp are spatially clustered and their grid gathers hit
+// few cache lines.  Results are independent of
+// the order up to fp32 summation order.
+//
+// Pass 1 (bin_count): each CTA histograms its contiguous chunk in smem and
+//   adds its non-zero bins to the global histogram (one atomic per
+//   (CTA, bin), not per sample: the samples lie on surfaces, so a few bins
+//   are hot and per-sample atomics serialise on them).
+// Pass 2 (bin_scan): exclusive scan of the 4096 bin totals (one CTA).
+// Pass 3 (bin_place): each CTA re-histograms its chunk, reserves its range in
+//   every non-zero bin with one atomic, then places its samples with smem
+//   atomics.
+#include "npm_kernels.cuh"
+
+namespace npm {
+namespace {
+
+constexpr int kBins = 1 << kBinBits;
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {   // 4 bits -> every third bit
+  v &= 0xFu;
+  v = (v | (v << 8)) & 0x0100F00Fu;
+  v = (v | (v << 4)) & 0x010C30C3u;
+  v = (v | (v << 2)) & 0x01249249u;
+  return v;
+}
+
+__device__ __forceinline__ uint32_t bin_key(const float* px, const float* py, const float* pz, int64_t i,
+                                            const GridDesc& g) {
+  const float ux = normalize_axis(__ldg(px + i), g.lo[0], g.inv[0]);
+  const float uy = normalize_axis(__ldg(py + i), g.lo[1], g.inv[1]);
+  const float uz = normalize_axis(__ldg(pz + i), g.lo[2], g.inv[2]);
+  const uint32_t cx = min((uint32_t)(ux * 16.0f), 15u), cy = min((uint32_t)(uy * 16.0f), 15u),
+                 cz = min((uint32_t)(uz * 16.0f), 15u);
+  return spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+}
+
+__global__ void __launch_bounds__(kThreads) bin_count_kernel(const float* __restrict__ px,
+                                                             const float* __restrict__ py,
+                                                             const float* __restrict__ pz, int64_t n,
+                                                             int64_t chunk, GridDesc g, uint32_t* __restrict__ keys,
+                                                             uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(i0 + chunk, n);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint32_t k = bin_key(px, py, pz, i, g);
+    keys[i] = k;
+    atomicAdd(h + k, 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+    if (h[b]) atomicAdd(hist + b, h[b]);
+}
+
+// Exclusive scan of kBins counters (one CTA of kThreads, kBins / kThreads each).
+__global__ void __launch_bounds__(kThreads) bin_scan_kernel(uint32_t* hist) {
+  constexpr int PER = kBins / kThreads;
+  __shared__ uint32_t warp_tot[kThreads / 32];
+  const int t = threadIdx.x;
+  uint32_t v[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { v[j] = hist[t * PER + j]; s += v[j]; }
+  uint32_t inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if ((t & 31) >= o) inc += y;
+  }
+  if ((t & 31) == 31) warp_tot[t >> 5] = inc;
+  __syncthreads();
+  if (t < 32) {
+    const uint32_t w = t < kThreads / 32 ? warp_tot[t] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (t >= o) wi += y;
+    }
+    if (t < kThreads / 32) warp_tot[t] = wi - w;
+  }
+  __syncthreads();
+  uint32_t run = warp_tot[t >> 5] + inc - s;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { hist[t * PER + j] = run; run += v[j]; }
+}
+
+__global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __restrict__ keys, int64_t n,
+                                                             int64_t chunk, uint32_t* __restrict__ cursor,
+                                                             uint32_t* __restrict__ perm) {
+  __shared__ uint32_t h[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(i0 + chunk, n);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(h + keys[i], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+    const uint32_t c = h[b];
+    h[b] = c ? atomicAdd(cursor + b, c) : 0u;   // this CTA's range in bin b
+  }
+  __syncthreads();
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint32_t slot = atomicAdd(h + keys[i], 1u);
+    perm[slot] = (uint32_t)i;
+  }
+}
+
+}  // namespace
+
+int launch_bin(const float* px, const float* py, const float* pz, int64_t n, const GridDesc& g, uint32_t* keys,
+               uint32_t* hist, uint32_t* perm, int sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  cudaMemsetAsync(hist, 0, kBins * sizeof(uint32_t), st);
+  const int64_t want = (n + 4095) / 4096;
+  const int blocks = (int)(want < (int64_t)sms * 2 ? want : (int64_t)sms * 2);
+  const int64_t chunk = (n + blocks - 1) / blocks;
+  bin_count_kernel<<<blocks, kThreads, 0, st>>>(px, py, pz, n, chunk, g, keys, hist);
+  bin_scan_kernel<<<1, kThreads, 0, st>>>(hist);
+  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, chunk, hist, perm);
+  return 3;
+}
+
+}  // namespace npm

@@ -77,6 +77,9 @@ struct npm_model {
   int64_t prof_launches[16] = {};
   double prof_ms[16] = {};
   bool use_tc = true;  // fused tcgen05 decoder (NPM_CUDACORE=1 selects the CUDA-core debug path)
+  bool use_bin = true; // spatial binning of batches >= kBinMin samples (NPM_BIN=0 disables)
+  bool bin_train = false;  // also bin training batches (NPM_BIN_TRAIN=1)
+  DevBuf bin_keys, bin_perm, bin_hist;
 };
 
 namespace {
@@ -178,8 +181,9 @@ void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryA
 }
 
 const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward", "weight_grad", "adam",
-                            "train_fused"};
-enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKTrainFused, kKinds };
+                            "train_fused", "bin"};
+enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKTrainFused, kKBin, kKinds };
+constexpr int64_t kBinMin = 4096;   // batches at least this large are spatially binned
 
 cudaEvent_t take_event(npm_model* m) {
   if (!m->pool.empty()) { cudaEvent_t e = m->pool.back(); m->pool.pop_back(); return e; }
@@ -206,6 +210,26 @@ npm_status check_launch(npm_model* m, int r) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(NPM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return NPM_OK;
+}
+
+// Spatial binning of a device-resident position batch (npm_bin.cu); returns
+// the processing order, or NULL (identity) for small batches / when disabled.
+npm_status maybe_bin(npm_model* m, const float* px, const float* py, const float* pz, int64_t n, cudaStream_t st,
+                     const uint32_t** perm) {
+  *perm = nullptr;
+  if (!m->use_tc || !m->use_bin || n < kBinMin) return NPM_OK;
+  cudaError_t e;
+  if ((e = m->bin_keys.ensure(n * sizeof(uint32_t))) != cudaSuccess ||
+      (e = m->bin_perm.ensure(n * sizeof(uint32_t))) != cudaSuccess ||
+      (e = m->bin_hist.ensure(((size_t)1 << kBinBits) * sizeof(uint32_t))) != cudaSuccess)
+    return fail(NPM_ERR_OOM, "binning scratch");
+  uint32_t* p = static_cast<uint32_t*>(m->bin_perm.p);
+  npm_status r = check_launch(m, timed(m, kKBin, st, [&] {
+    return launch_bin(px, py, pz, n, m->grid, static_cast<uint32_t*>(m->bin_keys.p),
+                      static_cast<uint32_t*>(m->bin_hist.p), p, m->num_sms, st);
+  }));
+  if (r == NPM_OK) *perm = p;
+  return r;
 }
 
 struct DeviceGuard {
@@ -280,6 +304,8 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   m->device = dev;
   m->shape = s;
   if (const char* e = getenv("NPM_CUDACORE")) m->use_tc = !(e[0] == '1');
+  if (const char* e = getenv("NPM_BIN")) m->use_bin = !(e[0] == '0');
+  if (const char* e = getenv("NPM_BIN_TRAIN")) m->bin_train = e[0] == '1';
   if (cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     delete m;
     return fail(NPM_ERR_CUDA, "no CUDA device");
@@ -358,6 +384,9 @@ npm_status npm_destroy(npm_model* m) {
   if (m->dstats) cudaFree(m->dstats);
   if (m->dcount) cudaFree(m->dcount);
   m->scratch_train.release();
+  m->bin_keys.release();
+  m->bin_perm.release();
+  m->bin_hist.release();
   for (auto& s : m->stage) s.release();
   for (auto& r : m->pending) { m->pool.push_back(r.a); m->pool.push_back(r.b); }
   for (auto e : m->pool) cudaEventDestroy(e);
@@ -530,7 +559,11 @@ npm_status npm_decode(npm_model* m, const npm_query* q, const float* feat, int u
   a.kappa = s.out(kappa, K * n);
   a.mu = s.out(mu, 3 * K * n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
-  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return (m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st)); }));
+  npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+  if (r != NPM_OK) return r;
+  r = check_launch(m, timed(m, kKQuery, st, [&] {
+    return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
+  }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -553,7 +586,11 @@ npm_status npm_pdf(npm_model* m, const npm_query* q, const float* wix, const flo
   a.wx = s.in(wix, n); a.wy = s.in(wiy, n); a.wz = s.in(wiz, n);
   a.pdf = s.out(pdf, n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
-  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return (m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st)); }));
+  npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+  if (r != NPM_OK) return r;
+  r = check_launch(m, timed(m, kKQuery, st, [&] {
+    return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
+  }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -586,7 +623,11 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   }
   a.sx = s.out(wix, n); a.sy = s.out(wiy, n); a.sz = s.out(wiz, n); a.spdf = s.out(pdf, n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
-  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return (m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st)); }));
+  npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+  if (r != NPM_OK) return r;
+  r = check_launch(m, timed(m, kKQuery, st, [&] {
+    return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
+  }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -636,11 +677,19 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.log_kmax = logf(m->cfg.kappa_max);
   a.stats = m->dstats;
   a.counters = m->dcount;
+  if (const char* e = getenv("NPM_DEBUG")) a.debug = atoi(e);   // measurement only
   // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
   const NetShape& sh = m->shape;
   if (m->use_tc) {
     CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
     CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+    // Training batches are not binned by default: measured on B200 (c2) the
+    // coherent gathers gain ~50 us but the scatter-adds then collide on the
+    // same L2 lines (+54 us) and the binning pass costs ~85 us (NPM_BIN_TRAIN=1).
+    if (m->bin_train) {
+      npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+      if (r != NPM_OK) return r;
+    }
     return check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
   }
   const size_t rows = (size_t)sh.n_in + (size_t)(sh.n_layers - 1) * sh.width  // acts

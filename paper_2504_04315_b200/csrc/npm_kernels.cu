@@ -8,24 +8,49 @@ namespace npm {
 namespace detail {
 // Adam + EMA (C-O17, C-O18); zeroes the gradient buffer.
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+  // float4 per thread; n_mlp and n_total are multiples of 4, so a vector is
+  // entirely MLP or entirely grid.  Untouched grid vectors (all g == 0) read
+  // only g, p, e and write only e.
   double gn = 0.0;
   unsigned nf = 0;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.n_total;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    float g = a.g[j];
-    const bool finite = isfinite(g);
-    if (!finite) { g = 0.0f; nf += 1; }
-    gn += (double)g * (double)g;
-    float p = a.p[j];
-    const bool skip = (j >= a.n_mlp) && g == 0.0f;  // untouched grid entry
-    if (!skip) {
-      const float m = a.beta1 * a.m[j] + (1.0f - a.beta1) * g;
-      const float v = a.beta2 * a.v[j] + (1.0f - a.beta2) * g * g;
-      p = p - a.lr * (m * a.c1) / (sqrtf(v * a.c2) + a.eps);
-      a.m[j] = m; a.v[j] = v; a.p[j] = p;
+  const int64_t n4 = a.n_total / 4;
+  float4* g4 = reinterpret_cast<float4*>(a.g);
+  float4* p4 = reinterpret_cast<float4*>(a.p);
+  float4* m4 = reinterpret_cast<float4*>(a.m);
+  float4* v4 = reinterpret_cast<float4*>(a.v);
+  float4* e4 = reinterpret_cast<float4*>(a.e);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+    float4 gv = g4[j];
+    float g[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!isfinite(g[q])) { g[q] = 0.0f; nf += 1; }
+      gn += (double)g[q] * (double)g[q];
     }
-    a.e[j] = a.decay * a.e[j] + (1.0f - a.decay) * p;
-    a.g[j] = 0.0f;
+    const bool grid = 4 * j >= a.n_mlp;
+    const bool any = g[0] != 0.0f || g[1] != 0.0f || g[2] != 0.0f || g[3] != 0.0f;
+    float4 pv = p4[j];
+    float p[4] = {pv.x, pv.y, pv.z, pv.w};
+    if (!grid || any) {
+      const float4 mv = m4[j], vv = v4[j];
+      float m[4] = {mv.x, mv.y, mv.z, mv.w}, v[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (grid && g[q] == 0.0f) continue;     // untouched grid entry
+        m[q] = a.beta1 * m[q] + (1.0f - a.beta1) * g[q];
+        v[q] = a.beta2 * v[q] + (1.0f - a.beta2) * g[q] * g[q];
+        p[q] = p[q] - a.lr * (m[q] * a.c1) / (sqrtf(v[q] * a.c2) + a.eps);
+      }
+      m4[j] = make_float4(m[0], m[1], m[2], m[3]);
+      v4[j] = make_float4(v[0], v[1], v[2], v[3]);
+      p4[j] = make_float4(p[0], p[1], p[2], p[3]);
+      g4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (gv.x != 0.0f || gv.y != 0.0f || gv.z != 0.0f || gv.w != 0.0f) {
+      g4[j] = make_float4(0.f, 0.f, 0.f, 0.f);   // non-finite entries zeroed
+    }
+    const float4 ev = e4[j];
+    e4[j] = make_float4(a.decay * ev.x + (1.0f - a.decay) * p[0], a.decay * ev.y + (1.0f - a.decay) * p[1],
+                        a.decay * ev.z + (1.0f - a.decay) * p[2], a.decay * ev.w + (1.0f - a.decay) * p[3]);
   }
   gn = warp_sum_d(gn);
   nf = warp_sum_u(nf);
@@ -149,8 +174,8 @@ int launch_encode(int L, const QueryArgs& a, int sms, cudaStream_t st) {
 }
 
 int launch_adam(const AdamArgs& a, int sms, cudaStream_t st) {
-  const int64_t need = (a.n_total + 255) / 256;
-  const int blocks = (int)(need < (int64_t)sms * 8 ? need : (int64_t)sms * 8);
+  const int64_t need = (a.n_total / 4 + 255) / 256;
+  const int blocks = (int)(need < (int64_t)sms * 16 ? need : (int64_t)sms * 16);
   adam_kernel<<<blocks, 256, 0, st>>>(a);
   return 1;
 }

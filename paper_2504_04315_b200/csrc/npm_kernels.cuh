@@ -15,6 +15,7 @@ struct NetShape {
 
 struct QueryArgs {
   int64_t n;
+  const uint32_t* perm;     // optional processing order (spatial binning); NULL = identity
   const float *px, *py, *pz, *wox, *woy, *woz, *nx, *ny, *nz, *rough;
   const float* params;      // live or EMA flat parameter buffer
   GridDesc grid;
@@ -38,6 +39,7 @@ struct QueryArgs {
 
 struct TrainArgs {
   int64_t n;
+  const uint32_t* perm;     // optional processing order (spatial binning); NULL = identity
   const float *px, *py, *pz, *wox, *woy, *woz, *nx, *ny, *nz, *rough;
   const float *wx, *wy, *wz;
   const float* target;      // [C][n]
@@ -51,6 +53,7 @@ struct TrainArgs {
   // scratch, feature-major [rows][n]
   float* act[3];            // inputs of layer k: z, h1, h2
   float* delta[3];          // d loss / d pre-activation of layer k
+  int debug;                // measurement knob (NPM_DEBUG): bit0 skip scatter, bit1 skip gathers
   double* stats;            // [0] loss, [1] unused, then int counters as double
   unsigned long long* counters;  // [0] used, [1] zero, [2] dropped
 };
@@ -79,4 +82,14 @@ int launch_train_tc(const NetShape& s, const TrainArgs& a, int num_sms, cudaStre
 int launch_init_params(float* p, int64_t n_mlp, int64_t n_total, const NetShape& s, uint64_t seed,
                        cudaStream_t st);
 
+}  // namespace npm
+
+namespace npm {
+// Spatial binning (npm_bin.cu): a counting sort of the samples by the Morton
+// code of their cell in a 16^3 grid over the AABB, so that the 32 samples of a
+// warp are spatially clustered and their grid gathers / scatter-adds touch
+// few cache lines.  perm[t] = original index of the t-th processed sample.
+constexpr int kBinBits = 12;
+int launch_bin(const float* px, const float* py, const float* pz, int64_t n, const GridDesc& g,
+               uint32_t* keys, uint32_t* hist, uint32_t* perm, int num_sms, cudaStream_t st);
 }  // namespace npm

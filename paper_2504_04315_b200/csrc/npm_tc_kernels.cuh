@@ -139,14 +139,20 @@ __device__ __forceinline__ void mma3(uint32_t d, uint64_t ahi, uint64_t alo, uin
   tc::mma_bf16(d, alo, bhi, idesc, 1u);
 }
 
+// Descriptors are built once per batch; a K step only advances the 14-bit
+// start-address field (addr >> 4 stays < 2^14 for any smem address), so each
+// further MMA costs one 64-bit add on the issuing thread.
+
 // Forward MMA: D[R x out] = X[R x K] W[out x K]^T, both K-major.
 __device__ __forceinline__ void issue_fwd(uint32_t d, uint32_t xhi, uint32_t xlo, uint32_t whi, uint32_t wlo,
                                           int K, int out) {
   const uint32_t idesc = tc::idesc_bf16(R, out, false, false);
+  const uint64_t ah = tc::sdesc(xhi, CH, 128), al = tc::sdesc(xlo, CH, 128);
+  const uint64_t bh = tc::sdesc(whi, out * 16, 128), bl = tc::sdesc(wlo, out * 16, 128);
+#pragma unroll
   for (int s = 0; s < K / 16; ++s) {
-    const uint32_t xa = (uint32_t)s * 2u * CH, wa = (uint32_t)s * 2u * (uint32_t)out * 16u;
-    mma3(d, tc::sdesc(xhi + xa, CH, 128), tc::sdesc(xlo + xa, CH, 128), tc::sdesc(whi + wa, out * 16, 128),
-         tc::sdesc(wlo + wa, out * 16, 128), idesc, s > 0 ? 1u : 0u);
+    const uint64_t xa = (uint64_t)(s * 2 * (int)CH) >> 4, wa = (uint64_t)(s * 2 * out * 16) >> 4;
+    mma3(d, ah + xa, al + xa, bh + wa, bl + wa, idesc, s > 0 ? 1u : 0u);
   }
 }
 
@@ -154,10 +160,12 @@ __device__ __forceinline__ void issue_fwd(uint32_t d, uint32_t xhi, uint32_t xlo
 __device__ __forceinline__ void issue_dx(uint32_t d, uint32_t dhi, uint32_t dlo, uint32_t whi, uint32_t wlo,
                                          int out, int nin) {
   const uint32_t idesc = tc::idesc_bf16(R, nin, false, true);
+  const uint64_t ah = tc::sdesc(dhi, CH, 128), al = tc::sdesc(dlo, CH, 128);
+  const uint64_t bh = tc::sdesc(whi, 128, out * 16), bl = tc::sdesc(wlo, 128, out * 16);
+#pragma unroll
   for (int s = 0; s < out / 16; ++s) {
-    const uint32_t da = (uint32_t)s * 2u * CH, wa = (uint32_t)s * 256u;
-    mma3(d, tc::sdesc(dhi + da, CH, 128), tc::sdesc(dlo + da, CH, 128), tc::sdesc(whi + wa, 128, out * 16),
-         tc::sdesc(wlo + wa, 128, out * 16), idesc, s > 0 ? 1u : 0u);
+    const uint64_t da = (uint64_t)(s * 2 * (int)CH) >> 4, wa = (uint64_t)(s * 256) >> 4;
+    mma3(d, ah + da, al + da, bh + wa, bl + wa, idesc, s > 0 ? 1u : 0u);
   }
 }
 
@@ -165,10 +173,12 @@ __device__ __forceinline__ void issue_dx(uint32_t d, uint32_t dhi, uint32_t dlo,
 __device__ __forceinline__ void issue_dw(uint32_t d, uint32_t xhi, uint32_t xlo, uint32_t dhi, uint32_t dlo,
                                          int out, uint32_t first) {
   const uint32_t idesc = tc::idesc_bf16(128, out, true, true);
+  const uint64_t ah = tc::sdesc(xhi, 128, CH), al = tc::sdesc(xlo, 128, CH);
+  const uint64_t bh = tc::sdesc(dhi, 128, CH), bl = tc::sdesc(dlo, 128, CH);
+#pragma unroll
   for (int s = 0; s < R / 16; ++s) {
-    const uint32_t ra = (uint32_t)s * 256u;
-    mma3(d, tc::sdesc(xhi + ra, 128, CH), tc::sdesc(xlo + ra, 128, CH), tc::sdesc(dhi + ra, 128, CH),
-         tc::sdesc(dlo + ra, 128, CH), idesc, (first && s == 0) ? 0u : 1u);
+    const uint64_t ra = (uint64_t)(s * 256) >> 4;
+    mma3(d, ah + ra, al + ra, bh + ra, bl + ra, idesc, (first && s == 0) ? 0u : 1u);
   }
 }
 
@@ -228,14 +238,15 @@ __device__ __forceinline__ void teardown_cta(uint32_t tbase, int tcols) {
 // B_q = sum_{q'<q} S_q' (S_q = sum of the quarter's e^{lambda'-M}) are
 // computed identically by the 4 threads of a row, so exactly one quarter owns
 // u1 and picks its first lobe with u1 < C_i (its last lobe at C = B_{q+1}).
-template <class N>
-__global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
+template <class N, int TPR>
+__global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a) {
   using T = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W;
-  constexpr int KQ = K / 4, WQ = W / 4, LQ = N::L / 4, GQ = 4 * LQ;
+  constexpr int KQ = K / TPR, WQ = W / TPR, LQ = N::L / TPR, GQ = 4 * LQ;
+  static_assert(K % TPR == 0 && N::L % TPR == 0, "parts");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = tc::smem_u32(smem);
-  const int tid = threadIdx.x, warp = tid >> 5, q = warp >> 2;
+  const int tid = threadIdx.x, warp = tid >> 5, q = warp >> 2;   // q: part of the row
   const int r = ((warp & 3) << 5) | (tid & 31);
   const uint32_t lane_addr = (uint32_t)((warp & 3) << 21);
   uint64_t* mbar;
@@ -244,17 +255,21 @@ __global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
   stage_weights_tc<N>(a.params, smem, T::WOFF_Q, T::BOFF_Q);
   const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
   const float* bias = reinterpret_cast<const float*>(smem + T::BOFF_Q);
-  float* red = reinterpret_cast<float*>(smem + T::RED_Q);   // [slot][4][R]
-  auto RS = [&](int slot, int qq) -> float& { return red[(slot * 4 + qq) * R + r]; };
+  float* red = reinterpret_cast<float*>(smem + T::RED_Q);   // [slot][TPR][R]
+  // slots 0..2: per-part partials; omega (3 floats) at 3 TPR R; slot 4 after it
+  auto RS = [&](int slot, int qq) -> float& {
+    return red[((slot < 3 ? slot * TPR : 3 * TPR + 3) + qq) * R + r];
+  };
   const int64_t n = a.n;
   const int64_t ntiles = (n + R - 1) / R;
   uint32_t phase = 0;
   const uint32_t xbuf[2] = {sb + T::QA, sb + T::QB};
   const uint32_t xlo[2] = {(uint32_t)(T::QAF / 8) * CH, (uint32_t)(W / 8) * CH};
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i = tile * R + r;
-    const bool valid = i < n;
-    const int64_t ic = valid ? i : 0;
+    const int64_t slot = tile * R + r;                 // processing slot (spatially binned order)
+    const bool valid = slot < n;
+    const int64_t i = valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
+    const int64_t ic = i;
     // ---- encode (Eq. 13): levels [q LQ, (q+1) LQ) + conditioning -> buffer A
     {
       float g[GQ];
@@ -289,14 +304,19 @@ __global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
       tc::store_feats<GQ>(xbuf[0], xbuf[0] + xlo[0], R, r, q * GQ, g);
       if constexpr (N::PRODUCT) {
         float e[16];
+        // extra feature blocks: 0 SH(w_o) [32,48), 1 SH(n) [48,64), 2 roughness [64,80)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) e[j] = 0.0f;
-        if (valid) {
-          if (q == 0) sh4(__ldg(a.wox + i), __ldg(a.woy + i), __ldg(a.woz + i), e);
-          else if (q == 1) sh4(__ldg(a.nx + i), __ldg(a.ny + i), __ldg(a.nz + i), e);
-          else if (q == 2) e[0] = __ldg(a.rough + i);
+        for (int blk = 0; blk < 3; ++blk) {
+          if (blk % TPR != q) continue;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) e[j] = 0.0f;
+          if (valid) {
+            if (blk == 0) sh4(__ldg(a.wox + i), __ldg(a.woy + i), __ldg(a.woz + i), e);
+            else if (blk == 1) sh4(__ldg(a.nx + i), __ldg(a.ny + i), __ldg(a.nz + i), e);
+            else e[0] = __ldg(a.rough + i);
+          }
+          tc::store_feats<16>(xbuf[0], xbuf[0] + xlo[0], R, r, 32 + 16 * blk, e);
         }
-        if (q < 3) tc::store_feats<16>(xbuf[0], xbuf[0] + xlo[0], R, r, 32 + 16 * q, e);
       }
     }
     // ---- decoder
@@ -380,7 +400,9 @@ __global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
     }
     RS(0, q) = mloc;
     __syncthreads();
-    const float M = fmaxf(fmaxf(RS(0, 0), RS(0, 1)), fmaxf(RS(0, 2), RS(0, 3)));
+    float M = RS(0, 0);
+#pragma unroll
+    for (int qq = 1; qq < TPR; ++qq) M = fmaxf(M, RS(0, qq));
     float e[KQ], S = 0.0f, P = 0.0f;
     const bool want_pdf = a.pdf != nullptr;
     float qx = 0.f, qy = 0.f, qz = 0.f;
@@ -394,22 +416,27 @@ __global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
     RS(1, q) = S;
     RS(2, q) = P;
     __syncthreads();
-    float B[5];
+    float B[TPR + 1];
     B[0] = 0.0f;
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) B[qq + 1] = B[qq] + RS(1, qq);
-    const float invS = 1.0f / B[4];
+    for (int qq = 0; qq < TPR; ++qq) B[qq + 1] = B[qq] + RS(1, qq);
+    const float invS = 1.0f / B[TPR];
     if (valid && a.lambda) {
 #pragma unroll
       for (int j = 0; j < KQ; ++j) a.lambda[(int64_t)(q * KQ + j) * n + i] = e[j] * invS;
     }
-    if (want_pdf && q == 0 && valid) a.pdf[i] = (RS(2, 0) + RS(2, 1) + RS(2, 2) + RS(2, 3)) * invS;
+    if (want_pdf && q == 0 && valid) {
+      float Pt = 0.0f;
+#pragma unroll
+      for (int qq = 0; qq < TPR; ++qq) Pt += RS(2, qq);
+      a.pdf[i] = Pt * invS;
+    }
     if (a.do_sample) {
       float3 u;
       if (a.u) u = make_float3(__ldg(a.u + ic), __ldg(a.u + n + ic), __ldg(a.u + 2 * n + ic));
       else u = philox_uniforms(a.seed, (uint64_t)ic + a.offset);
       const bool before = u.x < B[q] * invS;                 // an earlier quarter owns u1
-      const bool after = u.x >= B[q + 1] * invS && q < 3;    // a later quarter owns u1
+      const bool after = u.x >= B[q + 1] * invS && q < TPR - 1;   // a later part owns u1
       if (!before && !after) {
         int sel = KQ - 1;
         float cum = B[q];
@@ -424,10 +451,10 @@ __global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
           if (sel == j) { kk = kap[j]; mmx = mx[j]; mmy = my[j]; mmz = mz[j]; }
         float wx, wy, wz;
         lobe_sample(kk, mmx, mmy, mmz, u.y, u.z, wx, wy, wz);
-        RS(3, 0) = wx; RS(3, 1) = wy; RS(3, 2) = wz;
+        red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
       }
       __syncthreads();
-      const float wx = RS(3, 0), wy = RS(3, 1), wz = RS(3, 2);
+      const float wx = red[(3 * TPR) * R + r], wy = red[(3 * TPR) * R + R + r], wz = red[(3 * TPR) * R + 2 * R + r];
       float P2 = 0.0f;
 #pragma unroll
       for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_pdf(kap[j], mx[j], my[j], mz[j], wx, wy, wz);
@@ -435,7 +462,10 @@ __global__ void __launch_bounds__(4 * R, 1) tc_query_kernel(QueryArgs a) {
       __syncthreads();
       if (q == 0 && valid) {
         a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
-        a.spdf[i] = (RS(4, 0) + RS(4, 1) + RS(4, 2) + RS(4, 3)) * invS;
+        float Pt = 0.0f;
+#pragma unroll
+        for (int qq = 0; qq < TPR; ++qq) Pt += RS(4, qq);
+        a.spdf[i] = Pt * invS;
       }
     }
   }
@@ -484,9 +514,10 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
   }
   const uint32_t dlast_hi = sb + T::DOFF, dlast_lo = dlast_hi + (NOUT / 8) * CH;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i = tile * R + r;
-    const bool valid = i < n;
-    const int64_t ic = valid ? i : 0;
+    const int64_t slot = tile * R + r;                 // processing slot (spatially binned order)
+    const bool valid = slot < n;
+    const int64_t i = valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
+    const int64_t ic = i;
     uint32_t mask[NL];   // ReLU mask bits of this quarter's WQ columns of X_1..X_{NL-1}
     float ux = 0.f, uy = 0.f, uz = 0.f;
     // ---- encode: levels [q LQ, (q+1) LQ) -> features [q GQ, (q+1) GQ) of X0
@@ -504,7 +535,8 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
           const float4* t = tab + a.grid.off[l];
           float4 v[8];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] = __ldg(t + lc.idx[c]);
+          for (int c = 0; c < 8; ++c)
+            v[c] = (a.debug & 2) ? make_float4(lc.w[c], 0.f, 0.f, 0.f) : __ldg(t + lc.idx[c]);
           float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -711,7 +743,7 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
         float dz[GQ];
         tc::tmem_ldn<GQ>(tbase + lane_addr + (uint32_t)(q * GQ), dz);
         tc::tmem_wait_ld();
-        if (valid) {
+        if (valid && !(a.debug & 1)) {
 #pragma unroll
           for (int ll = 0; ll < LQ; ++ll) {
             const int l = q * LQ + ll;
@@ -770,12 +802,15 @@ template <class N>
 struct TcLaunch {
   static int query(const QueryArgs& a, int sms, cudaStream_t st) {
     using T = TC<N>;
-    cudaFuncSetAttribute(tc_query_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
+    // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA
+    // waits interleave); ~104 KB smem each.
+    constexpr int TPR = 2;
+    cudaFuncSetAttribute(tc_query_kernel<N, TPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
     const int64_t ntiles = (a.n + R - 1) / R;
-    // 512 threads x ~112 registers: one CTA per SM (persistent over tiles)
-    const int64_t cap = (int64_t)sms;
+    const int per_sm = (int)((228u * 1024u) / (T::SMEM_QUERY + 1024u)) >= 2 ? 2 : 1;
+    const int64_t cap = (int64_t)sms * per_sm;
     const int blocks = (int)(ntiles < cap ? ntiles : cap);
-    tc_query_kernel<N><<<blocks, 4 * R, T::SMEM_QUERY, st>>>(a);
+    tc_query_kernel<N, TPR><<<blocks, TPR * R, T::SMEM_QUERY, st>>>(a);
     return 1;
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
