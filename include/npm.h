@@ -43,11 +43,13 @@
  *     may run concurrently with each other; a training call must not overlap
  *     queries on the same model (training happens between render waves).
  *
- * Supported configurations (validated by npm_create): n_features = 4;
- * 1 <= n_levels <= 16; 1 <= n_lobes <= 16 ; decoder shapes
- * {n_in 16, width 32, 2 layers}, {n_in 32, width 64, 3 layers},
- * {n_in 64, width 64, 3 layers}, {product: n_in 65, width 64, 3 layers};
- * 4*n_lobes must be 32 or 64.
+ * Supported configurations (validated by npm_create; the decoder kernels are
+ * compiled per shape): n_features = 4 and
+ *   radiance, L = 4, K = 8,  2 affine layers of width 32  (n_in 16)  [c1]
+ *   radiance, L = 8, K = 8,  3 affine layers of width 64  (n_in 32)  [c2, c3]
+ *   radiance, L = 16, K = 8, 3 affine layers of width 64  (n_in 64)  [c5]
+ *   product,  L = 8, K = 16, 3 affine layers of width 64  (n_in 65)  [c4]
+ * with any D_1 < D_L, log2_hashmap, AABB.  Anything else -> NPM_ERR_INVALID.
  */
 #ifndef NPM_H
 #define NPM_H
