@@ -690,6 +690,31 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
       if (r != NPM_OK) return r;
     }
+    if (a.debug & 4) {   // measurement only: per-phase clock stamps of CTA 0
+      static long long* dclk = nullptr;
+      if (!dclk) cudaMalloc(&dclk, 64 * 16 * sizeof(long long));
+      cudaMemsetAsync(dclk, 0, 64 * 16 * sizeof(long long), st);
+      a.dbg_clock = dclk;
+      npm_status r = check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
+      long long h[64 * 16];
+      cudaMemcpyAsync(h, dclk, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      double acc[16] = {};
+      int cnt = 0;
+      for (int t = 1; t < 64; ++t) {   // skip tile 0 (weight staging)
+        if (h[t * 16 + 15] == 0) break;
+        for (int j = 1; j < 16; ++j) {
+          const long long prev = (j == 13) ? h[t * 16 + 12] : h[t * 16 + j - 1];
+          if (h[t * 16 + j]) acc[j] += (double)(h[t * 16 + j] - prev);
+        }
+        acc[0] += (double)(h[t * 16 + 15] - h[t * 16 + 0]);
+        ++cnt;
+      }
+      fprintf(stderr, "NPM_PHASES tiles=%d total=%.0f", cnt, cnt ? acc[0] / cnt : 0.0);
+      for (int j = 1; j < 16; ++j) if (j < 13 || j == 15) fprintf(stderr, " p%d=%.0f", j, cnt ? acc[j] / cnt : 0.0);
+      fprintf(stderr, "\n");
+      return r;
+    }
     return check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
   }
   const size_t rows = (size_t)sh.n_in + (size_t)(sh.n_layers - 1) * sh.width  // acts

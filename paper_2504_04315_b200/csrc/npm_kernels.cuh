@@ -53,7 +53,9 @@ struct TrainArgs {
   // scratch, feature-major [rows][n]
   float* act[3];            // inputs of layer k: z, h1, h2
   float* delta[3];          // d loss / d pre-activation of layer k
-  int debug;                // measurement knob (NPM_DEBUG): bit0 skip scatter, bit1 skip gathers
+  int debug;                // measurement knob (NPM_DEBUG): bit0 skip scatter, bit1 skip gathers,
+                            // bit2 record per-phase clock64 stamps of CTA 0 into dbg_clock
+  long long* dbg_clock;     // [64 tiles][16 stamps] (debug only)
   double* stats;            // [0] loss, [1] unused, then int counters as double
   unsigned long long* counters;  // [0] used, [1] zero, [2] dropped
 };

@@ -513,42 +513,69 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
     xlo[k] = xhi[k] + (T::xfeat(k) / 8) * CH;
   }
   const uint32_t dlast_hi = sb + T::DOFF, dlast_lo = dlast_hi + (NOUT / 8) * CH;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t slot = tile * R + r;                 // processing slot (spatially binned order)
-    const bool valid = slot < n;
-    const int64_t i = valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
+  int tile_no = 0;
+  const bool stamp = (a.debug & 4) && blockIdx.x == 0 && tid == 0;
+#define NPM_STAMP(idx) \
+  do { if (stamp && tile_no < 64) a.dbg_clock[tile_no * 16 + (idx)] = clock64(); } while (0)
+  // Per-tile record inputs of this thread (its row, its levels).  The encode of
+  // tile t+1 (index, position, gathers) is issued while tile t's last backward
+  // MMA batch runs; only the smem stores wait for that batch.
+  struct TileIn {
+    int64_t i;
+    bool valid;
+    float ux, uy, uz;
+    float g[GQ];
+  };
+  auto load_tile = [&](int64_t tl, TileIn& t) {
+    const int64_t slot = tl * R + r;                  // processing slot (binned order if perm)
+    t.valid = slot < n;
+    t.i = t.valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
+    t.ux = t.uy = t.uz = 0.f;
+    if (t.valid) {
+      t.ux = normalize_axis(__ldg(a.px + t.i), a.grid.lo[0], a.grid.inv[0]);
+      t.uy = normalize_axis(__ldg(a.py + t.i), a.grid.lo[1], a.grid.inv[1]);
+      t.uz = normalize_axis(__ldg(a.pz + t.i), a.grid.lo[2], a.grid.inv[2]);
+#pragma unroll
+      for (int ll = 0; ll < LQ; ++ll) {
+        const int l = q * LQ + ll;
+        LevelCorners lc;
+        level_corners(a.grid, l, t.ux, t.uy, t.uz, lc);
+        const float4* tb = tab + a.grid.off[l];
+        float4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          v[c] = (a.debug & 2) ? make_float4(lc.w[c], 0.f, 0.f, 0.f) : __ldg(tb + lc.idx[c]);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
+          a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
+        }
+        t.g[4 * ll] = a0; t.g[4 * ll + 1] = a1; t.g[4 * ll + 2] = a2; t.g[4 * ll + 3] = a3;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < GQ; ++j) t.g[j] = 0.0f;
+    }
+  };
+  TileIn cur;
+  if (blockIdx.x < ntiles) load_tile(blockIdx.x, cur);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_no) {
+    NPM_STAMP(0);
+    const bool valid = cur.valid;
+    const int64_t i = cur.i;
     const int64_t ic = i;
+    const float ux = cur.ux, uy = cur.uy, uz = cur.uz;
+    // head inputs: issued now, consumed after the forward MMAs
+    const float h_wx = __ldg(a.wx + ic), h_wy = __ldg(a.wy + ic), h_wz = __ldg(a.wz + ic);
+    const float h_t0 = __ldg(a.target + ic);
+    const float h_t1 = a.channels == 3 ? __ldg(a.target + n + ic) : 0.f;
+    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * n + ic) : 0.f;
+    const float h_p = __ldg(a.spdf + ic);
     uint32_t mask[NL];   // ReLU mask bits of this quarter's WQ columns of X_1..X_{NL-1}
-    float ux = 0.f, uy = 0.f, uz = 0.f;
     // ---- encode: levels [q LQ, (q+1) LQ) -> features [q GQ, (q+1) GQ) of X0
     {
-      float g[GQ];
-      if (valid) {
-        ux = normalize_axis(__ldg(a.px + i), a.grid.lo[0], a.grid.inv[0]);
-        uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
-        uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
-#pragma unroll
-        for (int ll = 0; ll < LQ; ++ll) {
-          const int l = q * LQ + ll;
-          LevelCorners lc;
-          level_corners(a.grid, l, ux, uy, uz, lc);
-          const float4* t = tab + a.grid.off[l];
-          float4 v[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            v[c] = (a.debug & 2) ? make_float4(lc.w[c], 0.f, 0.f, 0.f) : __ldg(t + lc.idx[c]);
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
-            a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
-          }
-          g[4 * ll] = a0; g[4 * ll + 1] = a1; g[4 * ll + 2] = a2; g[4 * ll + 3] = a3;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < GQ; ++j) g[j] = 0.0f;
-      }
+      float* g = cur.g;
       // SEP_D: the previous tile's deferred dW batch reads X_0 .. X_{NL-1} and the
       // deltas; the gathers above overlapped it, wait before overwriting.
       if constexpr (T::SEP_D) {
@@ -589,6 +616,7 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       handoff_to_mma();
+      NPM_STAMP(1 + 2 * k);
       if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF_T + T::woff(k);
@@ -596,6 +624,7 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
         tc::mma_commit(mbar);
       }
       wait_mma(mbar, phase);
+      NPM_STAMP(2 + 2 * k);
       const float* b = bias + T::boff(k) / 4;
       if (k < NL - 1) {
         float h[WQ];
@@ -626,23 +655,23 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
           lp[j] += b[q * KQ + j]; kp[j] += b[K + q * KQ + j];
           tp[j] += b[2 * K + q * KQ + j]; pp[j] += b[3 * K + q * KQ + j];
         }
-        // record scale (every quarter evaluates it for its row)
-        float t = __ldg(a.target + ic);
+        // record scale (every quarter evaluates it for its row; inputs prefetched)
+        float t = h_t0;
         bool all_zero = t == 0.0f;
         if (a.channels == 3) {
-          const float tg = __ldg(a.target + n + ic), tb = __ldg(a.target + 2 * n + ic);
-          all_zero = all_zero && tg == 0.0f && tb == 0.0f;
-          t = 0.2126f * t + 0.7152f * tg + 0.0722f * tb;
+          all_zero = all_zero && h_t1 == 0.0f && h_t2 == 0.0f;
+          t = 0.2126f * t + 0.7152f * h_t1 + 0.0722f * h_t2;
         }
-        const float p = __ldg(a.spdf + ic);
+        const float p = h_p;
         const float ratio = t / p;
         const bool drop = valid && (!isfinite(ratio) || !isfinite(p) || !(p > 0.0f));
         const bool zero = valid && !drop && all_zero;
         const bool use = valid && !drop && !zero;
         const float s = use ? (float)(-(double)ratio * a.inv_n_global) : 0.0f;
-        const float wx = __ldg(a.wx + ic), wy = __ldg(a.wy + ic), wz = __ldg(a.wz + ic);
+        const float wx = h_wx, wy = h_wy, wz = h_wz;
         // own lobes: kappa, mu, v_i(w)
         float kap[KQ], mx[KQ], my[KQ], mz[KQ], th[KQ], ph[KQ], v[KQ];
+        float sth[KQ], cth[KQ], sph[KQ], cph[KQ];
         float mloc = lp[0];
 #pragma unroll
         for (int j = 0; j < KQ; ++j) {
@@ -650,10 +679,9 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
           kap[j] = expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
           th[j] = 1.0f / (1.0f + expf(-tp[j]));
           ph[j] = 1.0f / (1.0f + expf(-pp[j]));
-          float st, ct, sp, cp;
-          sincospif(th[j], &st, &ct);
-          sincospif(2.0f * ph[j], &sp, &cp);
-          mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
+          sincospif(th[j], &sth[j], &cth[j]);
+          sincospif(2.0f * ph[j], &sph[j], &cph[j]);
+          mx[j] = sth[j] * cph[j]; my[j] = sth[j] * sph[j]; mz[j] = cth[j];
           v[j] = lobe_pdf(kap[j], mx[j], my[j], mz[j], wx, wy, wz);
         }
         // softmax max over all K lambda' (cross-quarter)
@@ -686,9 +714,7 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
           const float em = -expm1f(-2.0f * kap[j]);
           const float dkk = s * gam * (1.0f - kap[j] * 0.5f * d2 - 2.0f * kap[j] * expf(-2.0f * kap[j]) / em);
           dk[j] = (kp[j] < a.log_kmin || kp[j] > a.log_kmax) ? 0.0f : dkk;
-          float st, ct, sp, cp;
-          sincospif(th[j], &st, &ct);
-          sincospif(2.0f * ph[j], &sp, &cp);
+          const float st = sth[j], ct = cth[j], sp = sph[j], cp = cph[j];
           const float wdth = kPi * (ct * cp * wx + ct * sp * wy - st * wz);
           const float wdph = kTwoPi * (-st * sp * wx + st * cp * wy);
           const float sgk = s * gam * kap[j];
@@ -707,9 +733,11 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
     }
     // ---- backward
     uint32_t dhi = dlast_hi, dlo = dlast_lo;
+    TileIn nxt;
 #pragma unroll
     for (int k = NL - 1; k >= 0; --k) {
       handoff_to_mma();
+      NPM_STAMP(1 + 2 * NL + 2 * (NL - 1 - k));
       if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF_T + T::woff(k);
@@ -724,7 +752,10 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
           tc::mma_commit(mbar);
         }
       }
+      // next tile's encode (index, position, gathers) overlaps the last MMA batch
+      if (k == 0 && tile + gridDim.x < ntiles) load_tile(tile + gridDim.x, nxt);
       wait_mma(mbar, phase);
+      NPM_STAMP(2 + 2 * NL + 2 * (NL - 1 - k));
       if (k > 0) {
         float d[WQ];
         tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), d);
@@ -762,7 +793,10 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
       }
     }
     first = 0;
+    NPM_STAMP(15);
+    cur = nxt;
   }
+#undef NPM_STAMP
   // ---- flush dW^T / db: lane r = input feature r (r == in: bias); quarter q
   // takes columns [q out/4, (q+1) out/4)
   if (!first) {
