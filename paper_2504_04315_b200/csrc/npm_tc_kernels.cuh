@@ -774,19 +774,39 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
         float dz[GQ];
         tc::tmem_ldn<GQ>(tbase + lane_addr + (uint32_t)(q * GQ), dz);
         tc::tmem_wait_ld();
-        if (valid && !(a.debug & 1)) {
+        if (!(a.debug & 1)) {
 #pragma unroll
           for (int ll = 0; ll < LQ; ++ll) {
             const int l = q * LQ + ll;
             const float g0 = dz[4 * ll], g1 = dz[4 * ll + 1], g2 = dz[4 * ll + 2], g3 = dz[4 * ll + 3];
-            if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f && g3 == 0.0f) continue;
             LevelCorners lc;
             level_corners(a.grid, l, ux, uy, uz, lc);
             float4* t = gtab + a.grid.off[l];
+            // Warp-uniform cell (spatially binned batches, coarse levels): reduce
+            // the 8 weighted corner updates over the warp, one RED per corner.
+            const uint32_t c0 = valid ? lc.idx[0] : 0xFFFFFFFFu;
+            const bool uniform = __all_sync(0xffffffffu, c0 == __shfl_sync(0xffffffffu, c0, 0) && valid);
+            if (uniform) {
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float w = lc.w[c];
-              atomicAdd(t + lc.idx[c], make_float4(w * g0, w * g1, w * g2, w * g3));
+              for (int c = 0; c < 8; ++c) {
+                const float w = lc.w[c];
+                float s0 = w * g0, s1 = w * g1, s2 = w * g2, s3 = w * g3;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                  s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                  s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                  s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                  s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+                }
+                if ((tid & 31) == 0 && (s0 != 0.0f || s1 != 0.0f || s2 != 0.0f || s3 != 0.0f))
+                  atomicAdd(t + lc.idx[c], make_float4(s0, s1, s2, s3));
+              }
+            } else if (valid && (g0 != 0.0f || g1 != 0.0f || g2 != 0.0f || g3 != 0.0f)) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const float w = lc.w[c];
+                atomicAdd(t + lc.idx[c], make_float4(w * g0, w * g1, w * g2, w * g3));
+              }
             }
           }
         }
