@@ -285,8 +285,18 @@ def main():
     else:
         algo = per_unit.get(kname, 0) * units
     achieved = algo / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    traffic = None   # dram bytes per launch from the committed ncu --set full capture (profiles/traffic.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("workload") == name:
+            traffic = tj["dram_bytes_per_launch"].get(kname)
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "kernel": kname, "kernel_ms_per_launch": kms / max(kl, 1),
+            "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)" if traffic else None,
+            "algorithmic_bytes_per_launch": per_unit.get(kname, 0) * n,
+            "kernel": kname, "kernel_ms_per_launch": kms / max(kl, 1),
             "kernel_share_of_step": (kms / 1e3) / t_tot if t_tot > 0 else None, "peak_source": src,
             "per_unit_bytes": per_unit.get(kname), "units_per_launch": n}
 
