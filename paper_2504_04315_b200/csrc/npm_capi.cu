@@ -678,6 +678,7 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.stats = m->dstats;
   a.counters = m->dcount;
   if (const char* e = getenv("NPM_DEBUG")) a.debug = atoi(e);   // measurement only
+  if (const char* e = getenv("NPM_TRAIN128")) a.legacy = e[0] == '1';
   // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
   const NetShape& sh = m->shape;
   if (m->use_tc) {

@@ -56,6 +56,7 @@ struct TrainArgs {
   int debug;                // measurement knob (NPM_DEBUG): bit0 skip scatter, bit1 skip gathers,
                             // bit2 record per-phase clock64 stamps of CTA 0 into dbg_clock
   long long* dbg_clock;     // [64 tiles][16 stamps] (debug only)
+  int legacy;               // 1: one 128-sample tile per CTA (tc_train_kernel) instead of two 64-sample tiles
   double* stats;            // [0] loss, [1] unused, then int counters as double
   unsigned long long* counters;  // [0] used, [1] zero, [2] dropped
 };

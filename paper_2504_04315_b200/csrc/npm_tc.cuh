@@ -141,6 +141,70 @@ __device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
   }
 }
 
+// 16 lanes x (8 X) fp32 columns ("16x256b.xX"): thread t of the warp gets
+// lanes {t/4, t/4 + 8} (relative to the address lane) and, in repetition j,
+// columns 8j + 2(t%4) + {0, 1}.  Register order: v[w + 2 half + 4 j].
+template <int X>
+__device__ __forceinline__ void tmem_ld16dp(uint32_t taddr, float* v) {
+  static_assert(X == 1 || X == 2 || X == 4 || X == 8, "x");
+  uint32_t r[4 * X];
+  if constexpr (X == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+  } else if constexpr (X == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+  } else if constexpr (X == 4) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+  } else {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+  }
+#pragma unroll
+  for (int i = 0; i < 4 * X; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Zero 16 fp32 columns of this warp's 32 TMEM lanes.
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" :: "r"(taddr), "r"(z) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Named barrier over `count` threads (id 1..15; id 0 is __syncthreads).
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void split_pack(float a, float b, uint32_t& hi, uint32_t& lo);
+
+// Store one bf16 pair (features f, f+1 of a row), split hi/lo, chunk-major.
+__device__ __forceinline__ void store_pair(uint32_t hi_base, uint32_t lo_base, int rows, int row, int f, float a,
+                                           float b) {
+  uint32_t h, l;
+  split_pack(a, b, h, l);
+  const uint32_t off = (uint32_t)((f / 8) * rows * 16 + row * 16 + (f % 8) * 2);
+  asm volatile("st.shared.b32 [%0], %1;" :: "r"(hi_base + off), "r"(h) : "memory");
+  asm volatile("st.shared.b32 [%0], %1;" :: "r"(lo_base + off), "r"(l) : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }

@@ -852,6 +852,474 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
   teardown_cta(tbase, T::TCOLS_TRAIN);
 }
 
+// ---------------------------------------------------------------------------
+// Two-tile training kernel: a CTA (512 threads) runs two independent 64-sample
+// tiles, one per 256-thread group g = warp / 8, so one group's MMA round trips
+// and epilogues overlap the other's.  MMAs are M = 64 (cta_group::1): row r of
+// an accumulator lives in TMEM lane 32 (r / 16) + r % 16; warp (quarter
+// Q = warp % 4, h = (warp / 4) % 2) reads its 16 rows with tcgen05.ld
+// 16x256b: thread t gets rows r0 = 16 Q + t / 4 and r0 + 8, column pairs
+// 8 j + 2 (t % 4).  Ownership per thread (c = t % 4):
+//   encode / scatter: row r0 + 8 (c & 1), levels h L/2 + 2 j + c / 2 (j < L/4)
+//   hidden epilogues: both rows, columns [h W/2, (h+1) W/2) (pairs 2c)
+//   Eq. 9 head:       row r0 + 8 h, lobes 8 jj + 2 c + {0,1} (4 threads of a
+//                     row are adjacent lanes: softmax / mixture sums by shuffles)
+// The weight-gradient accumulators (M = 128 over features, K = the 64 samples
+// of a tile) are shared by both groups; zeroed once, always accumulated.
+template <class N>
+struct TC64 {
+  using B = TC<N>;
+  static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN;
+  static constexpr int RT = 64;
+  static constexpr uint32_t CHT = RT * 16;
+  static constexpr int ZF = B::ZF, HF = B::HF;
+  __host__ __device__ static constexpr uint32_t xfeat(int k) { return k == 0 ? ZF : HF; }
+  __host__ __device__ static constexpr uint32_t xoff(int k) {
+    return k == 0 ? 0u : xoff(k - 1) + 2u * (xfeat(k - 1) / 8) * CHT;
+  }
+  static constexpr uint32_t DOFF = xoff(NL);
+  static constexpr uint32_t GBYTES = DOFF + 2u * (NOUT / 8) * CHT;
+  static constexpr uint32_t WOFF = 2u * GBYTES;
+  static constexpr uint32_t BOFF = WOFF + B::WBYTES;
+  static constexpr uint32_t MISC = (BOFF + B::BBYTES + 127u) & ~127u;
+  // dW^T A operands read 16 feature chunks (M = 128) from a lo base
+  __host__ __device__ static constexpr uint32_t overread(int k) {
+    return GBYTES + xoff(k) + (xfeat(k) / 8) * CHT + 16u * CHT;
+  }
+  __host__ __device__ static constexpr uint32_t max_overread(int k) {
+    return k < 0 ? 0u : (overread(k) > max_overread(k - 1) ? overread(k) : max_overread(k - 1));
+  }
+  static constexpr uint32_t SMEM_RAW = MISC + 64;
+  static constexpr uint32_t SMEM = SMEM_RAW > max_overread(NL - 1) ? SMEM_RAW : max_overread(NL - 1);
+  __host__ __device__ static constexpr int dwcol(int k) { return k == 0 ? 128 : dwcol(k - 1) + B::out(k - 1); }
+  static constexpr int DWCOLS = dwcol(NL) - 128;
+  static constexpr int TCOLS = 512;
+};
+
+template <int ROWS>
+__device__ __forceinline__ void issue_fwd_r(uint32_t d, uint32_t xhi, uint32_t xlo, uint32_t whi, uint32_t wlo,
+                                            int K, int out) {
+  constexpr uint32_t CHR = ROWS * 16;
+  const uint32_t idesc = tc::idesc_bf16(ROWS, out, false, false);
+  const uint64_t ah = tc::sdesc(xhi, CHR, 128), al = tc::sdesc(xlo, CHR, 128);
+  const uint64_t bh = tc::sdesc(whi, out * 16, 128), bl = tc::sdesc(wlo, out * 16, 128);
+#pragma unroll
+  for (int s = 0; s < K / 16; ++s) {
+    const uint64_t xa = (uint64_t)(s * 2 * (int)CHR) >> 4, wa = (uint64_t)(s * 2 * out * 16) >> 4;
+    mma3(d, ah + xa, al + xa, bh + wa, bl + wa, idesc, s > 0 ? 1u : 0u);
+  }
+}
+
+template <int ROWS>
+__device__ __forceinline__ void issue_dx_r(uint32_t d, uint32_t dhi, uint32_t dlo, uint32_t whi, uint32_t wlo,
+                                           int out, int nin) {
+  constexpr uint32_t CHR = ROWS * 16;
+  const uint32_t idesc = tc::idesc_bf16(ROWS, nin, false, true);
+  const uint64_t ah = tc::sdesc(dhi, CHR, 128), al = tc::sdesc(dlo, CHR, 128);
+  const uint64_t bh = tc::sdesc(whi, 128, out * 16), bl = tc::sdesc(wlo, 128, out * 16);
+#pragma unroll
+  for (int s = 0; s < out / 16; ++s) {
+    const uint64_t da = (uint64_t)(s * 2 * (int)CHR) >> 4, wa = (uint64_t)(s * 256) >> 4;
+    mma3(d, ah + da, al + da, bh + wa, bl + wa, idesc, s > 0 ? 1u : 0u);
+  }
+}
+
+// dW^T[128 feats x out] += X^T delta over the ROWS samples of a tile (always accumulates)
+template <int ROWS>
+__device__ __forceinline__ void issue_dw_r(uint32_t d, uint32_t xhi, uint32_t xlo, uint32_t dhi, uint32_t dlo,
+                                           int out) {
+  constexpr uint32_t CHR = ROWS * 16;
+  const uint32_t idesc = tc::idesc_bf16(128, out, true, true);
+  const uint64_t ah = tc::sdesc(xhi, 128, CHR), al = tc::sdesc(xlo, 128, CHR);
+  const uint64_t bh = tc::sdesc(dhi, 128, CHR), bl = tc::sdesc(dlo, 128, CHR);
+#pragma unroll
+  for (int s = 0; s < ROWS / 16; ++s) {
+    const uint64_t ra = (uint64_t)(s * 256) >> 4;
+    mma3(d, ah + ra, al + ra, bh + ra, bl + ra, idesc, 1u);
+  }
+}
+
+template <class N>
+__global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
+  using T = TC64<N>;
+  using TB = TC<N>;
+  constexpr int NL = N::NL, K = N::K, W = N::W, NOUT = N::NOUT, L = N::L;
+  constexpr int RT = T::RT;
+  constexpr uint32_t CHT = T::CHT;
+  constexpr int WH = W / 2, XH = WH / 8;        // hidden cols per warp-pair half, 16dp reps
+  constexpr int LJ = L / 4;                     // levels per thread (encode / scatter)
+  constexpr int KJ = K / 8;                     // lobe groups of 8 per raw parameter block
+  constexpr int KL = K / 4;                     // lobes per thread in the head
+  static_assert(K % 8 == 0 && L % 4 == 0 && W % 16 == 0, "two-tile kernel shape");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp >> 3, wq = warp & 3, h = (warp >> 2) & 1, c = lane & 3;
+  const int gtid = tid & 255;
+  const int r0 = 16 * wq + (lane >> 2);
+  const int re = r0 + 8 * (c & 1);              // encode / scatter row
+  const int rh = r0 + 8 * h;                    // head row
+  const uint32_t qaddr = (uint32_t)(wq * 32) << 16;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + T::MISC);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::MISC + 32);
+  if (tid == 0) {
+    tc::mbar_init(mbar, 1);
+    tc::mbar_init(mbar + 1, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, (uint32_t)T::TCOLS);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tslot;
+  stage_weights_tc<N>(a.params, smem, T::WOFF, T::BOFF);
+  // zero the shared dW^T accumulators (all later MMAs accumulate)
+  for (int col = 16 * (warp >> 2); col < T::DWCOLS; col += 64)
+    tc::tmem_zero16(tbase + qaddr + (uint32_t)(128 + col));
+  tc::tmem_wait_st();
+  const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
+  float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
+  const float* bias = reinterpret_cast<const float*>(smem + T::BOFF);
+  uint64_t* gbar = mbar + g;
+  const uint32_t gsb = sb + (uint32_t)g * T::GBYTES;
+  uint32_t xhi[NL], xlo[NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    xhi[k] = gsb + T::xoff(k);
+    xlo[k] = xhi[k] + (T::xfeat(k) / 8) * CHT;
+  }
+  const uint32_t dlast_hi = gsb + T::DOFF, dlast_lo = dlast_hi + (NOUT / 8) * CHT;
+  // constant "ones" features (bias rows of dW^T): X_0 at NIN (radiance), X_k at W
+  if (gtid < RT) {
+    const float e1[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, e0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if constexpr (!N::PRODUCT) {
+#pragma unroll
+      for (int f = N::NGRID; f < T::ZF; f += 8) tc::store_chunk(xhi[0], xlo[0], RT, gtid, f / 8, f == N::NGRID ? e1 : e0);
+    }
+#pragma unroll
+    for (int k = 1; k < NL; ++k) tc::store_chunk(xhi[k], xlo[k], RT, gtid, W / 8, e1);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + RT - 1) / RT;
+  uint32_t phase = 0;
+  double loss = 0.0;
+  unsigned c_used = 0, c_zero = 0, c_drop = 0;
+  auto gsync = [&]() { tc::named_sync(1u + (uint32_t)g, 256u); };
+  auto handoff = [&]() {
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    gsync();
+  };
+  struct TileIn {
+    int64_t i;
+    bool valid;
+    float ux, uy, uz;
+    float gf[4 * LJ];
+  };
+  auto load_tile = [&](int64_t tl, TileIn& t) {
+    const int64_t slot = tl * RT + re;
+    t.valid = slot < n;
+    t.i = t.valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
+    t.ux = t.uy = t.uz = 0.f;
+    if (t.valid) {
+      t.ux = normalize_axis(__ldg(a.px + t.i), a.grid.lo[0], a.grid.inv[0]);
+      t.uy = normalize_axis(__ldg(a.py + t.i), a.grid.lo[1], a.grid.inv[1]);
+      t.uz = normalize_axis(__ldg(a.pz + t.i), a.grid.lo[2], a.grid.inv[2]);
+#pragma unroll
+      for (int j = 0; j < LJ; ++j) {
+        const int l = h * (L / 2) + 2 * j + (c >> 1);
+        LevelCorners lc;
+        level_corners(a.grid, l, t.ux, t.uy, t.uz, lc);
+        const float4* tb = tab + a.grid.off[l];
+        float4 v[8];
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          v[cc] = (a.debug & 2) ? make_float4(lc.w[cc], 0.f, 0.f, 0.f) : __ldg(tb + lc.idx[cc]);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          a0 = fmaf(lc.w[cc], v[cc].x, a0); a1 = fmaf(lc.w[cc], v[cc].y, a1);
+          a2 = fmaf(lc.w[cc], v[cc].z, a2); a3 = fmaf(lc.w[cc], v[cc].w, a3);
+        }
+        t.gf[4 * j] = a0; t.gf[4 * j + 1] = a1; t.gf[4 * j + 2] = a2; t.gf[4 * j + 3] = a3;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4 * LJ; ++j) t.gf[j] = 0.0f;
+    }
+  };
+  const int64_t first_tile = (int64_t)blockIdx.x * 2 + g;
+  const int64_t tstride = (int64_t)gridDim.x * 2;
+  TileIn cur;
+  if (first_tile < ntiles) load_tile(first_tile, cur);
+  for (int64_t tile = first_tile; tile < ntiles; tile += tstride) {
+    const bool evalid = cur.valid;
+    const float ux = cur.ux, uy = cur.uy, uz = cur.uz;
+    // head row inputs (consumed after the forward MMAs)
+    const int64_t hslot = tile * RT + rh;
+    const bool hvalid = hslot < n;
+    const int64_t ih = hvalid ? (a.perm ? (int64_t)__ldg(a.perm + hslot) : hslot) : 0;
+    const float h_wx = __ldg(a.wx + ih), h_wy = __ldg(a.wy + ih), h_wz = __ldg(a.wz + ih);
+    const float h_t0 = __ldg(a.target + ih);
+    const float h_t1 = a.channels == 3 ? __ldg(a.target + n + ih) : 0.f;
+    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * n + ih) : 0.f;
+    const float h_p = __ldg(a.spdf + ih);
+    uint32_t mask[NL];
+    // ---- encode stores: this thread's levels of row re
+#pragma unroll
+    for (int j = 0; j < LJ; ++j) {
+      const int l = h * (L / 2) + 2 * j + (c >> 1);
+      tc::store_feats<4>(xhi[0], xlo[0], RT, re, 4 * l, cur.gf + 4 * j);
+    }
+    if constexpr (N::PRODUCT) {
+      // per row: SH(w_o) [32,48) by (h0, c0/c1), SH(n) [48,64) by (h0, c2/c3),
+      // roughness + ones [64,80) by (h1, c0/c1)
+      const int64_t ie = cur.i;
+      float e[16];
+      const int blk = h == 0 ? (c >> 1) : (c < 2 ? 2 : 3);
+      if (blk < 3) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) e[j] = 0.0f;
+        if (blk == 0 && evalid) sh4(__ldg(a.wox + ie), __ldg(a.woy + ie), __ldg(a.woz + ie), e);
+        if (blk == 1 && evalid) sh4(__ldg(a.nx + ie), __ldg(a.ny + ie), __ldg(a.nz + ie), e);
+        if (blk == 2) {
+          e[0] = evalid ? __ldg(a.rough + ie) : 0.0f;
+          e[1] = 1.0f;   // feature NIN = 65: ones (bias row of dW_0^T)
+        }
+        tc::store_feats<16>(xhi[0], xlo[0], RT, re, 32 + 16 * blk, e);
+      }
+    }
+    // ---- forward
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      handoff();
+      if (gtid == 0) {
+        tc::fence_after_sync();
+        const uint32_t w = sb + T::WOFF + TB::woff(k);
+        issue_fwd_r<RT>(tbase + (uint32_t)(64 * g), xhi[k], xlo[k], w, w + TB::wbytes(k), TB::in_p(k), TB::out(k));
+        tc::mma_commit(gbar);
+      }
+      wait_mma(gbar, phase);
+      const float* b = bias + TB::boff(k) / 4;
+      if (k < NL - 1) {
+        float v[4 * XH];
+        tc::tmem_ld16dp<XH>(tbase + qaddr + (uint32_t)(64 * g + WH * h), v);
+        tc::tmem_wait_ld();
+        uint32_t mk = 0;
+#pragma unroll
+        for (int j = 0; j < XH; ++j) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int col = WH * h + 8 * j + 2 * c;
+            const int idx = 2 * half + 4 * j;
+            const float y0 = fmaxf(v[idx] + b[col], 0.0f), y1 = fmaxf(v[idx + 1] + b[col + 1], 0.0f);
+            mk |= (y0 > 0.0f ? 1u : 0u) << (idx);
+            mk |= (y1 > 0.0f ? 1u : 0u) << (idx + 1);
+            tc::store_pair(xhi[k + 1], xlo[k + 1], RT, r0 + 8 * half, col, y0, y1);
+          }
+        }
+        mask[k + 1] = mk;
+      } else {
+        // ---- Eq. 9 head (C-O12, C-O13): row rh, lobes 8 jj + 2 c + w
+        float v[2 * NOUT / 8 * 2];   // 16x256b x(NOUT/8): both row halves
+        tc::tmem_ld16dp<NOUT / 8>(tbase + qaddr + (uint32_t)(64 * g), v);
+        tc::tmem_wait_ld();
+        float lp[KL], kp[KL], tp[KL], pp[KL];
+#pragma unroll
+        for (int jj = 0; jj < KJ; ++jj) {
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const int m = 2 * jj + w, lobe = 8 * jj + 2 * c + w;
+            const int base = w + 2 * h;
+            lp[m] = v[base + 4 * (0 * KJ + jj)] + b[lobe];
+            kp[m] = v[base + 4 * (1 * KJ + jj)] + b[K + lobe];
+            tp[m] = v[base + 4 * (2 * KJ + jj)] + b[2 * K + lobe];
+            pp[m] = v[base + 4 * (3 * KJ + jj)] + b[3 * K + lobe];
+          }
+        }
+        float t = h_t0;
+        bool all_zero = t == 0.0f;
+        if (a.channels == 3) {
+          all_zero = all_zero && h_t1 == 0.0f && h_t2 == 0.0f;
+          t = 0.2126f * t + 0.7152f * h_t1 + 0.0722f * h_t2;
+        }
+        const float p = h_p;
+        const float ratio = t / p;
+        const bool drop = hvalid && (!isfinite(ratio) || !isfinite(p) || !(p > 0.0f));
+        const bool zero = hvalid && !drop && all_zero;
+        const bool use = hvalid && !drop && !zero;
+        const float s = use ? (float)(-(double)ratio * a.inv_n_global) : 0.0f;
+        const float wx = h_wx, wy = h_wy, wz = h_wz;
+        float kap[KL], mx[KL], my[KL], mz[KL], th[KL], ph[KL], vv[KL], sth[KL], cth[KL], sph[KL], cph[KL];
+        float mloc = lp[0];
+#pragma unroll
+        for (int m = 0; m < KL; ++m) {
+          mloc = fmaxf(mloc, lp[m]);
+          kap[m] = expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
+          th[m] = 1.0f / (1.0f + expf(-tp[m]));
+          ph[m] = 1.0f / (1.0f + expf(-pp[m]));
+          sincospif(th[m], &sth[m], &cth[m]);
+          sincospif(2.0f * ph[m], &sph[m], &cph[m]);
+          mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
+          vv[m] = lobe_pdf(kap[m], mx[m], my[m], mz[m], wx, wy, wz);
+        }
+        // the 4 threads of a row are lanes 4i..4i+3: reduce with xor 1, 2
+        mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
+        mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2));
+        float e[KL], S = 0.0f, P = 0.0f;
+#pragma unroll
+        for (int m = 0; m < KL; ++m) {
+          e[m] = expf(lp[m] - mloc);
+          S += e[m];
+          P += e[m] * vv[m];
+        }
+        S += __shfl_xor_sync(0xffffffffu, S, 1);
+        S += __shfl_xor_sync(0xffffffffu, S, 2);
+        P += __shfl_xor_sync(0xffffffffu, P, 1);
+        P += __shfl_xor_sync(0xffffffffu, P, 2);
+        const float invS = 1.0f / S;
+        const float Vb = fmaxf(P * invS, kVFloor);
+        const float invV = 1.0f / Vb;
+#pragma unroll
+        for (int jj = 0; jj < KJ; ++jj) {
+          float dl[2], dk[2], dt[2], dp[2];
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const int m = 2 * jj + w;
+            const float lam = e[m] * invS;
+            const float gam = lam * vv[m] * invV;
+            dl[w] = s * (gam - lam);
+            const float dx = mx[m] - wx, dy = my[m] - wy, dz = mz[m] - wz;
+            const float d2 = dx * dx + dy * dy + dz * dz;
+            const float em = -expm1f(-2.0f * kap[m]);
+            const float dkk = s * gam * (1.0f - kap[m] * 0.5f * d2 - 2.0f * kap[m] * expf(-2.0f * kap[m]) / em);
+            dk[w] = (kp[m] < a.log_kmin || kp[m] > a.log_kmax) ? 0.0f : dkk;
+            const float wdth = kPi * (cth[m] * cph[m] * wx + cth[m] * sph[m] * wy - sth[m] * wz);
+            const float wdph = kTwoPi * (-sth[m] * sph[m] * wx + sth[m] * cph[m] * wy);
+            const float sgk = s * gam * kap[m];
+            dt[w] = sgk * wdth * th[m] * (1.0f - th[m]);
+            dp[w] = sgk * wdph * ph[m] * (1.0f - ph[m]);
+          }
+          const int f = 8 * jj + 2 * c;
+          tc::store_pair(dlast_hi, dlast_lo, RT, rh, f, dl[0], dl[1]);
+          tc::store_pair(dlast_hi, dlast_lo, RT, rh, K + f, dk[0], dk[1]);
+          tc::store_pair(dlast_hi, dlast_lo, RT, rh, 2 * K + f, dt[0], dt[1]);
+          tc::store_pair(dlast_hi, dlast_lo, RT, rh, 3 * K + f, dp[0], dp[1]);
+        }
+        if (c == 0) {
+          c_drop += drop; c_zero += zero;
+          if (use) { loss += (double)s * (double)logf(Vb); c_used += 1; }
+        }
+      }
+    }
+    // ---- backward
+    uint32_t dhi = dlast_hi, dlo = dlast_lo;
+    TileIn nxt;
+#pragma unroll
+    for (int k = NL - 1; k >= 0; --k) {
+      handoff();
+      if (gtid == 0) {
+        tc::fence_after_sync();
+        const uint32_t w = sb + T::WOFF + TB::woff(k);
+        issue_dx_r<RT>(tbase + (uint32_t)(64 * g), dhi, dlo, w, w + TB::wbytes(k), TB::out(k), k > 0 ? W : N::NGRID);
+        issue_dw_r<RT>(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, TB::out(k));
+        tc::mma_commit(gbar);
+      }
+      if (k == 0 && tile + tstride < ntiles) load_tile(tile + tstride, nxt);
+      wait_mma(gbar, phase);
+      if (k > 0) {
+        float v[4 * XH];
+        tc::tmem_ld16dp<XH>(tbase + qaddr + (uint32_t)(64 * g + WH * h), v);
+        tc::tmem_wait_ld();
+        const uint32_t mk = mask[k];
+        // delta_{k-1} overwrites X_k's first W features (hi and lo); its ones chunk stays
+        dhi = xhi[k];
+        dlo = xlo[k];
+#pragma unroll
+        for (int j = 0; j < XH; ++j) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int col = WH * h + 8 * j + 2 * c;
+            const int idx = 2 * half + 4 * j;
+            const float d0 = ((mk >> idx) & 1u) ? v[idx] : 0.0f;
+            const float d1 = ((mk >> (idx + 1)) & 1u) ? v[idx + 1] : 0.0f;
+            tc::store_pair(dhi, dlo, RT, r0 + 8 * half, col, d0, d1);
+          }
+        }
+      } else {
+        // dz: warp half h holds grid features [2 L h, 2 L (h+1)); pair lanes c, c^1
+        // exchange so each holds the 4 features of level h L/2 + 2 j + c/2 of row re
+        float v[4 * LJ];
+        tc::tmem_ld16dp<LJ>(tbase + qaddr + (uint32_t)(64 * g + 2 * L * h), v);
+        tc::tmem_wait_ld();
+        const bool odd = c & 1;
+#pragma unroll
+        for (int j = 0; j < LJ; ++j) {
+          const float s0 = odd ? v[4 * j + 0] : v[4 * j + 2];   // the partner's row
+          const float s1 = odd ? v[4 * j + 1] : v[4 * j + 3];
+          const float r0v = __shfl_xor_sync(0xffffffffu, s0, 1);
+          const float r1v = __shfl_xor_sync(0xffffffffu, s1, 1);
+          float gq[4];
+          if (!odd) { gq[0] = v[4 * j]; gq[1] = v[4 * j + 1]; gq[2] = r0v; gq[3] = r1v; }
+          else { gq[0] = r0v; gq[1] = r1v; gq[2] = v[4 * j + 2]; gq[3] = v[4 * j + 3]; }
+          if (evalid && !(a.debug & 1) && (gq[0] != 0.0f || gq[1] != 0.0f || gq[2] != 0.0f || gq[3] != 0.0f)) {
+            const int l = h * (L / 2) + 2 * j + (c >> 1);
+            LevelCorners lc;
+            level_corners(a.grid, l, ux, uy, uz, lc);
+            float4* tg = gtab + a.grid.off[l];
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const float w = lc.w[cc];
+              atomicAdd(tg + lc.idx[cc], make_float4(w * gq[0], w * gq[1], w * gq[2], w * gq[3]));
+            }
+          }
+        }
+      }
+    }
+    cur = nxt;
+  }
+  // ---- flush dW^T / db (M = 128 layout: lane = input feature; quarter = warp / 4)
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  {
+    const int q = warp >> 2, r = ((warp & 3) << 5) | lane;
+    const uint32_t lane_addr = (uint32_t)((warp & 3) << 21);
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      constexpr int MAXO = (NOUT > W ? NOUT : W) / 4;
+      float vv[MAXO];
+      const int out = TB::out(k), in = TB::in(k), oq = out / 4;
+      if (out == NOUT) tc::tmem_ldn<NOUT / 4>(tbase + lane_addr + (uint32_t)(T::dwcol(k) + q * (NOUT / 4)), vv);
+      else tc::tmem_ldn<W / 4>(tbase + lane_addr + (uint32_t)(T::dwcol(k) + q * (W / 4)), vv);
+      tc::tmem_wait_ld();
+      if (r < in) {
+        float* gp = a.grads + N::gw_off(k) + r;
+        for (int o = 0; o < oq; ++o) atomicAdd(gp + (q * oq + o) * in, vv[o]);
+      } else if (r == in) {
+        float* gp = a.grads + N::gb_off(k);
+        for (int o = 0; o < oq; ++o) atomicAdd(gp + q * oq + o, vv[o]);
+      }
+    }
+  }
+  loss = warp_sum_d(loss);
+  c_used = warp_sum_u(c_used); c_zero = warp_sum_u(c_zero); c_drop = warp_sum_u(c_drop);
+  if (lane == 0) {
+    atomicAdd(a.stats, loss);
+    atomicAdd(a.counters + 0, (unsigned long long)c_used);
+    atomicAdd(a.counters + 1, (unsigned long long)c_zero);
+    atomicAdd(a.counters + 2, (unsigned long long)c_drop);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tbase, (uint32_t)T::TCOLS);
+}
+
 template <class N>
 struct TcLaunch {
   static int query(const QueryArgs& a, int sms, cudaStream_t st) {
@@ -869,6 +1337,14 @@ struct TcLaunch {
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
     using T = TC<N>;
+    if (!a.legacy) {   // two 64-sample tiles per CTA (tc_train64_kernel)
+      using T64 = TC64<N>;
+      cudaFuncSetAttribute(tc_train64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T64::SMEM);
+      const int64_t pairs = (a.n + 2 * T64::RT - 1) / (2 * T64::RT);
+      const int blocks = (int)(pairs < (int64_t)sms ? pairs : (int64_t)sms);
+      tc_train64_kernel<N><<<blocks, 512, T64::SMEM, st>>>(a);
+      return 1;
+    }
     cudaFuncSetAttribute(tc_train_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_TRAIN);
     const int64_t ntiles = (a.n + R - 1) / R;
     // 512 threads, ~150 KB smem: one CTA per SM
