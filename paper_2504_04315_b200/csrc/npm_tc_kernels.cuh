@@ -373,18 +373,20 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
         a.raw[(int64_t)(3 * K + l) * n + i] = pp[j];
       }
     }
-    float kap[KQ], mx[KQ], my[KQ], mz[KQ];
+    float kap[KQ], mx[KQ], my[KQ], mz[KQ], nrm[KQ];
     float mloc = lp[0];
 #pragma unroll
     for (int j = 0; j < KQ; ++j) {
       mloc = fmaxf(mloc, lp[j]);
-      kap[j] = expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
-      const float th = 1.0f / (1.0f + expf(-tp[j]));
-      const float ph = 1.0f / (1.0f + expf(-pp[j]));
+      kap[j] = __expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
+      const float th = fast_sigmoid(tp[j]);
+      const float ph = fast_sigmoid(pp[j]);
       float st, ct, sp, cp;
-      sincospif(th, &st, &ct);
-      sincospif(2.0f * ph, &sp, &cp);
+      __sincosf(kPi * th, &st, &ct);
+      __sincosf(kTwoPi * ph, &sp, &cp);
       mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
+      float em;
+      nrm[j] = lobe_norm(kap[j], em);
     }
     if (valid && a.kappa) {
 #pragma unroll
@@ -409,9 +411,9 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
     if (want_pdf) { qx = __ldg(a.wx + ic); qy = __ldg(a.wy + ic); qz = __ldg(a.wz + ic); }
 #pragma unroll
     for (int j = 0; j < KQ; ++j) {
-      e[j] = expf(lp[j] - M);
+      e[j] = __expf(lp[j] - M);
       S += e[j];
-      if (want_pdf) P += e[j] * lobe_pdf(kap[j], mx[j], my[j], mz[j], qx, qy, qz);
+      if (want_pdf) P += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], qx, qy, qz);
     }
     RS(1, q) = S;
     RS(2, q) = P;
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       const float wx = red[(3 * TPR) * R + r], wy = red[(3 * TPR) * R + R + r], wz = red[(3 * TPR) * R + 2 * R + r];
       float P2 = 0.0f;
 #pragma unroll
-      for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_pdf(kap[j], mx[j], my[j], mz[j], wx, wy, wz);
+      for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
       RS(4, q) = P2;
       __syncthreads();
       if (q == 0 && valid) {
@@ -1155,17 +1157,19 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         const float s = use ? (float)(-(double)ratio * a.inv_n_global) : 0.0f;
         const float wx = h_wx, wy = h_wy, wz = h_wz;
         float kap[KL], mx[KL], my[KL], mz[KL], th[KL], ph[KL], vv[KL], sth[KL], cth[KL], sph[KL], cph[KL];
+        float emk[KL];
         float mloc = lp[0];
 #pragma unroll
         for (int m = 0; m < KL; ++m) {
           mloc = fmaxf(mloc, lp[m]);
-          kap[m] = expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
-          th[m] = 1.0f / (1.0f + expf(-tp[m]));
-          ph[m] = 1.0f / (1.0f + expf(-pp[m]));
-          sincospif(th[m], &sth[m], &cth[m]);
-          sincospif(2.0f * ph[m], &sph[m], &cph[m]);
+          kap[m] = __expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
+          th[m] = fast_sigmoid(tp[m]);
+          ph[m] = fast_sigmoid(pp[m]);
+          __sincosf(kPi * th[m], &sth[m], &cth[m]);
+          __sincosf(kTwoPi * ph[m], &sph[m], &cph[m]);
           mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
-          vv[m] = lobe_pdf(kap[m], mx[m], my[m], mz[m], wx, wy, wz);
+          const float nrm = lobe_norm(kap[m], emk[m]);
+          vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);
         }
         // the 4 threads of a row are lanes 4i..4i+3: reduce with xor 1, 2
         mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
@@ -1173,7 +1177,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         float e[KL], S = 0.0f, P = 0.0f;
 #pragma unroll
         for (int m = 0; m < KL; ++m) {
-          e[m] = expf(lp[m] - mloc);
+          e[m] = __expf(lp[m] - mloc);
           S += e[m];
           P += e[m] * vv[m];
         }
@@ -1195,8 +1199,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
             dl[w] = s * (gam - lam);
             const float dx = mx[m] - wx, dy = my[m] - wy, dz = mz[m] - wz;
             const float d2 = dx * dx + dy * dy + dz * dz;
-            const float em = -expm1f(-2.0f * kap[m]);
-            const float dkk = s * gam * (1.0f - kap[m] * 0.5f * d2 - 2.0f * kap[m] * expf(-2.0f * kap[m]) / em);
+            // 2 kappa e^{-2 kappa} / (1 - e^{-2 kappa}) with em = 1 - e^{-2 kappa}
+            const float dkk = s * gam * (1.0f - kap[m] * 0.5f * d2 - __fdividef(2.0f * kap[m] * (1.0f - emk[m]), emk[m]));
             dk[w] = (kp[m] < a.log_kmin || kp[m] > a.log_kmax) ? 0.0f : dkk;
             const float wdth = kPi * (cth[m] * cph[m] * wx + cth[m] * sph[m] * wy - sth[m] * wz);
             const float wdph = kTwoPi * (-sth[m] * sph[m] * wx + sth[m] * cph[m] * wy);
