@@ -166,14 +166,15 @@ def main():
     from paper_2504_04315_b200.dp import DataParallel
 
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = "WORLD_SIZE" in os.environ   # launched by torchrun (also world size 1)
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     name = args.workload
     cfg = CONFIGS[name]
     n = cfg["n"] if name != "c3" else cfg["n_global"] // world
     m = npm.Model(local, **cfg["model"])
-    dp = DataParallel(m, world)
+    dp = DataParallel(m, world, force_allreduce=distributed)
     # inputs resident in HBM (device-timed value)
     qb = synth.query_batch(n, seed=100 + rank, product=m.product)
     tb = synth.training_batch(n, seed=200 + rank, product=m.product)
@@ -330,7 +331,7 @@ def main():
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
                 "clocks": clk.summary(), "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

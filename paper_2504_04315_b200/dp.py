@@ -56,13 +56,14 @@ class NpmTrainer:
 
 
 class DataParallel:
-    def __init__(self, model, world=None, group=None):
+    def __init__(self, model, world=None, group=None, force_allreduce=False):
         self.t = model if hasattr(model, "accumulate") else NpmTrainer(model)
         self.world = world if world is not None else (dist.get_world_size() if dist.is_initialized() else 1)
         self.group = group
+        self.reduce = self.world > 1 or force_allreduce   # force: exercise the collective at world size 1
 
     def allreduce_grads(self):
-        if self.world > 1:
+        if self.reduce:
             dist.all_reduce(self.t.grad_tensor(), op=dist.ReduceOp.SUM, group=self.group)
 
     def train_step(self, q, wi, target, spdf, n_local=None, n_global=None, want_stats=False):
