@@ -87,12 +87,31 @@ __device__ __forceinline__ void level_corners(const GridDesc& g, int l, float ux
   cell_axis(uy, d, iy, fy);
   cell_axis(uz, d, iz, fz);
   const bool hashed = (g.hashed_mask >> l) & 1u;
-  const float gx[2] = {1.0f - fx, fx}, gy[2] = {1.0f - fy, fy}, gz[2] = {1.0f - fz, fz};
+  const float gx0 = 1.0f - fx, gy0 = 1.0f - fy, gz0 = 1.0f - fz;
+  // w_c = (gx * gy) * gz, the same product order as corner-by-corner
+  const float wxy[4] = {gx0 * gy0, fx * gy0, gx0 * fy, fx * fy};
+  // Same integer results as corner_index() per corner, built incrementally:
+  // dense  base + cx + D cy + D^2 cz;  hashed  (x ^ y P1 ^ z P2) with
+  // (y + 1) P1 = y P1 + P1 (mod 2^32).
+  uint32_t ox[2], oy[2], oz[2];
+  if (!hashed) {
+    const uint32_t ud = (uint32_t)d;
+    const uint32_t base = (uint32_t)ix + ud * ((uint32_t)iy + ud * (uint32_t)iz);
+    ox[0] = base; ox[1] = base + 1u;
+    oy[0] = 0u; oy[1] = ud;
+    oz[0] = 0u; oz[1] = ud * ud;
+  } else {
+    const uint32_t hy = (uint32_t)iy * 2654435761u, hz = (uint32_t)iz * 805459861u;
+    ox[0] = (uint32_t)ix; ox[1] = (uint32_t)ix + 1u;
+    oy[0] = hy; oy[1] = hy + 2654435761u;
+    oz[0] = hz; oz[1] = hz + 805459861u;
+  }
+  const uint32_t mask = g.tsize[l] - 1u;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
-    lc.idx[c] = corner_index((uint32_t)(ix + cx), (uint32_t)(iy + cy), (uint32_t)(iz + cz), d, g.tsize[l], hashed);
-    lc.w[c] = gx[cx] * gy[cy] * gz[cz];
+    lc.idx[c] = hashed ? ((ox[cx] ^ oy[cy] ^ oz[cz]) & mask) : (ox[cx] + oy[cy] + oz[cz]);
+    lc.w[c] = wxy[c & 3] * (cz ? fz : gz0);
   }
 }
 

@@ -74,6 +74,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       :: "r"(smem_u32(mbar)), "r"(parity) : "memory");
 }
 
+// Same wait with a suspend-time hint: the thread sleeps in the try_wait until
+// the phase completes (or ~1 ms passes) instead of re-polling.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "NPM_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra NPM_WAITS_%=;\n\t}\n"
+      :: "r"(smem_u32(mbar)), "r"(parity), "r"(1000000u) : "memory");
+}
+
 // TMEM allocation: executed by one full warp; writes the base address to smem.
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"

@@ -1011,6 +1011,14 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
   double loss = 0.0;
   unsigned c_used = 0, c_zero = 0, c_drop = 0;
   auto gsync = [&]() { tc::named_sync(1u + (uint32_t)g, 256u); };
+  // One warp of the group polls the MMA mbarrier; the other seven sleep in the
+  // named barrier instead of spinning (the spin loop was ~9 % of all issued
+  // instructions, competing with the other group's work).
+  auto gwait = [&]() {
+    tc::mbar_wait_sleep(gbar, phase);
+    phase ^= 1u;
+    tc::fence_after_sync();
+  };
   auto handoff = [&]() {
     tc::fence_proxy_async();
     tc::fence_before_sync();
@@ -1105,7 +1113,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         issue_fwd_r<RT>(tbase + (uint32_t)(64 * g), xhi[k], xlo[k], w, w + TB::wbytes(k), TB::in_p(k), TB::out(k));
         tc::mma_commit(gbar);
       }
-      wait_mma(gbar, phase);
+      gwait();
       const float* b = bias + TB::boff(k) / 4;
       if (k < NL - 1) {
         float v[4 * XH];
@@ -1118,7 +1126,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
           for (int half = 0; half < 2; ++half) {
             const int col = WH * h + 8 * j + 2 * c;
             const int idx = 2 * half + 4 * j;
-            const float y0 = fmaxf(v[idx] + b[col], 0.0f), y1 = fmaxf(v[idx + 1] + b[col + 1], 0.0f);
+            const float2 bb = *reinterpret_cast<const float2*>(b + col);   // col even: 8-byte aligned
+            const float y0 = fmaxf(v[idx] + bb.x, 0.0f), y1 = fmaxf(v[idx + 1] + bb.y, 0.0f);
             mk |= (y0 > 0.0f ? 1u : 0u) << (idx);
             mk |= (y1 > 0.0f ? 1u : 0u) << (idx + 1);
             tc::store_pair(xhi[k + 1], xlo[k + 1], RT, r0 + 8 * half, col, y0, y1);
@@ -1234,7 +1243,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         tc::mma_commit(gbar);
       }
       if (k == 0 && tile + tstride < ntiles) load_tile(tile + tstride, nxt);
-      wait_mma(gbar, phase);
+      gwait();
       if (k > 0) {
         float v[4 * XH];
         tc::tmem_ld16dp<XH>(tbase + qaddr + (uint32_t)(64 * g + WH * h), v);

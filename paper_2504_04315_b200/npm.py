@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnpm.so")
+LIB_PATH = os.environ.get("NPM_LIB") or os.path.join(_HERE, "libnpm.so")   # NPM_LIB: A/B builds
 
 RADIANCE, PRODUCT = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_ADAM_M, BUF_ADAM_V, BUF_EMA = range(5)
