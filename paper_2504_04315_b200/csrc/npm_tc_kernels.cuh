@@ -265,10 +265,31 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
   uint32_t phase = 0;
   const uint32_t xbuf[2] = {sb + T::QA, sb + T::QB};
   const uint32_t xlo[2] = {(uint32_t)(T::QAF / 8) * CH, (uint32_t)(W / 8) * CH};
+  // index + normalised position of this thread's row, prefetched one tile
+  // ahead (issued while the current tile's first MMA runs): the
+  // perm -> x -> gathers load chain was a third of the stall samples
+  struct RowIn {
+    int64_t i;
+    bool valid;
+    float ux, uy, uz;
+  };
+  auto load_row = [&](int64_t tl, RowIn& o) {
+    const int64_t slot = tl * R + r;                   // processing slot (spatially binned order)
+    o.valid = slot < n;
+    o.i = o.valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
+    o.ux = o.uy = o.uz = 0.0f;
+    if (o.valid && !a.feat_in) {
+      o.ux = normalize_axis(__ldg(a.px + o.i), a.grid.lo[0], a.grid.inv[0]);
+      o.uy = normalize_axis(__ldg(a.py + o.i), a.grid.lo[1], a.grid.inv[1]);
+      o.uz = normalize_axis(__ldg(a.pz + o.i), a.grid.lo[2], a.grid.inv[2]);
+    }
+  };
+  RowIn nx_row;
+  if (blockIdx.x < ntiles) load_row(blockIdx.x, nx_row);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t slot = tile * R + r;                 // processing slot (spatially binned order)
-    const bool valid = slot < n;
-    const int64_t i = valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
+    const RowIn row = nx_row;
+    const bool valid = row.valid;
+    const int64_t i = row.i;
     const int64_t ic = i;
     // ---- encode (Eq. 13): levels [q LQ, (q+1) LQ) + conditioning -> buffer A
     {
@@ -277,9 +298,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
 #pragma unroll
         for (int j = 0; j < GQ; ++j) g[j] = __ldg(a.feat_in + (int64_t)(q * GQ + j) * n + i);
       } else if (valid) {
-        const float ux = normalize_axis(__ldg(a.px + i), a.grid.lo[0], a.grid.inv[0]);
-        const float uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
-        const float uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
+        const float ux = row.ux, uy = row.uy, uz = row.uz;
 #pragma unroll
         for (int ll = 0; ll < LQ; ++ll) {
           const int l = q * LQ + ll;
@@ -330,13 +349,20 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
         issue_fwd(tbase, xbuf[src], xbuf[src] + xlo[src], w, w + T::wbytes(k), T::in_p(k), T::out(k));
         tc::mma_commit(mbar);
       }
+      if (k == 0 && tile + gridDim.x < ntiles) load_row(tile + gridDim.x, nx_row);
       wait_mma(mbar, phase);
       float h[WQ];
       tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), h);
       tc::tmem_wait_ld();
-      const float* b = bias + T::boff(k) / 4;
+      const float4* b4 = reinterpret_cast<const float4*>(bias + T::boff(k) / 4 + q * WQ);   // 16-byte aligned
 #pragma unroll
-      for (int j = 0; j < WQ; ++j) h[j] = fmaxf(h[j] + b[q * WQ + j], 0.0f);
+      for (int j = 0; j < WQ / 4; ++j) {
+        const float4 bb = b4[j];
+        h[4 * j] = fmaxf(h[4 * j] + bb.x, 0.0f);
+        h[4 * j + 1] = fmaxf(h[4 * j + 1] + bb.y, 0.0f);
+        h[4 * j + 2] = fmaxf(h[4 * j + 2] + bb.z, 0.0f);
+        h[4 * j + 3] = fmaxf(h[4 * j + 3] + bb.w, 0.0f);
+      }
       tc::store_feats<WQ>(xbuf[dst], xbuf[dst] + xlo[dst], R, r, q * WQ, h);
     }
     {
