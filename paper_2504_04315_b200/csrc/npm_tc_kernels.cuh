@@ -1092,7 +1092,12 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
   const int64_t tstride = (int64_t)gridDim.x * 2;
   TileIn cur;
   if (first_tile < ntiles) load_tile(first_tile, cur);
+  int tile_no = 0;
+  const bool stamp = (a.debug & 4) && blockIdx.x == 0 && gtid == 0 && g == 0;
+#define NPM_STAMP64(idx) \
+  do { if (stamp && tile_no < 64) a.dbg_clock[tile_no * 16 + (idx)] = clock64(); } while (0)
   for (int64_t tile = first_tile; tile < ntiles; tile += tstride) {
+    NPM_STAMP64(0);
     const bool evalid = cur.valid;
     const float ux = cur.ux, uy = cur.uy, uz = cur.uz;
     // head row inputs (consumed after the forward MMAs)
@@ -1133,6 +1138,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       handoff();
+      NPM_STAMP64(1 + 2 * k);
       if (gtid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF + TB::woff(k);
@@ -1140,6 +1146,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         tc::mma_commit(gbar);
       }
       gwait();
+      NPM_STAMP64(2 + 2 * k);
       const float* b = bias + TB::boff(k) / 4;
       if (k < NL - 1) {
         float v[4 * XH];
@@ -1261,6 +1268,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
 #pragma unroll
     for (int k = NL - 1; k >= 0; --k) {
       handoff();
+      NPM_STAMP64(1 + 2 * NL + 2 * (NL - 1 - k));
       if (gtid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + T::WOFF + TB::woff(k);
@@ -1270,6 +1278,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
       }
       if (k == 0 && tile + tstride < ntiles) load_tile(tile + tstride, nxt);
       gwait();
+      NPM_STAMP64(2 + 2 * NL + 2 * (NL - 1 - k));
       if (k > 0) {
         float v[4 * XH];
         tc::tmem_ld16dp<XH>(tbase + qaddr + (uint32_t)(64 * g + WH * h), v);
@@ -1319,6 +1328,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         }
       }
     }
+    NPM_STAMP64(15);
+    ++tile_no;
     cur = nxt;
   }
   // ---- flush dW^T / db (M = 128 layout: lane = input feature; quarter = warp / 4)
