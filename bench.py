@@ -95,16 +95,19 @@ def cpu_oracle_step(name, n, seed=0):
     queries, gradient over n records, Adam + EMA over all parameters."""
     from oracle import npm as onpm, vmf as ovmf, philox as ophilox
     cfg = onpm.Config(**CONFIGS[name]["model"])
+    prod = cfg.mode == onpm.PRODUCT
     p = synth.random_params(cfg.layer_dims, cfg.n_grid, cfg.n_lobes, seed=seed).astype(np.float64)
     state = onpm.State(cfg, p)
-    qb = synth.query_batch(n, seed=seed + 1)
-    tb = synth.training_batch(n, seed=seed + 2)
+    qb = synth.query_batch(n, seed=seed + 1, product=prod)
+    tb = synth.training_batch(n, seed=seed + 2, product=prod)
+    cond = lambda b: dict(x=b["x"], **(dict(wo=b["wo"].astype(np.float64), n=b["nrm"].astype(np.float64),
+                                            rough=b["rough"].astype(np.float64)) if prod else {}))
     t0 = time.perf_counter()
-    _, act = onpm.decode(cfg, state.ema, dict(x=qb["x"]))
+    _, act = onpm.decode(cfg, state.ema, cond(qb))
     u = ophilox.sample_uniforms(n, 1234, 0)
     ovmf.sample(act, u, cfg.n_lobes)
     ovmf.mixture_pdf(qb["wq"].astype(np.float64), act)
-    onpm.train_step(state, dict(x=tb["x"]), tb["wi"].astype(np.float64), tb["target"].astype(np.float64),
+    onpm.train_step(state, cond(tb), tb["wi"].astype(np.float64), tb["target"].astype(np.float64),
                     tb["pdf"].astype(np.float64), n)
     return time.perf_counter() - t0
 
@@ -118,7 +121,7 @@ def cpu_baseline(name, target_s=12.0):
         dt2 = cpu_oracle_step(name, n2)
     return {"value": 2 * n2 / dt2, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": "%s workload, %d queries + %d records, one step (float64 numpy oracle, 1 thread; "
-                      "Adam over all %s params)" % (name, n2, n2, "c2")}
+                      "Adam over all %s params)" % (name, n2, n2, name)}
 
 
 def run_reference(args, rank):
