@@ -33,11 +33,19 @@ struct Net {
   __host__ __device__ static constexpr int in_dim(int k) { return k == 0 ? NIN : W; }
   __host__ __device__ static constexpr int inp_dim(int k) { return k == 0 ? NINP : W; }
   __host__ __device__ static constexpr int out_dim(int k) { return k == NL - 1 ? NOUT : W; }
-  __host__ __device__ static constexpr int w_off(int k) { return k == 0 ? 0 : b_off(k - 1) + out_dim(k - 1); }
+  // sum of out_dim(j) for j < k (k <= NL).  Offsets below are closed forms, not
+  // recursions: nvcc emits recursive constexpr functions as real device calls
+  // when the argument is an unrolled loop index.
+  __host__ __device__ static constexpr int osum(int k) { return k < NL ? k * W : (NL - 1) * W + NOUT; }
+  __host__ __device__ static constexpr int w_off(int k) {
+    return k == 0 ? 0 : out_dim(0) * (NINP + 1) + (W + 1) * (osum(k) - out_dim(0));
+  }
   __host__ __device__ static constexpr int b_off(int k) { return w_off(k) + out_dim(k) * inp_dim(k); }
   static constexpr int SMEM_FLOATS = b_off(NL - 1) + NOUT;
   // offsets in the global (logical, unpadded) layout
-  __host__ __device__ static constexpr int gw_off(int k) { return k == 0 ? 0 : gb_off(k - 1) + out_dim(k - 1); }
+  __host__ __device__ static constexpr int gw_off(int k) {
+    return k == 0 ? 0 : out_dim(0) * (NIN + 1) + (W + 1) * (osum(k) - out_dim(0));
+  }
   __host__ __device__ static constexpr int gb_off(int k) { return gw_off(k) + out_dim(k) * in_dim(k); }
   static constexpr int N_MLP = gb_off(NL - 1) + NOUT;
 };

@@ -46,21 +46,22 @@ struct TC {
   __host__ __device__ static constexpr int in(int k) { return k == 0 ? NIN : W; }
   // bf16 weight bytes of layer k (hi or lo)
   __host__ __device__ static constexpr uint32_t wbytes(int k) { return (uint32_t)(in_p(k) * out(k) * 2); }
+  __host__ __device__ static constexpr int osum(int k) { return N::osum(k); }   // sum of out(j), j < k
   __host__ __device__ static constexpr uint32_t woff(int k) {  // offset of layer k (hi, then lo)
-    return k == 0 ? 0u : woff(k - 1) + 2u * wbytes(k - 1);
+    return k == 0 ? 0u : (uint32_t)(4 * (KIN * out(0) + W * (osum(k) - out(0))));
   }
   static constexpr uint32_t WBYTES = woff(NL);
-  __host__ __device__ static constexpr uint32_t boff(int k) { return k == 0 ? 0u : boff(k - 1) + 4u * out(k - 1); }
+  __host__ __device__ static constexpr uint32_t boff(int k) { return 4u * (uint32_t)osum(k); }
   static constexpr uint32_t BBYTES = boff(NL);
   // TMEM columns: scratch [0, 64), dW^T accumulators after it
   static constexpr int SCR = 64;
-  __host__ __device__ static constexpr int dwcol(int k) { return k == 0 ? SCR : dwcol(k - 1) + out(k - 1); }
+  __host__ __device__ static constexpr int dwcol(int k) { return SCR + osum(k); }
   static constexpr int TCOLS_TRAIN = 256;
   static constexpr int TCOLS_QUERY = 64;
   // ---- train smem map: X_0 (ZF), X_1..X_{NL-1} (HF), D_last (NOUT), weights, bias
   __host__ __device__ static constexpr uint32_t xfeat(int k) { return k == 0 ? ZF : HF; }
   __host__ __device__ static constexpr uint32_t xoff(int k) {  // hi at xoff, lo at xoff + xfeat/8*CH
-    return k == 0 ? 0u : xoff(k - 1) + 2u * (xfeat(k - 1) / 8) * CH;
+    return k == 0 ? 0u : 2u * (ZF / 8) * CH + (uint32_t)(k - 1) * 2u * (HF / 8) * CH;
   }
   static constexpr uint32_t DOFF = xoff(NL);
   // hidden-layer deltas D_0..D_{NL-2} get their own buffers when smem allows
@@ -903,7 +904,7 @@ struct TC64 {
   static constexpr int ZF = B::ZF, HF = B::HF;
   __host__ __device__ static constexpr uint32_t xfeat(int k) { return k == 0 ? ZF : HF; }
   __host__ __device__ static constexpr uint32_t xoff(int k) {
-    return k == 0 ? 0u : xoff(k - 1) + 2u * (xfeat(k - 1) / 8) * CHT;
+    return k == 0 ? 0u : 2u * (ZF / 8) * CHT + (uint32_t)(k - 1) * 2u * (HF / 8) * CHT;
   }
   static constexpr uint32_t DOFF = xoff(NL);
   static constexpr uint32_t GBYTES = DOFF + 2u * (NOUT / 8) * CHT;
@@ -919,7 +920,7 @@ struct TC64 {
   }
   static constexpr uint32_t SMEM_RAW = MISC + 64;
   static constexpr uint32_t SMEM = SMEM_RAW > max_overread(NL - 1) ? SMEM_RAW : max_overread(NL - 1);
-  __host__ __device__ static constexpr int dwcol(int k) { return k == 0 ? 128 : dwcol(k - 1) + B::out(k - 1); }
+  __host__ __device__ static constexpr int dwcol(int k) { return 128 + B::osum(k); }
   static constexpr int DWCOLS = dwcol(NL) - 128;
   static constexpr int TCOLS = 512;
 };
@@ -967,6 +968,19 @@ __device__ __forceinline__ void issue_dw_r(uint32_t d, uint32_t xhi, uint32_t xl
   }
 }
 
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+// f(IC<k>{}) for a k that is a constant after loop unrolling (the branches fold)
+template <int NK, class F>
+__device__ __forceinline__ void with_k(int k, F&& f) {
+  if constexpr (NK > 0) {
+    if (k == NK - 1) f(IC<NK - 1>{});
+    else with_k<NK - 1>(k, f);
+  }
+}
+
 template <class N>
 __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
   using T = TC64<N>;
@@ -999,7 +1013,13 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tbase = *tslot;
+  // A 512-column allocation is the whole TMEM: its base is column 0, lane 0.
+  // Using the constant (checked) keeps every MMA operand warp-uniform, so the
+  // issue below compiles to uniform-datapath descriptor arithmetic with no
+  // per-MMA R2UR/ELECT waterfall.
+  static_assert(T::TCOLS == 512, "constant TMEM base needs the full allocation");
+  constexpr uint32_t tbase = 0;
+  if (*tslot != 0u) __trap();
   stage_weights_tc<N>(a.params, smem, T::WOFF, T::BOFF);
   // zero the shared dW^T accumulators (all later MMAs accumulate)
   for (int col = 16 * (warp >> 2); col < T::DWCOLS; col += 64)
@@ -1009,6 +1029,28 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
   float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
   const float* bias = reinterpret_cast<const float*>(smem + T::BOFF);
   uint64_t* gbar = mbar + g;
+  // MMA issue for group G (compile-time): operand addresses are sb-relative
+  // constants, i.e. uniform registers.
+  auto issue_fwd_g = [&](auto G, auto KC) {
+    constexpr int gg = decltype(G)::value, k = decltype(KC)::value;
+    const uint32_t base = sb + (uint32_t)gg * T::GBYTES;
+    const uint32_t xh = base + T::xoff(k), xl = xh + (T::xfeat(k) / 8) * CHT;
+    const uint32_t w = sb + T::WOFF + TB::woff(k);
+    issue_fwd_r<RT>(tbase + (uint32_t)(64 * gg), xh, xl, w, w + TB::wbytes(k), TB::in_p(k), TB::out(k));
+    tc::mma_commit(mbar + gg);
+  };
+  auto issue_bwd_g = [&](auto G, auto KC) {
+    constexpr int gg = decltype(G)::value, k = decltype(KC)::value;
+    const uint32_t base = sb + (uint32_t)gg * T::GBYTES;
+    const uint32_t xh = base + T::xoff(k), xl = xh + (T::xfeat(k) / 8) * CHT;
+    // delta_k: D_last for the top layer, else it overwrote X_{k+1}'s first W features
+    const uint32_t dh = k == NL - 1 ? base + T::DOFF : base + T::xoff(k + 1);
+    const uint32_t dl = k == NL - 1 ? dh + (NOUT / 8) * CHT : dh + (T::xfeat(k + 1) / 8) * CHT;
+    const uint32_t w = sb + T::WOFF + TB::woff(k);
+    issue_dx_r<RT>(tbase + (uint32_t)(64 * gg), dh, dl, w, w + TB::wbytes(k), TB::out(k), k > 0 ? W : N::NGRID);
+    issue_dw_r<RT>(tbase + (uint32_t)T::dwcol(k), xh, xl, dh, dl, TB::out(k));
+    tc::mma_commit(mbar + gg);
+  };
   const uint32_t gsb = sb + (uint32_t)g * T::GBYTES;
   uint32_t xhi[NL], xlo[NL];
 #pragma unroll
@@ -1141,9 +1183,10 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
       NPM_STAMP64(1 + 2 * k);
       if (gtid == 0) {
         tc::fence_after_sync();
-        const uint32_t w = sb + T::WOFF + TB::woff(k);
-        issue_fwd_r<RT>(tbase + (uint32_t)(64 * g), xhi[k], xlo[k], w, w + TB::wbytes(k), TB::in_p(k), TB::out(k));
-        tc::mma_commit(gbar);
+        with_k<NL>(k, [&](auto KC) {
+          if (g == 0) issue_fwd_g(IC<0>{}, KC);
+          else issue_fwd_g(IC<1>{}, KC);
+        });
       }
       gwait();
       NPM_STAMP64(2 + 2 * k);
@@ -1153,13 +1196,16 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         tc::tmem_ld16dp<XH>(tbase + qaddr + (uint32_t)(64 * g + WH * h), v);
         tc::tmem_wait_ld();
         uint32_t mk = 0;
+        float2 bj[XH];   // loaded before the stores (their asm memory clobbers force reloads)
+#pragma unroll
+        for (int j = 0; j < XH; ++j) bj[j] = *reinterpret_cast<const float2*>(b + WH * h + 8 * j + 2 * c);
 #pragma unroll
         for (int j = 0; j < XH; ++j) {
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             const int col = WH * h + 8 * j + 2 * c;
             const int idx = 2 * half + 4 * j;
-            const float2 bb = *reinterpret_cast<const float2*>(b + col);   // col even: 8-byte aligned
+            const float2 bb = bj[j];
             const float y0 = fmaxf(v[idx] + bb.x, 0.0f), y1 = fmaxf(v[idx + 1] + bb.y, 0.0f);
             mk |= (y0 > 0.0f ? 1u : 0u) << (idx);
             mk |= (y1 > 0.0f ? 1u : 0u) << (idx + 1);
@@ -1271,10 +1317,10 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
       NPM_STAMP64(1 + 2 * NL + 2 * (NL - 1 - k));
       if (gtid == 0) {
         tc::fence_after_sync();
-        const uint32_t w = sb + T::WOFF + TB::woff(k);
-        issue_dx_r<RT>(tbase + (uint32_t)(64 * g), dhi, dlo, w, w + TB::wbytes(k), TB::out(k), k > 0 ? W : N::NGRID);
-        issue_dw_r<RT>(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, TB::out(k));
-        tc::mma_commit(gbar);
+        with_k<NL>(k, [&](auto KC) {
+          if (g == 0) issue_bwd_g(IC<0>{}, KC);
+          else issue_bwd_g(IC<1>{}, KC);
+        });
       }
       if (k == 0 && tile + tstride < ntiles) load_tile(tile + tstride, nxt);
       gwait();
