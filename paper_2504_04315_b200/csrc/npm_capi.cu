@@ -709,7 +709,8 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       for (int t = 1; t < 64; ++t) {   // skip tile 0 (weight staging)
         if (h[t * 16 + 15] == 0) break;
         for (int j = 1; j < 16; ++j) {
-          const long long prev = (j == 13) ? h[t * 16 + 12] : h[t * 16 + j - 1];
+          long long prev = 0;   // the last stamp before j (13, 14 unused below NL = 4)
+          for (int i = j - 1; i >= 0 && !prev; --i) prev = h[t * 16 + i];
           if (h[t * 16 + j]) acc[j] += (double)(h[t * 16 + j] - prev);
         }
         acc[0] += (double)(h[t * 16 + 15] - h[t * 16 + 0]);

@@ -907,7 +907,26 @@ struct TC64 {
     return k == 0 ? 0u : 2u * (ZF / 8) * CHT + (uint32_t)(k - 1) * 2u * (HF / 8) * CHT;
   }
   static constexpr uint32_t DOFF = xoff(NL);
-  static constexpr uint32_t GBYTES = DOFF + 2u * (NOUT / 8) * CHT;
+  static constexpr uint32_t DAOFF = DOFF + 2u * (NOUT / 8) * CHT;   // extra delta buffer (SEP)
+  static constexpr uint32_t GB_NOSEP = DAOFF;
+  static constexpr uint32_t GB_SEP = DAOFF + 2u * (W / 8) * CHT;
+  // SEP: each backward batch commits dX_k before issuing dW_k, so the epilogue
+  // (delta_{k-1}) runs under the dW_k MMAs; delta_{k-1} then needs a buffer that
+  // dW_k does not read (neither X_k nor delta_k).  Measured on B200: c2 (173 KB)
+  // 1 % faster; c5 (196 KB) 41 % slower -- the smaller L1 costs its
+  // HBM-resident gathers more than the overlap gains.  Off above 180 KB.
+  static constexpr bool SEP =
+      2u * GB_SEP + B::WBYTES + B::BBYTES + 256u <= 180u * 1024u;
+  static constexpr uint32_t GBYTES = SEP ? GB_SEP : GB_NOSEP;
+  // buffer of delta_k (hi part; lo follows after dfeat(k) / 8 chunks):
+  //   delta_{NL-1}: D_last.  SEP: alternately DA and X_{k+2} (free once dW_{k+1}
+  //   completed).  !SEP: delta_k overwrites X_{k+1} (its ones chunk stays).
+  __host__ __device__ static constexpr uint32_t dboff(int k) {
+    return k == NL - 1 ? DOFF : (!SEP ? xoff(k + 1) : (((NL - 2 - k) % 2 == 0) ? DAOFF : xoff(k + 2)));
+  }
+  __host__ __device__ static constexpr uint32_t dfeat(int k) {
+    return k == NL - 1 ? (uint32_t)NOUT : (!SEP ? xfeat(k + 1) : (((NL - 2 - k) % 2 == 0) ? (uint32_t)W : xfeat(k + 2)));
+  }
   static constexpr uint32_t WOFF = 2u * GBYTES;
   static constexpr uint32_t BOFF = WOFF + B::WBYTES;
   static constexpr uint32_t MISC = (BOFF + B::BBYTES + 127u) & ~127u;
@@ -1043,13 +1062,15 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
     constexpr int gg = decltype(G)::value, k = decltype(KC)::value;
     const uint32_t base = sb + (uint32_t)gg * T::GBYTES;
     const uint32_t xh = base + T::xoff(k), xl = xh + (T::xfeat(k) / 8) * CHT;
-    // delta_k: D_last for the top layer, else it overwrote X_{k+1}'s first W features
-    const uint32_t dh = k == NL - 1 ? base + T::DOFF : base + T::xoff(k + 1);
-    const uint32_t dl = k == NL - 1 ? dh + (NOUT / 8) * CHT : dh + (T::xfeat(k + 1) / 8) * CHT;
+    const uint32_t dh = base + T::dboff(k), dl = dh + (T::dfeat(k) / 8) * CHT;
     const uint32_t w = sb + T::WOFF + TB::woff(k);
     issue_dx_r<RT>(tbase + (uint32_t)(64 * gg), dh, dl, w, w + TB::wbytes(k), TB::out(k), k > 0 ? W : N::NGRID);
+    // SEP: the epilogue waits for dX_k only; dW_k completes before the next
+    // commit (dX_{k-1}) fires, which is all a later overwrite needs.  k = 0
+    // commits both: the next tile's encode rewrites X_0.
+    if (T::SEP && k > 0) tc::mma_commit(mbar + gg);
     issue_dw_r<RT>(tbase + (uint32_t)T::dwcol(k), xh, xl, dh, dl, TB::out(k));
-    tc::mma_commit(mbar + gg);
+    if (!(T::SEP && k > 0)) tc::mma_commit(mbar + gg);
   };
   const uint32_t gsb = sb + (uint32_t)g * T::GBYTES;
   uint32_t xhi[NL], xlo[NL];
@@ -1224,11 +1245,13 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
 #pragma unroll
           for (int w = 0; w < 2; ++w) {
             const int m = 2 * jj + w, lobe = 8 * jj + 2 * c + w;
-            const int base = w + 2 * h;
-            lp[m] = v[base + 4 * (0 * KJ + jj)] + b[lobe];
-            kp[m] = v[base + 4 * (1 * KJ + jj)] + b[K + lobe];
-            tp[m] = v[base + 4 * (2 * KJ + jj)] + b[2 * K + lobe];
-            pp[m] = v[base + 4 * (3 * KJ + jj)] + b[3 * K + lobe];
+            // row half h selects registers w or w + 2 (a select, not a dynamic
+            // index: that would put v in local memory)
+            auto pick = [&](int blk) { return h ? v[w + 2 + 4 * (blk * KJ + jj)] : v[w + 4 * (blk * KJ + jj)]; };
+            lp[m] = pick(0) + b[lobe];
+            kp[m] = pick(1) + b[K + lobe];
+            tp[m] = pick(2) + b[2 * K + lobe];
+            pp[m] = pick(3) + b[3 * K + lobe];
           }
         }
         float t = h_t0;
@@ -1330,9 +1353,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         tc::tmem_ld16dp<XH>(tbase + qaddr + (uint32_t)(64 * g + WH * h), v);
         tc::tmem_wait_ld();
         const uint32_t mk = mask[k];
-        // delta_{k-1} overwrites X_k's first W features (hi and lo); its ones chunk stays
-        dhi = xhi[k];
-        dlo = xlo[k];
+        dhi = gsb + T::dboff(k - 1);
+        dlo = dhi + (T::dfeat(k - 1) / 8) * CHT;
 #pragma unroll
         for (int j = 0; j < XH; ++j) {
 #pragma unroll
