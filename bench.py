@@ -327,6 +327,25 @@ def main():
             "kernel_share_of_step": (kms / 1e3) / t_tot if t_tot > 0 else None, "peak_source": src,
             "per_unit_bytes": per_unit.get(kname), "units_per_launch": n}
 
+    # grid-access ceiling: the same number of uniformly random 16-B
+    # gathers / v4 scatter-adds into a table of this model's size, timed by the
+    # library's probe kernels (include/npm.h npm_probe_grid_access).  For
+    # L2-resident tables this, not HBM, bounds the fused kernels' grid stage.
+    try:
+        ents = m.n_grid // F
+        tg = npm.npm_probe_grid_access(local, ents, n, L, 0)
+        ts_ = npm.npm_probe_grid_access(local, ents, n, L, 1)
+        acc = 8 * L * n
+        probe = {"table_entries": ents, "table_mb": 16 * ents / 1e6, "accesses_per_launch": acc,
+                 "gather_ms": tg, "scatter_ms": ts_,
+                 "gathers_per_s": acc / (tg / 1e3), "scatter_adds_per_s": acc / (ts_ / 1e3)}
+        for k, need in (("query", tg), ("train_fused", tg + ts_)):
+            if k in prof and prof[k][0]:
+                probe["%s_frac_of_probe" % k] = need / (prof[k][1] / prof[k][0])
+        roof["grid_access_probe"] = probe
+    except Exception as exc:   # the probe is context; never fail the bench line on it
+        roof["grid_access_probe"] = {"error": str(exc)}
+
     # decoder tensor-core work (algorithmic MACs of the 64-wide MLP; split-bf16 issues 3x)
     dims = [(m.cfg.n_levels * m.F + (33 if m.product else 0), m.cfg.mlp_width)]
     dims += [(m.cfg.mlp_width, m.cfg.mlp_width)] * (m.cfg.mlp_linear_layers - 2)

@@ -230,6 +230,20 @@ npm_status npm_profile_reset(npm_model* model);
 npm_status npm_profile_read(npm_model* model, int kind, const char** name, int64_t* launches,
                             double* total_ms);
 
+/* Measurement probe ("a measured L2 random-gather peak"), not
+ * part of the method.  Times `reps` launches of a kernel that, for each of
+ * n_samples samples, makes 8*levels uniformly random float4 accesses into a
+ * table of table_entries float4 (16 B) entries: kind 0 = gathers (ld.global.nc
+ * .v4), kind 1 = scatter-adds (red.global.add.v4.f32).  With a c2-sized table
+ * (636,927 entries, 10.2 MB) the table is L2-resident, which is the ceiling
+ * for the fused kernels' grid accesses; with c5's (632 MB) it is HBM-bound.
+ * Allocates and frees its own device memory on cuda_device; synchronous.
+ * levels must be even and > 0; table_entries in [1, 2^32).  Writes the mean
+ * milliseconds per launch to *ms_per_rep.  Errors: NPM_ERR_INVALID for bad
+ * arguments, NPM_ERR_CUDA (npm_last_error unset) for CUDA failures. */
+npm_status npm_probe_grid_access(int cuda_device, int64_t table_entries, int64_t n_samples, int levels,
+                                 int kind, int reps, double* ms_per_rep);
+
 const char* npm_last_error(void);
 int npm_version(void);
 

@@ -94,6 +94,7 @@ def _load():
         "npm_profile_reset": (I32, [M]),
         "npm_profile_read": (I32, [M, I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(I64),
                                    ctypes.POINTER(ctypes.c_double)]),
+        "npm_probe_grid_access": (I32, [I32, I64, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_double)]),
         "npm_last_error": (ctypes.c_char_p, []),
         "npm_version": (I32, []),
     }
@@ -259,6 +260,13 @@ def npm_profile_enable(h, on):
 
 def npm_profile_reset(h):
     _check(_lib.npm_profile_reset(h))
+
+
+def npm_probe_grid_access(device, table_entries, n_samples, levels, kind, reps=5):
+    """Mean ms per launch of the random grid-access probe (include/npm.h)."""
+    ms = ctypes.c_double()
+    _check(_lib.npm_probe_grid_access(device, table_entries, n_samples, levels, kind, reps, ctypes.byref(ms)))
+    return ms.value
 
 
 def npm_profile_read(h):
