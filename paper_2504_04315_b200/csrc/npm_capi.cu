@@ -354,7 +354,9 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   if (nm % 4) { delete m; return fail(NPM_ERR_INVALID, "internal: MLP size not 16B aligned"); }
   m->n_total = m->n_mlp + m->n_grid;
   for (int b = 0; b < 5; ++b) {
-    if (cudaMalloc(&m->buf[b], m->n_total * sizeof(float)) != cudaSuccess) {
+    // +8 floats: the paired grid gathers (gather_level) read the 32-B entry
+    // pair containing the last table entry
+    if (cudaMalloc(&m->buf[b], (m->n_total + 8) * sizeof(float)) != cudaSuccess) {
       npm_destroy(m);
       return fail(NPM_ERR_OOM, "parameter buffers");
     }

@@ -115,6 +115,41 @@ __device__ __forceinline__ void level_corners(const GridDesc& g, int l, float ux
   }
 }
 
+// Eq. 13 gather + trilinear blend of one level, fetching x-neighbour corners
+// together.  Corners c and c + 1 (cx = 0, 1) are entries e and e + 1 (dense)
+// or e and e ^ 1 (hashed, ix even: the x prime is 1).  A 32-byte load of the
+// aligned entry pair {e & ~1, e | 1} (absolute index from the 32-B aligned
+// table start) returns both whenever they share it -- one L1/L2 sector
+// instead of two; otherwise the second corner is a separate 16-byte load.
+// Same products and summation order as the 8-load form (bit-identical).
+// Requires: tab 32-B aligned and readable one entry past the last (the model
+// pads its parameter buffers).
+__device__ __forceinline__ void ld_pair(const float4* p, float4& lo, float4& hi) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(p));
+}
+
+__device__ __forceinline__ float4 gather_level(const float4* __restrict__ tab, uint32_t off, const LevelCorners& lc) {
+  float4 v[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t e0 = off + lc.idx[2 * p], e1 = off + lc.idx[2 * p + 1];
+    float4 lo, hi;
+    ld_pair(tab + (e0 & ~1u), lo, hi);
+    v[2 * p] = (e0 & 1u) ? hi : lo;
+    if ((e0 ^ e1) == 1u) v[2 * p + 1] = (e1 & 1u) ? hi : lo;
+    else v[2 * p + 1] = __ldg(tab + e1);
+  }
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
+    a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
+  }
+  return make_float4(a0, a1, a2, a3);
+}
+
 // ---------------------------------------------------------------------------
 // Real orthonormal SH, 4 bands, l-major / m ascending, no Condon-Shortley
 // phase (C-A20, C-O6).  Cartesian polynomial forms.

@@ -37,6 +37,7 @@ __host__ __device__ constexpr int r16(int x) { return (x + 15) & ~15; }
 template <class N>
 struct TC {
   static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN;
+  static_assert(N::N_MLP % 8 == 0, "grid tables must start 32-B aligned (paired gathers)");
   static constexpr int KIN = r16(NIN);          // layer-0 MMA K
   // train X0 features: ones at NIN (bias row of dW_0^T), >= KIN for the forward K
   static constexpr int ZF = KIN > ((NIN + 8) & ~7) ? KIN : ((NIN + 8) & ~7);
@@ -305,17 +306,20 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
           const int l = q * LQ + ll;
           LevelCorners lc;
           level_corners(a.grid, l, ux, uy, uz, lc);
+          // 8 single loads here: the binned query gathers are coherent already and
+          // the paired form's wider registers cost more than it saves (B200: c2
+          // query 269 -> 293 us with pairs, train 655 -> 641 us)
           const float4* t = tab + a.grid.off[l];
           float4 v[8];
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[c] = __ldg(t + lc.idx[c]);
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+          float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
-            a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
+            gl.x = fmaf(lc.w[c], v[c].x, gl.x); gl.y = fmaf(lc.w[c], v[c].y, gl.y);
+            gl.z = fmaf(lc.w[c], v[c].z, gl.z); gl.w = fmaf(lc.w[c], v[c].w, gl.w);
           }
-          g[4 * ll] = a0; g[4 * ll + 1] = a1; g[4 * ll + 2] = a2; g[4 * ll + 3] = a3;
+          g[4 * ll] = gl.x; g[4 * ll + 1] = gl.y; g[4 * ll + 2] = gl.z; g[4 * ll + 3] = gl.w;
         }
       } else {
 #pragma unroll
@@ -1133,18 +1137,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         const int l = h * (L / 2) + 2 * j + (c >> 1);
         LevelCorners lc;
         level_corners(a.grid, l, t.ux, t.uy, t.uz, lc);
-        const float4* tb = tab + a.grid.off[l];
-        float4 v[8];
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc)
-          v[cc] = (a.debug & 2) ? make_float4(lc.w[cc], 0.f, 0.f, 0.f) : __ldg(tb + lc.idx[cc]);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          a0 = fmaf(lc.w[cc], v[cc].x, a0); a1 = fmaf(lc.w[cc], v[cc].y, a1);
-          a2 = fmaf(lc.w[cc], v[cc].z, a2); a3 = fmaf(lc.w[cc], v[cc].w, a3);
-        }
-        t.gf[4 * j] = a0; t.gf[4 * j + 1] = a1; t.gf[4 * j + 2] = a2; t.gf[4 * j + 3] = a3;
+        const float4 gl = gather_level(tab, a.grid.off[l], lc);
+        t.gf[4 * j] = gl.x; t.gf[4 * j + 1] = gl.y; t.gf[4 * j + 2] = gl.z; t.gf[4 * j + 3] = gl.w;
       }
     } else {
 #pragma unroll

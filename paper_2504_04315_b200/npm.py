@@ -98,7 +98,10 @@ def _load():
         "npm_last_error": (ctypes.c_char_p, []),
         "npm_version": (I32, []),
     }
+    optional = {"npm_probe_grid_access"}   # measurement only; absent in older A/B builds (NPM_LIB)
     for name, (res, args) in sig.items():
+        if name in optional and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype, f.argtypes = res, args
     return lib
