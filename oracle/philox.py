@@ -38,15 +38,16 @@ def philox4x32_10(ctr, key):
     return c0, c1, c2, c3
 
 
-def sample_uniforms(n, seed, offset):
+def sample_uniforms(n, seed, offset, count=3):
     """Uniforms for sample i (C-O11): key = (lo32(seed), hi32(seed)),
     counter = (lo32(i + offset), hi32(i + offset), 0, 0);
-    u_j = (out_j >> 8) * 2^-24 for j = 0, 1, 2 (24-bit, in [0, 1)).
-    Returns float64 array [3, n]."""
+    u_j = (out_j >> 8) * 2^-24 for j = 0, 1, 2 (24-bit, in [0, 1)); count=4
+    adds u_3 from out_3, the technique selector of combined sampling (C-A25).
+    Returns float64 array [count, n]."""
     idx = np.arange(n, dtype=np.uint64) + np.uint64(offset)
     ctr = (idx & np.uint64(MASK32), idx >> np.uint64(32),
            np.zeros(n, np.uint64), np.zeros(n, np.uint64))
     key = (np.uint64(seed & MASK32), np.uint64((seed >> 32) & MASK32))
     o = philox4x32_10(ctr, key)
     return np.stack([(o[j] >> np.uint64(8)).astype(np.float64) * 2.0 ** -24
-                     for j in range(3)])
+                     for j in range(count)])
