@@ -234,6 +234,41 @@ def main():
     K = args.steps
     value = 2 * n * world * K / t_tot
 
+    # ---- f-1 context: combined BSDF/guide sampling (alpha = 0.5) over the same n
+    # queries and the record unwind of n records (8-vertex paths), device-timed
+    def timed_ms(fn, reps=5):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            fn()
+            a1.record()
+            torch.cuda.synchronize()
+            ts.append(a0.elapsed_time(a1))
+        return float(np.median(ts))
+
+    nv = np.random.default_rng(300 + rank).normal(size=(3, n))
+    nrm = T((nv / np.linalg.norm(nv, axis=0)).astype(np.float32))
+    cw, cp, cg = torch.empty(3, n, device=dev), torch.empty(n, device=dev), torch.empty(n, device=dev)
+    ct = torch.empty(n, dtype=torch.int32, device=dev)
+    t_comb = timed_ms(lambda: npm.npm_combined_sample(m.h, qq, nrm[0], nrm[1], nrm[2], 0.5, None, 0xC0FFEE, 0, True,
+                                                      cw[0], cw[1], cw[2], cp, cg, ct, stream=stream))
+    Dp, npaths = 8, n // 8
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    le_ = torch.rand(3, Dp, npaths, device=dev, generator=g)
+    fs_ = torch.rand(3, Dp, npaths, device=dev, generator=g)
+    cs_ = torch.rand(Dp, npaths, device=dev, generator=g)
+    pd_ = torch.rand(Dp, npaths, device=dev, generator=g) + 0.05
+    dp_ = torch.randint(0, Dp + 1, (npaths,), device=dev, dtype=torch.int32, generator=g)
+    tg_ = torch.empty(3, Dp, npaths, device=dev)
+    t_unw = timed_ms(lambda: npm.npm_unwind_records(m.h, le_, fs_, cs_, pd_, dp_, 3, Dp, npaths, 0, tg_, stream=stream))
+    f1 = {"combined_sample_ms": t_comb, "combined_sample_queries_per_s": n / (t_comb / 1e3), "alpha": 0.5,
+          "unwind_ms": t_unw, "unwind_records_per_s": Dp * npaths / (t_unw / 1e3),
+          "unwind_bytes_per_record": 4 * (3 + 3 + 1 + 1 + 3) + 4 / Dp,
+          "unwind_gb_s": (4 * 11 * Dp * npaths + 4 * npaths) / (t_unw / 1e3) / 1e9}
+
     # ---- e2e: same step through the C ABI with pinned HOST buffers ------------------------
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     hqx, hwq = pin(qb["x"]), pin(qb["wq"])
@@ -374,7 +409,7 @@ def main():
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "gpu_launches_per_step": launches / K,
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
-                "clocks": clk.summary(), "cpu_baseline": cpu, "paper_context": paper_ctx}
+                "clocks": clk.summary(), "cpu_baseline": cpu, "paper_context": paper_ctx, "f1_guided_mis": f1}
         print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()

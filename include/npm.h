@@ -186,6 +186,40 @@ npm_status npm_sample(npm_model* model, const npm_query* q, const float* u, uint
                       float* pdf, const float* qx, const float* qy, const float* qz,
                       float* pdf_q, void* stream);
 
+/* f-1, guided one-sample MIS ("a combination of the BSDF importance
+ * sampling and guiding distribution"; P:425 BSDF selection probability 50 %;
+ * SPEC S:339-347).  Per query: u_sel < alpha -> BSDF sample, else a guide
+ * sample exactly as npm_sample; pdf = p~ = alpha p_bsdf(w) + (1 - alpha) V(w)
+ * (balance heuristic, the divisor to store in the training record).  BSDF
+ * stand-in (C-A24): Lambertian about the unit normals nx/ny/nz [n],
+ * p_bsdf = max(n.w, 0)/pi, cosine-sampled from (u1, u2) in the Duff ONB of n.
+ * u: [4][n] = (u1, u2, u3, u_sel) or NULL -> Philox4x32-10 (C-O11; u_sel =
+ * out3, C-A25).  If the guide branch is taken and V(w) < 1e-30 or non-finite
+ * (C-A26), the record falls back to the BSDF sample with pdf = p_bsdf.
+ * Outputs [n]: wix/wiy/wiz, pdf (p~); optional guide_pdf (V(w); 0 on
+ * fallback) and technique (int32: 0 BSDF, 1 guide, 2 fallback).
+ * alpha in [0, 1] else NPM_ERR_INVALID; needs the tensor-core path. */
+npm_status npm_combined_sample(npm_model* model, const npm_query* q, const float* nx, const float* ny,
+                               const float* nz, float alpha, const float* u, uint64_t seed, uint64_t offset,
+                               int use_ema, float* wix, float* wiy, float* wiz, float* pdf, float* guide_pdf,
+                               int32_t* technique, void* stream);
+
+/* f-1, training-record construction ("collect MC radiance estimates
+ * along each traced path"): backward unwind per path
+ *   <L_i(x_v)> = le[v] + fs[v+1] cos[v+1] / pdf[v+1] * <L_i(x_{v+1})>
+ * for v < depth, where le[v] is the radiance arriving at vertex v along its
+ * sampled ray (emitted by the vertex it hit), fs/cos/pdf the BSDF value,
+ * |cos theta_i| and p~ of vertex v's sampled direction.  A successor with
+ * p~ <= 0 or non-finite ends the path (C-A27); v >= depth gives 0.
+ * target = <L_i> (product = 0) or fs[v] <L_i> cos[v] (product = 1, Eq. 12).
+ * Layouts (n = n_paths, D = max_depth, C = channels in {1, 3}):
+ * le, fs, target [C][D][n]; cos_theta, pdf [D][n]; depth int32 [n] -- i.e.
+ * target is directly the [C][D*n] target of npm_train_step over D*n records.
+ * Uses the model only for its stream staging (host or device pointers). */
+npm_status npm_unwind_records(npm_model* model, const float* le, const float* fs, const float* cos_theta,
+                              const float* pdf, const int32_t* depth, int channels, int max_depth, int64_t n_paths,
+                              int product, float* target, void* stream);
+
 /* One optimisation step ("optimization step is performed for each spp"):
  * Eq. 9 gradient over the batch, back propagation through decoder and grid
  * (P:216), [allreduce if a communicator is attached], Adam + EMA.

@@ -181,8 +181,8 @@ void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryA
 }
 
 const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward", "weight_grad", "adam",
-                            "train_fused", "bin"};
-enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKTrainFused, kKBin, kKinds };
+                            "train_fused", "bin", "unwind"};
+enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKTrainFused, kKBin, kKUnwind, kKinds };
 constexpr int64_t kBinMin = 65536;  // batches at least this large are spatially binned
 
 cudaEvent_t take_event(npm_model* m) {
@@ -634,6 +634,67 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   r = check_launch(m, timed(m, kKQuery, st, [&] {
     return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
   }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+npm_status npm_combined_sample(npm_model* m, const npm_query* q, const float* nx, const float* ny,
+                               const float* nz, float alpha, const float* u, uint64_t seed, uint64_t offset,
+                               int use_ema, float* wix, float* wiy, float* wiz, float* pdf, float* guide_pdf,
+                               int32_t* technique, void* stream) {
+  if (!m || !query_ok(m, q) || !(alpha >= 0.0f && alpha <= 1.0f) ||
+      (q->n > 0 && (!nx || !ny || !nz || !wix || !wiy || !wiz || !pdf)))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (!m->use_tc) return fail(NPM_ERR_INVALID, "combined sampling needs the tensor-core query kernel");
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const size_t n = (size_t)q->n;
+  QueryArgs a;
+  fill_query_args(m, d, use_ema, a);
+  a.do_sample = 1;
+  a.combined = 1;
+  a.alpha = alpha;
+  a.u = s.in(u, 4 * n);
+  a.seed = seed;
+  a.offset = offset;
+  a.bnx = s.in(nx, n); a.bny = s.in(ny, n); a.bnz = s.in(nz, n);
+  a.sx = s.out(wix, n); a.sy = s.out(wiy, n); a.sz = s.out(wiz, n); a.spdf = s.out(pdf, n);
+  a.gpdf = s.out(guide_pdf, n);
+  a.tech = s.out(technique, n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+  if (r != NPM_OK) return r;
+  r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query_tc(m->shape, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
+npm_status npm_unwind_records(npm_model* m, const float* le, const float* fs, const float* cos_theta,
+                              const float* pdf, const int32_t* depth, int channels, int max_depth, int64_t n_paths,
+                              int product, float* target, void* stream) {
+  if (!m || n_paths < 0 || max_depth < 0 || (channels != 1 && channels != 3) ||
+      (n_paths > 0 && max_depth > 0 && (!le || !fs || !cos_theta || !pdf || !depth || !target)))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (n_paths == 0 || max_depth == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  const size_t nv = (size_t)max_depth * (size_t)n_paths, nc = (size_t)channels * nv;
+  UnwindArgs a;
+  a.le = s.in(le, nc); a.fs = s.in(fs, nc); a.cosv = s.in(cos_theta, nv); a.pdf = s.in(pdf, nv);
+  a.depth = s.in(depth, (size_t)n_paths);
+  a.target = s.out(target, nc);
+  a.channels = channels; a.max_depth = max_depth; a.n = n_paths; a.product = product ? 1 : 0;
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  npm_status r = check_launch(m, timed(m, kKUnwind, st, [&] { return launch_unwind(a, m->num_sms, st); }));
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;

@@ -47,6 +47,15 @@ __device__ __forceinline__ float3 philox_uniforms(uint64_t seed, uint64_t ctr) {
   return make_float3((float)(o.x >> 8) * s, (float)(o.y >> 8) * s, (float)(o.z >> 8) * s);
 }
 
+// The same counter's fourth output as a fourth uniform (C-A25: the technique
+// selector of combined BSDF/guide sampling).
+__device__ __forceinline__ float4 philox_uniforms4(uint64_t seed, uint64_t ctr) {
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), 0u, 0u),
+                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const float s = 5.9604644775390625e-08f;  // 2^-24
+  return make_float4((float)(o.x >> 8) * s, (float)(o.y >> 8) * s, (float)(o.z >> 8) * s, (float)(o.w >> 8) * s);
+}
+
 // ---------------------------------------------------------------------------
 // Pinned fp32 cell-index sequence (C-O1, C-O3; C-A1): no FMA contraction.
 __device__ __forceinline__ float normalize_axis(float x, float lo, float inv) {
@@ -287,6 +296,29 @@ __device__ __forceinline__ void lobe_sample(float kap, float mux, float muy, flo
   wx = w * mux + r * (cp * t1x + sp * t2x);
   wy = w * muy + r * (cp * t1y + sp * t2y);
   wz = w * muz + r * (cp * t1z + sp * t2z);
+}
+
+// BSDF stand-in (C-A24, f-1): Lambertian about the unit shading normal n.
+// pdf max(n.w, 0) / pi; cosine-weighted sample r = sqrt(u1), phi = 2 pi u2,
+// local (r cos phi, r sin phi, sqrt(1 - u1)) in the Duff ONB of n.
+__device__ __forceinline__ float bsdf_pdf(float nx, float ny, float nz, float wx, float wy, float wz) {
+  return fmaxf(nx * wx + ny * wy + nz * wz, 0.0f) * 0.31830988618379067f;
+}
+
+__device__ __forceinline__ void bsdf_sample(float nx, float ny, float nz, float u1, float u2, float& wx, float& wy,
+                                            float& wz) {
+  const float r = sqrtf(u1), lz = sqrtf(fmaxf(1.0f - u1, 0.0f));
+  float sp, cp;
+  sincospif(2.0f * u2, &sp, &cp);
+  const float s = copysignf(1.0f, nz);
+  const float a = -1.0f / (s + nz);
+  const float b = nx * ny * a;
+  const float t1x = 1.0f + s * nx * nx * a, t1y = s * b, t1z = -s * nx;
+  const float t2x = b, t2y = s + ny * ny * a, t2z = -ny;
+  const float lx = r * cp, ly = r * sp;
+  wx = lx * t1x + ly * t2x + lz * nx;
+  wy = lx * t1y + ly * t2y + lz * ny;
+  wz = lx * t1z + ly * t2z + lz * nz;
 }
 
 // Eq. 9 head (C-O13): d loss / d raw for one record, multiplied by s.

@@ -60,6 +60,85 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
   }
 }
 
+// Training-record unwind (f-1): <L_i(x_v)> = L_e[v] + f_s cos / p~ at v + 1 times
+// <L_i(x_{v+1})>, backward along each path; a successor
+// with p~ <= 0 or non-finite ends the path (C-A27); v >= depth -> 0.
+// D^ = <L_i> (radiance) or f_s <L_i> cos (product, Eq. 12).  Thread per path;
+// every [.][v][n] access is coalesced over paths.  For D <= MAXD all of a
+// path's inputs are loaded into registers before the (sequential) recurrence,
+// so the loads of all vertices are in flight at once (a path batch has few
+// threads: n = records / D).
+template <int MAXD>
+__global__ void __launch_bounds__(256) unwind_kernel(UnwindArgs a) {
+  const int64_t n = a.n;
+  const int D = a.max_depth, C = a.channels;
+  const float* __restrict__ le = a.le;
+  const float* __restrict__ fs = a.fs;
+  const float* __restrict__ cosv = a.cosv;
+  const float* __restrict__ pdf = a.pdf;
+  float* __restrict__ out = a.target;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int d = min(max(__ldg(a.depth + p), 0), D);
+    float L[3][MAXD], F[3][MAXD], cs[MAXD], pd[MAXD];
+#pragma unroll
+    for (int v = 0; v < MAXD; ++v) {
+      const int64_t at = (int64_t)v * n + p;
+      const bool in = v < d;
+      cs[v] = in ? __ldg(cosv + at) : 0.0f;
+      pd[v] = in ? __ldg(pdf + at) : 0.0f;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const bool inc = in && c < C;
+        L[c][v] = inc ? __ldg(le + (int64_t)c * D * n + at) : 0.0f;
+        F[c][v] = inc ? __ldg(fs + (int64_t)c * D * n + at) : 0.0f;
+      }
+    }
+    float li[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int v = MAXD - 1; v >= 0; --v) {
+      if (v >= D) continue;
+      const int64_t at = (int64_t)v * n + p;
+      const float q = v + 1 < MAXD ? pd[v + 1 < MAXD ? v + 1 : v] : 0.0f;   // p~ at the successor
+      const bool cont = v + 1 < d && isfinite(q) && q > 0.0f;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (c >= C) continue;
+        float acc = L[c][v];
+        if (cont) acc += __fdiv_rn(F[c][v + 1 < MAXD ? v + 1 : v] * cs[v + 1 < MAXD ? v + 1 : v], q) * li[c];
+        li[c] = v < d ? acc : 0.0f;
+        out[(int64_t)c * D * n + at] = a.product ? F[c][v] * li[c] * cs[v] : li[c];
+      }
+    }
+  }
+}
+
+// Same recurrence for long paths (D > 32), one vertex at a time.
+__global__ void __launch_bounds__(256) unwind_long_kernel(UnwindArgs a) {
+  const int64_t n = a.n;
+  const int D = a.max_depth, C = a.channels;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int d = min(max(__ldg(a.depth + p), 0), D);
+    float li[3] = {0.f, 0.f, 0.f};
+    for (int v = D - 1; v >= 0; --v) {
+      const int64_t at = (int64_t)v * n + p;
+      if (v >= d) {
+        for (int c = 0; c < C; ++c) a.target[(int64_t)c * D * n + at] = 0.0f;
+        continue;
+      }
+      const float q = v + 1 < d ? __ldg(a.pdf + at + n) : 0.0f;
+      const bool cont = isfinite(q) && q > 0.0f;
+      const float cs = cont ? __ldg(a.cosv + at + n) : 0.0f;
+      for (int c = 0; c < C; ++c) {
+        const int64_t ca = (int64_t)c * D * n + at;
+        float acc = __ldg(a.le + ca);
+        if (cont) acc += __fdiv_rn(__ldg(a.fs + ca + n) * cs, q) * li[c];   // (f_s cos) / p~ * Li
+        li[c] = acc;
+        a.target[ca] = a.product ? __ldg(a.fs + ca) * acc * __ldg(a.cosv + at) : acc;
+      }
+    }
+  }
+}
+
 // Initialisation (C-A21): Xavier-uniform weights, zero biases, features
 // U(-1e-2, 1e-2); uniforms from Philox keyed by the init seed.
 __global__ void init_kernel(float* p, int64_t n_mlp, int64_t n_total, uint64_t seed, int nl, int4 dims_in,
@@ -171,6 +250,17 @@ int launch_encode(int L, const QueryArgs& a, int sms, cudaStream_t st) {
 #undef NPM_L
     default: return -1;
   }
+}
+
+int launch_unwind(const UnwindArgs& a, int sms, cudaStream_t st) {
+  if (a.n == 0 || a.max_depth == 0) return 0;
+  const int64_t need = (a.n + 255) / 256;
+  const int blocks = (int)(need < (int64_t)sms * 8 ? need : (int64_t)sms * 8);
+  if (a.max_depth <= 4) unwind_kernel<4><<<blocks, 256, 0, st>>>(a);
+  else if (a.max_depth <= 8) unwind_kernel<8><<<blocks, 256, 0, st>>>(a);
+  else if (a.max_depth <= 16) unwind_kernel<16><<<blocks, 256, 0, st>>>(a);
+  else unwind_long_kernel<<<blocks, 256, 0, st>>>(a);
+  return 1;
 }
 
 int launch_adam(const AdamArgs& a, int sms, cudaStream_t st) {

@@ -35,6 +35,12 @@ struct QueryArgs {
   const float* u;           // [3][n] or NULL -> Philox
   uint64_t seed, offset;
   float *sx, *sy, *sz, *spdf;
+  // combined BSDF / guide sampling (f-1; C-A24..C-A26): u is [4][n] then
+  int combined;
+  float alpha;                        // BSDF selection probability
+  const float *bnx, *bny, *bnz;       // unit shading normals (BSDF stand-in)
+  float* gpdf;                        // V(w) at the returned direction (0 on fallback), optional
+  int32_t* tech;                      // 0 BSDF, 1 guide, 2 fallback; optional
 };
 
 struct TrainArgs {
@@ -79,6 +85,17 @@ int launch_train_forward(const NetShape& s, const TrainArgs& a, int num_sms, cud
 int launch_train_backward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_weight_grads(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_adam(const AdamArgs& a, int num_sms, cudaStream_t st);
+
+// Training-record unwind (f-1, C-A27): one thread per path.
+struct UnwindArgs {
+  const float *le, *fs;     // [C][D][n]
+  const float *cosv, *pdf;  // [D][n]
+  const int32_t* depth;     // [n]
+  float* target;            // [C][D][n]
+  int channels, max_depth, product;
+  int64_t n;
+};
+int launch_unwind(const UnwindArgs& a, int num_sms, cudaStream_t st);
 // Fused tcgen05/TMEM decoder paths (npm_tc_kernels.cuh).
 int launch_query_tc(const NetShape& s, const QueryArgs& a, int num_sms, cudaStream_t st);
 int launch_train_tc(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);

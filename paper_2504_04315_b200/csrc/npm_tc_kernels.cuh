@@ -465,12 +465,21 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       a.pdf[i] = Pt * invS;
     }
     if (a.do_sample) {
-      float3 u;
-      if (a.u) u = make_float3(__ldg(a.u + ic), __ldg(a.u + n + ic), __ldg(a.u + 2 * n + ic));
-      else u = philox_uniforms(a.seed, (uint64_t)ic + a.offset);
+      float4 u;
+      if (a.u) u = make_float4(__ldg(a.u + ic), __ldg(a.u + n + ic), __ldg(a.u + 2 * n + ic),
+                               a.combined ? __ldg(a.u + 3 * n + ic) : 1.0f);
+      else u = philox_uniforms4(a.seed, (uint64_t)ic + a.offset);
+      // f-1: BSDF with probability alpha (C-A25), else the guide
+      const bool use_bsdf = a.combined && u.w < a.alpha;
       const bool before = u.x < B[q] * invS;                 // an earlier quarter owns u1
       const bool after = u.x >= B[q + 1] * invS && q < TPR - 1;   // a later part owns u1
-      if (!before && !after) {
+      if (use_bsdf) {
+        if (q == 0) {
+          float wx, wy, wz;
+          bsdf_sample(__ldg(a.bnx + ic), __ldg(a.bny + ic), __ldg(a.bnz + ic), u.x, u.y, wx, wy, wz);
+          red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
+        }
+      } else if (!before && !after) {
         int sel = KQ - 1;
         float cum = B[q];
 #pragma unroll
@@ -494,11 +503,27 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       RS(4, q) = P2;
       __syncthreads();
       if (q == 0 && valid) {
-        a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
         float Pt = 0.0f;
 #pragma unroll
         for (int qq = 0; qq < TPR; ++qq) Pt += RS(4, qq);
-        a.spdf[i] = Pt * invS;
+        float V = Pt * invS, ox = wx, oy = wy, oz = wz, p = V;
+        if (a.combined) {
+          const float nx = __ldg(a.bnx + ic), ny = __ldg(a.bny + ic), nz = __ldg(a.bnz + ic);
+          int32_t t = use_bsdf ? 0 : 1;
+          if (!use_bsdf && !(isfinite(V) && V >= kVFloor)) {   // guide pdf underflow (C-A26)
+            bsdf_sample(nx, ny, nz, u.x, u.y, ox, oy, oz);
+            p = bsdf_pdf(nx, ny, nz, ox, oy, oz);
+            V = 0.0f;
+            t = 2;
+          } else {
+            // one-sample balance heuristic p~ = alpha p_bsdf + (1 - alpha) V
+            p = a.alpha * bsdf_pdf(nx, ny, nz, ox, oy, oz) + (1.0f - a.alpha) * V;
+          }
+          if (a.gpdf) a.gpdf[i] = V;
+          if (a.tech) a.tech[i] = t;
+        }
+        a.sx[i] = ox; a.sy[i] = oy; a.sz[i] = oz;
+        a.spdf[i] = p;
       }
     }
   }

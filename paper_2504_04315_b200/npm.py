@@ -82,6 +82,9 @@ def _load():
         "npm_decode": (I32, [M, ctypes.POINTER(npm_query), V, I32, V, V, V, V, V]),
         "npm_pdf": (I32, [M, ctypes.POINTER(npm_query), V, V, V, I32, V, V]),
         "npm_sample": (I32, [M, ctypes.POINTER(npm_query), V, U64, U64, I32, V, V, V, V, V, V, V, V, V]),
+        "npm_combined_sample": (I32, [M, ctypes.POINTER(npm_query), V, V, V, ctypes.c_float, V, U64, U64, I32,
+                                      V, V, V, V, V, V, V]),
+        "npm_unwind_records": (I32, [M, V, V, V, V, V, I32, I32, I64, I32, V, V]),
         "npm_train_step": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
                                  ctypes.POINTER(npm_step_stats), V]),
         "npm_accumulate_grads": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
@@ -190,6 +193,19 @@ def npm_sample(h, q, u, seed, offset, use_ema, wx, wy, wz, pdf, qx=None, qy=None
     _check(_lib.npm_sample(h, ctypes.byref(q), _ptr(u), int(seed), int(offset), int(use_ema), _ptr(wx),
                            _ptr(wy), _ptr(wz), _ptr(pdf), _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q),
                            _stream(stream)))
+
+
+def npm_combined_sample(h, q, nx, ny, nz, alpha, u, seed, offset, use_ema, wx, wy, wz, pdf, guide_pdf=None,
+                        technique=None, stream=None):
+    _check(_lib.npm_combined_sample(h, ctypes.byref(q), _ptr(nx), _ptr(ny), _ptr(nz), float(alpha), _ptr(u),
+                                    int(seed), int(offset), int(use_ema), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(pdf),
+                                    _ptr(guide_pdf), _ptr(technique), _stream(stream)))
+
+
+def npm_unwind_records(h, le, fs, cos_theta, pdf, depth, channels, max_depth, n_paths, product, target,
+                       stream=None):
+    _check(_lib.npm_unwind_records(h, _ptr(le), _ptr(fs), _ptr(cos_theta), _ptr(pdf), _ptr(depth), int(channels),
+                                   int(max_depth), int(n_paths), int(product), _ptr(target), _stream(stream)))
 
 
 def npm_train_step(h, q, wx, wy, wz, target, channels, spdf, n_global, want_stats=True, stream=None):
@@ -396,6 +412,30 @@ class Model:
             return wi, pdf, pdf_q
         npm_sample(self.h, q, u, seed, offset, use_ema, wi[0], wi[1], wi[2], pdf, stream=self._stream())
         return wi, pdf
+
+    def combined_sample(self, q, nrm, alpha=0.5, u=None, seed=0, offset=0, use_ema=False):
+        """f-1 one-sample MIS of the BSDF stand-in and the guide.  nrm: unit
+        shading normals [3, n]; u: [4, n] or None (Philox).  Returns
+        (wi [3, n], p~ [n], V(wi) [n], technique int32 [n])."""
+        n = q.n
+        nrm, u = self._f32(nrm), self._f32(u)
+        wi, pdf, gpdf = self._empty(3, n), self._empty(n), self._empty(n)
+        tech = self._empty(n, dtype=self.torch.int32)
+        npm_combined_sample(self.h, q, nrm[0], nrm[1], nrm[2], alpha, u, seed, offset, use_ema, wi[0], wi[1], wi[2],
+                            pdf, gpdf, tech, stream=self._stream())
+        return wi, pdf, gpdf, tech
+
+    def unwind_records(self, le, fs, cos_theta, pdf, depth, product=False):
+        """f-1 training-record unwind: le, fs [C, D, n]; cos_theta, pdf [D, n];
+        depth int32 [n] -> D^ [C, D, n]."""
+        le, fs, cos_theta, pdf = self._f32(le), self._f32(fs), self._f32(cos_theta), self._f32(pdf)
+        t = self.torch
+        depth = (t.from_numpy(np.ascontiguousarray(depth, dtype=np.int32)) if isinstance(depth, np.ndarray)
+                 else depth).to(device=self.device, dtype=t.int32).contiguous()
+        C, D, n = le.shape
+        out = self._empty(C, D, n)
+        npm_unwind_records(self.h, le, fs, cos_theta, pdf, depth, C, D, n, int(product), out, stream=self._stream())
+        return out
 
     def _train_args(self, wi, target, spdf):
         wi, target, spdf = self._f32(wi), self._f32(target), self._f32(spdf)
