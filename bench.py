@@ -325,7 +325,20 @@ def main():
             a1.record()
             torch.cuda.synchronize()
             ts.append(a0.elapsed_time(a1))
+        # f-3: the whole frame batch as 2^18-record micro-steps, one call
+        tsm = []
+        for _ in range(5):
+            flush.zero_()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            m.train_stream(qt, twi, ttg, tpd, micro_batch=k18, want_stats=False)
+            a1.record()
+            torch.cuda.synchronize()
+            tsm.append(a0.elapsed_time(a1))
+        f3 = {"frame_records": n, "micro_batch": k18, "micro_steps": (n + k18 - 1) // k18,
+              "ms": float(np.median(tsm)), "records_per_s": n / (float(np.median(tsm)) / 1e3)}
         paper_ctx = {"train_step_2e18_records_ms": float(np.median(ts)), "paper_rtx3070_ms": 10.0,
+                     "f3_micro_step_stream": f3,
                      "eval_1280x720_sample_plus_pdf_ms": 1e3 * t_q / K, "paper_eval_rtx3070_ms": 3.0,
                      "note": "paper numbers are another machine's (RTX 3070, P:309, P:482): context only"}
     # ---- roofline of the dominant kernel -----------------------------------------------------

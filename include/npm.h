@@ -220,6 +220,21 @@ npm_status npm_unwind_records(npm_model* model, const float* le, const float* fs
                               const float* pdf, const int32_t* depth, int channels, int max_depth, int64_t n_paths,
                               int product, float* target, void* stream);
 
+/* f-3, micro-step training on a frame's record stream ("split them
+ * into mini-batches for training. The optimization step is performed for
+ * each spp"; 2^18 samples per batch).  The n records of q (and wi,
+ * target [C][n], sample_pdf) are cut into consecutive micro-batches of
+ * micro_batch records (the last may be shorter); each is one full
+ * optimisation step: Eq. 9 with 1/N = that micro-batch's size, back
+ * propagation, Adam + EMA.  Equivalent to npm_train_step on each slice in
+ * order; single-GPU (the data-parallel form loops accumulate / allreduce /
+ * optimizer per micro-step in dp.py).  per_step: optional host array of
+ * ceil(n / micro_batch) stats (one host sync per micro-step when given).
+ * micro_batch <= 0 -> NPM_ERR_INVALID. */
+npm_status npm_train_stream(npm_model* model, const npm_query* q, const float* wix, const float* wiy,
+                            const float* wiz, const float* target, int target_channels, const float* sample_pdf,
+                            int64_t micro_batch, npm_step_stats* per_step, void* stream);
+
 /* One optimisation step ("optimization step is performed for each spp"):
  * Eq. 9 gradient over the batch, back propagation through decoder and grid
  * (P:216), [allreduce if a communicator is attached], Adam + EMA.

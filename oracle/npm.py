@@ -201,3 +201,18 @@ def train_step(state, q, wi, target, sample_pdf, n_global=None):
     stats['grad_norm_sq'] = float(np.sum(np.where(np.isfinite(g), g, 0.0) ** 2))
     stats['n_nonfinite_grad'] = optimizer_step(state, g)
     return g, stats
+
+
+def train_stream(state, q, wi, target, sample_pdf, micro_batch):
+    """f-3 ("split them into mini-batches for training. The optimization
+    step is performed for each spp"; P:482 2^18 per batch): one train_step per
+    consecutive micro-batch, 1/N = the micro-batch size.  Returns the list of
+    per-step (gradient, stats)."""
+    n = np.asarray(q['x']).shape[1]
+    out = []
+    for a in range(0, n, micro_batch):
+        b = min(a + micro_batch, n)
+        sl = lambda v: np.asarray(v)[..., a:b]
+        qs = {k: sl(v) for k, v in q.items()}
+        out.append(train_step(state, qs, sl(wi), sl(target), sl(sample_pdf), b - a))
+    return out

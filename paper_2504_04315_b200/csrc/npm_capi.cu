@@ -722,7 +722,7 @@ static npm_status read_stats(npm_model* m, cudaStream_t st, npm_step_stats* out,
 
 static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
                              const float* wiz, const float* target, int channels, const float* spdf,
-                             int64_t n_global, cudaStream_t st, Stager& s) {
+                             int64_t n_global, cudaStream_t st, Stager& s, int64_t target_stride = -1) {
   const size_t n = (size_t)q->n;
   npm_query d;
   stage_query(s, m, q, d);
@@ -733,6 +733,7 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.wox = d.wox; a.woy = d.woy; a.woz = d.woz; a.nx = d.nx; a.ny = d.ny; a.nz = d.nz; a.rough = d.rough;
   a.wx = s.in(wix, n); a.wy = s.in(wiy, n); a.wz = s.in(wiz, n);
   a.target = s.in(target, (size_t)channels * n);
+  a.target_stride = target_stride < 0 ? (int64_t)n : target_stride;   // strided only for device slices
   a.channels = channels;
   a.spdf = s.in(spdf, n);
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
@@ -845,6 +846,49 @@ static npm_status optimizer(npm_model* m, cudaStream_t st) {
   CUDA_TRY(cudaMemsetAsync(m->dstats + 1, 0, sizeof(double), st));
   CUDA_TRY(cudaMemsetAsync(m->dcount + 3, 0, sizeof(unsigned long long), st));
   return check_launch(m, timed(m, kKAdam, st, [&] { return launch_adam(a, m->num_sms, st); }));
+}
+
+npm_status npm_train_stream(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
+                            const float* wiz, const float* target, int channels, const float* spdf,
+                            int64_t micro_batch, npm_step_stats* per_step, void* stream) {
+  if (!train_args_ok(m, q, wix, wiy, wiz, target, channels, spdf, q ? (q->n > 0 ? q->n : 1) : 1) ||
+      micro_batch <= 0)
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  // stage the whole frame batch once; micro-steps then address device slices
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const int64_t n = q->n;
+  const float* dwx = s.in(wix, (size_t)n);
+  const float* dwy = s.in(wiy, (size_t)n);
+  const float* dwz = s.in(wiz, (size_t)n);
+  const float* dtg = s.in(target, (size_t)channels * n);
+  const float* dpd = s.in(spdf, (size_t)n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  int64_t j = 0;
+  for (int64_t a0 = 0; a0 < n; a0 += micro_batch, ++j) {
+    const int64_t b = a0 + micro_batch < n ? micro_batch : n - a0;
+    npm_query sub = d;
+    sub.n = b;
+    auto sl = [&](const float* p) { return p ? p + a0 : p; };
+    sub.px = sl(d.px); sub.py = sl(d.py); sub.pz = sl(d.pz);
+    sub.wox = sl(d.wox); sub.woy = sl(d.woy); sub.woz = sl(d.woz);
+    sub.nx = sl(d.nx); sub.ny = sl(d.ny); sub.nz = sl(d.nz); sub.rough = sl(d.rough);
+    Stager s2{m, st};   // device slices: pass-through
+    // one optimisation step per micro-batch: Eq. 9's 1/N over the micro-batch
+    npm_status r = accumulate(m, &sub, dwx + a0, dwy + a0, dwz + a0, dtg + a0, channels, dpd + a0, b, st, s2, n);
+    if (r != NPM_OK) return r;
+    if ((r = optimizer(m, st)) != NPM_OK) return r;
+    if (per_step) {
+      memset(per_step + j, 0, sizeof(npm_step_stats));
+      if ((r = read_stats(m, st, per_step + j, true, true)) != NPM_OK) return r;
+    }
+  }
+  return NPM_OK;
 }
 
 npm_status npm_optimizer_step(npm_model* m, npm_step_stats* stats, void* stream) {

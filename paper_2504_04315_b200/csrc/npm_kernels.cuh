@@ -48,7 +48,8 @@ struct TrainArgs {
   const uint32_t* perm;     // optional processing order (spatial binning); NULL = identity
   const float *px, *py, *pz, *wox, *woy, *woz, *nx, *ny, *nz, *rough;
   const float *wx, *wy, *wz;
-  const float* target;      // [C][n]
+  const float* target;      // [C][target_stride] (channel c at target + c * target_stride)
+  int64_t target_stride;    // = n unless the batch is a slice of a longer one (micro-steps)
   int channels;
   const float* spdf;        // p~
   double inv_n_global;

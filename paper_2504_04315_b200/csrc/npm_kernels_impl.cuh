@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads) train_forward_kernel(TrainArgs a) {
       float t = __ldg(a.target + i);
       bool all_zero = t == 0.0f;
       if (a.channels == 3) {
-        const float tg = __ldg(a.target + n + i), tb = __ldg(a.target + 2 * n + i);
+        const float tg = __ldg(a.target + a.target_stride + i), tb = __ldg(a.target + 2 * a.target_stride + i);
         all_zero = all_zero && tg == 0.0f && tb == 0.0f;   // D^ = 0 iff every channel is 0
         t = 0.2126f * t + 0.7152f * tg + 0.0722f * tb;
       }

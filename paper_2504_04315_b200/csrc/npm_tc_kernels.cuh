@@ -627,8 +627,8 @@ __global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
     // head inputs: issued now, consumed after the forward MMAs
     const float h_wx = __ldg(a.wx + ic), h_wy = __ldg(a.wy + ic), h_wz = __ldg(a.wz + ic);
     const float h_t0 = __ldg(a.target + ic);
-    const float h_t1 = a.channels == 3 ? __ldg(a.target + n + ic) : 0.f;
-    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * n + ic) : 0.f;
+    const float h_t1 = a.channels == 3 ? __ldg(a.target + a.target_stride + ic) : 0.f;
+    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * a.target_stride + ic) : 0.f;
     const float h_p = __ldg(a.spdf + ic);
     uint32_t mask[NL];   // ReLU mask bits of this quarter's WQ columns of X_1..X_{NL-1}
     // ---- encode: levels [q LQ, (q+1) LQ) -> features [q GQ, (q+1) GQ) of X0
@@ -1188,8 +1188,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
     const int64_t ih = hvalid ? (a.perm ? (int64_t)__ldg(a.perm + hslot) : hslot) : 0;
     const float h_wx = __ldg(a.wx + ih), h_wy = __ldg(a.wy + ih), h_wz = __ldg(a.wz + ih);
     const float h_t0 = __ldg(a.target + ih);
-    const float h_t1 = a.channels == 3 ? __ldg(a.target + n + ih) : 0.f;
-    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * n + ih) : 0.f;
+    const float h_t1 = a.channels == 3 ? __ldg(a.target + a.target_stride + ih) : 0.f;
+    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * a.target_stride + ih) : 0.f;
     const float h_p = __ldg(a.spdf + ih);
     uint32_t mask[NL];
     // ---- encode stores: this thread's levels of row re

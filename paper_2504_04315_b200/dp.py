@@ -86,3 +86,19 @@ class DataParallel:
             st["loss_proxy"], st["n_used"], st["n_zero_target"], st["n_dropped"] = (
                 v[0].item(), int(v[1].item()), int(v[2].item()), int(v[3].item()))
         return st
+
+    def train_stream(self, make_slice, n_local, micro_local, want_stats=False):
+        """f-3: micro-step training with one exchange per step.
+        Each rank cuts its n_local records into consecutive slices of
+        micro_local (make_slice(a, b) -> (q, wi, target, spdf) of local
+        records [a, b)); micro-step j is one optimisation step over the union
+        of every rank's slice j, N_global = world * slice size (equal shards).
+        Returns the per-step stats (reduced over ranks) if want_stats."""
+        out = []
+        for a in range(0, int(n_local), int(micro_local)):
+            b = min(a + int(micro_local), int(n_local))
+            q, wi, target, spdf = make_slice(a, b)
+            st = self.train_step(q, wi, target, spdf, n_local=b - a, want_stats=want_stats)
+            if want_stats:
+                out.append(st)
+        return out if want_stats else None

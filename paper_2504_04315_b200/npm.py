@@ -89,6 +89,8 @@ def _load():
                                  ctypes.POINTER(npm_step_stats), V]),
         "npm_accumulate_grads": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
                                        ctypes.POINTER(npm_step_stats), V]),
+        "npm_train_stream": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
+                                   ctypes.POINTER(npm_step_stats), V]),
         "npm_optimizer_step": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
         "npm_buffer_device_ptr": (I32, [M, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(I64)]),
         "npm_launch_count": (I64, [M]),
@@ -193,6 +195,14 @@ def npm_sample(h, q, u, seed, offset, use_ema, wx, wy, wz, pdf, qx=None, qy=None
     _check(_lib.npm_sample(h, ctypes.byref(q), _ptr(u), int(seed), int(offset), int(use_ema), _ptr(wx),
                            _ptr(wy), _ptr(wz), _ptr(pdf), _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q),
                            _stream(stream)))
+
+
+def npm_train_stream(h, q, wx, wy, wz, target, channels, spdf, micro_batch, want_stats=True, stream=None):
+    steps = (q.n + micro_batch - 1) // micro_batch if micro_batch > 0 else 0
+    arr = (npm_step_stats * max(steps, 1))() if want_stats else None
+    _check(_lib.npm_train_stream(h, ctypes.byref(q), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(target), int(channels),
+                                 _ptr(spdf), int(micro_batch), arr, _stream(stream)))
+    return [arr[i].as_dict() for i in range(steps)] if want_stats else None
 
 
 def npm_combined_sample(h, q, nx, ny, nz, alpha, u, seed, offset, use_ema, wx, wy, wz, pdf, guide_pdf=None,
@@ -436,6 +446,12 @@ class Model:
         out = self._empty(C, D, n)
         npm_unwind_records(self.h, le, fs, cos_theta, pdf, depth, C, D, n, int(product), out, stream=self._stream())
         return out
+
+    def train_stream(self, q, wi, target, spdf, micro_batch=1 << 18, want_stats=True):
+        """f-3: one optimisation step per consecutive micro-batch of the records."""
+        wi, target, spdf = self._train_args(wi, target, spdf)
+        return npm_train_stream(self.h, q, wi[0], wi[1], wi[2], target, target.shape[0], spdf, micro_batch,
+                                want_stats, self._stream())
 
     def _train_args(self, wi, target, spdf):
         wi, target, spdf = self._f32(wi), self._f32(target), self._f32(spdf)

@@ -105,3 +105,44 @@ def test_two_rank_gloo_step_equals_union_batch():
         assert a["n_used"] == b["n_used"] and a["n_dropped"] == b["n_dropped"]
         assert np.isclose(a["loss_proxy"], b["loss_proxy"], rtol=1e-12)
         assert np.isclose(a["grad_norm_sq"], b["grad_norm_sq"], rtol=1e-10)
+
+
+def _stream_worker(rank, world, port, n, micro_local, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg, q, wi, tgt, pdf = _batch(n, 8)
+    tr = OracleTrainer(cfg, random_params(cfg, np.random.default_rng(9)))
+    dp = DataParallel(tr, world)
+    a, b = shard_range(n, rank, world)
+
+    def make_slice(s0, s1):
+        sl = lambda x: np.ascontiguousarray(x[..., a + s0:a + s1])
+        return dict(x=sl(q["x"])), sl(wi), sl(tgt), sl(pdf)
+
+    stats = dp.train_stream(make_slice, b - a, micro_local, want_stats=True)
+    out[rank] = (tr.state.params.copy(), tr.state.t, stats)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_micro_step_stream_equals_union_micro_batches():
+    # f-3 with one exchange per micro-step: micro-step j is one optimisation
+    # step over the union of both ranks' slice j
+    n, micro_local, world = 60, 12, 2      # shards of 30 -> slices 12, 12, 6
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_stream_worker, args=(world, port, n, micro_local, out), nprocs=world, join=True)
+    p0, t0, s0 = out[0]
+    p1, t1, s1 = out[1]
+    assert np.array_equal(p0, p1) and t0 == t1 == 3
+    from oracle import npm as onpm
+    cfg, q, wi, tgt, pdf = _batch(n, 8)
+    st = onpm.State(cfg, random_params(cfg, np.random.default_rng(9)))
+    shards = [shard_range(n, r, world) for r in range(world)]
+    for j in range(3):
+        idx = np.concatenate([np.arange(a + j * micro_local, min(a + (j + 1) * micro_local, b)) for a, b in shards])
+        _, ref = onpm.train_step(st, dict(x=q["x"][:, idx]), wi[:, idx], tgt[..., idx], pdf[idx], idx.size)
+        assert s0[j]["n_used"] == ref["n_used"] and np.isclose(s0[j]["loss_proxy"], ref["loss_proxy"], rtol=1e-12)
+    assert np.allclose(p0, st.params, rtol=1e-12, atol=1e-14)

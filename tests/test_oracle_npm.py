@@ -97,3 +97,26 @@ def test_param_layout_counts():
     assert c1.resolutions == [2, 4, 8, 16] and c1.n_mlp == 1600 and c1.n_grid == 18720
     c4 = npm.Config(mode=npm.PRODUCT, n_lobes=16)
     assert c4.n_in == 65
+
+
+def test_train_stream_is_a_sequence_of_slice_steps():
+    # f-3 (P:298 one optimisation step per mini-batch; P:482 2^18 per batch):
+    # micro = n reproduces train_step; micro < n is train_step on each
+    # consecutive slice with 1/N = the slice size (last slice ragged)
+    cfg = tiny_cfg()
+    rng = np.random.default_rng(14)
+    p0 = random_params(cfg, rng) * 0.3
+    q, wi, tgt, pdf = random_batch(cfg, rng, 50)
+    a, b = npm.State(cfg, p0.copy()), npm.State(cfg, p0.copy())
+    npm.train_stream(a, q, wi, tgt, pdf, 50)
+    npm.train_step(b, q, wi, tgt, pdf)
+    assert np.array_equal(a.params, b.params) and a.t == b.t == 1
+    c, d = npm.State(cfg, p0.copy()), npm.State(cfg, p0.copy())
+    outs = npm.train_stream(c, q, wi, tgt, pdf, 20)
+    assert c.t == 3 and len(outs) == 3
+    for s0, s1 in ((0, 20), (20, 40), (40, 50)):
+        sl = lambda v: v[..., s0:s1]
+        g, st = npm.train_step(d, {k: sl(v) for k, v in q.items()}, sl(wi), sl(tgt), sl(pdf), s1 - s0)
+    assert np.array_equal(c.params, d.params) and np.array_equal(c.ema, d.ema)
+    # the micro-steps differ from one step over the union (not a reordering)
+    assert not np.allclose(c.params, a.params)
