@@ -33,4 +33,5 @@ vmf     Table 1 mappings, Eq. 3/4 pdf, Jakob sampling, Eq. 9 gradient head
 adam    Adam + EMA (C-O17, C-O18)
 npm     the model: encode / decode / pdf / sample / train_step
 guide   one-sample MIS of BSDF and guide, training-record unwind (f-1)
+product closed-form vMF product, cosine-lobe factorisation (f-2)
 """
