@@ -264,6 +264,11 @@ def main():
     dp_ = torch.randint(0, Dp + 1, (npaths,), device=dev, dtype=torch.int32, generator=g)
     tg_ = torch.empty(3, Dp, npaths, device=dev)
     t_unw = timed_ms(lambda: npm.npm_unwind_records(m.h, le_, fs_, cs_, pd_, dp_, 3, Dp, npaths, 0, tg_, stream=stream))
+    pq_ = torch.empty(n, device=dev)
+    t_cos = timed_ms(lambda: npm.npm_sample_cosine_product(m.h, qq, nrm[0], nrm[1], nrm[2], 2.1438, None, 0xC0FFEE, 0,
+                                                           True, cw[0], cw[1], cw[2], cp, wq[0], wq[1], wq[2], pq_,
+                                                           stream=stream))
+    f2 = {"cosine_product_sample_plus_pdf_ms": t_cos, "queries_per_s": n / (t_cos / 1e3), "kappa_c": 2.1438}
     f1 = {"combined_sample_ms": t_comb, "combined_sample_queries_per_s": n / (t_comb / 1e3), "alpha": 0.5,
           "unwind_ms": t_unw, "unwind_records_per_s": Dp * npaths / (t_unw / 1e3),
           "unwind_bytes_per_record": 4 * (3 + 3 + 1 + 1 + 3) + 4 / Dp,
@@ -422,7 +427,8 @@ def main():
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "gpu_launches_per_step": launches / K,
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
-                "clocks": clk.summary(), "cpu_baseline": cpu, "paper_context": paper_ctx, "f1_guided_mis": f1}
+                "clocks": clk.summary(), "cpu_baseline": cpu, "paper_context": paper_ctx, "f1_guided_mis": f1,
+                "f2_cosine_product": f2}
         print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()

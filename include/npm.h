@@ -186,6 +186,23 @@ npm_status npm_sample(npm_model* model, const npm_query* q, const float* u, uint
                       float* pdf, const float* qx, const float* qy, const float* qz,
                       float* pdf_q, void* stream);
 
+/* f-2, cosine-lobe product ("the cosine term could be approximated with
+ * a constant vMF lobe"; "closed-form product"): the decoded mixture is
+ * multiplied by v(. | n, kappa_c) and renormalised -- per lobe
+ * kappa_p mu_p = kappa mu + kappa_c n, weight lambda s / sum(lambda s) with
+ * s = C(kappa) C(kappa_c) / C(kappa_p) exp(kappa_p - kappa - kappa_c),
+ * C(k) = k / (2 pi (1 - e^{-2k})), C(0) = 1/(4 pi) (C-A28) -- then sampled and
+ * evaluated exactly as npm_sample (same u / Philox convention, optional fused
+ * pdf at qx/qy/qz).  nx/ny/nz: unit shading normals [n].  kappa_c in [0, 1e5]
+ * (C-A29 least-squares fit to the clamped cosine: 2.1438).  Optional outputs
+ * of the product mixture: lambda, kappa [K][n], mu [3][K][n].  Needs the
+ * tensor-core path. */
+npm_status npm_sample_cosine_product(npm_model* model, const npm_query* q, const float* nx, const float* ny,
+                                     const float* nz, float kappa_c, const float* u, uint64_t seed, uint64_t offset,
+                                     int use_ema, float* wix, float* wiy, float* wiz, float* pdf, const float* qx,
+                                     const float* qy, const float* qz, float* pdf_q, float* lambda, float* kappa,
+                                     float* mu, void* stream);
+
 /* f-1, guided one-sample MIS ("a combination of the BSDF importance
  * sampling and guiding distribution"; P:425 BSDF selection probability 50 %;
  * SPEC S:339-347).  Per query: u_sel < alpha -> BSDF sample, else a guide

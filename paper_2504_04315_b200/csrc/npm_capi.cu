@@ -639,6 +639,57 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   return NPM_OK;
 }
 
+npm_status npm_sample_cosine_product(npm_model* m, const npm_query* q, const float* nx, const float* ny,
+                                     const float* nz, float kappa_c, const float* u, uint64_t seed, uint64_t offset,
+                                     int use_ema, float* wix, float* wiy, float* wiz, float* pdf, const float* qx,
+                                     const float* qy, const float* qz, float* pdf_q, float* lambda, float* kappa,
+                                     float* mu, void* stream) {
+  if (!m || !query_ok(m, q) || !(kappa_c >= 0.0f && kappa_c <= 1e5f) ||
+      (q->n > 0 && (!nx || !ny || !nz || !wix || !wiy || !wiz || !pdf)))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  const bool fused = qx && qy && qz && pdf_q;
+  if ((qx || qy || qz || pdf_q) && !fused) return fail(NPM_ERR_INVALID, "fused query needs qx, qy, qz, pdf_q");
+  if (!m->use_tc) return fail(NPM_ERR_INVALID, "the cosine product needs the tensor-core query kernel");
+  if (q->n == 0) return NPM_OK;
+  DeviceGuard g(m->device);
+  std::lock_guard<std::mutex> lk(m->stage_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager s{m, st};
+  npm_query d;
+  stage_query(s, m, q, d);
+  const size_t n = (size_t)q->n;
+  const size_t K = (size_t)m->cfg.n_lobes;
+  QueryArgs a;
+  fill_query_args(m, d, use_ema, a);
+  a.do_sample = 1;
+  a.cos_product = 1;
+  a.kappa_c = kappa_c;
+  {
+    const double kc = kappa_c;
+    const double r = kc > 0.0 ? kc / -std::expm1(-2.0 * kc) : 0.5;
+    a.log_c_kc = (float)(std::log(r) - std::log(2.0 * 3.14159265358979323846));
+  }
+  a.u = s.in(u, 3 * n);
+  a.seed = seed;
+  a.offset = offset;
+  a.bnx = s.in(nx, n); a.bny = s.in(ny, n); a.bnz = s.in(nz, n);
+  if (fused) {
+    a.wx = s.in(qx, n); a.wy = s.in(qy, n); a.wz = s.in(qz, n);
+    a.pdf = s.out(pdf_q, n);
+  }
+  a.sx = s.out(wix, n); a.sy = s.out(wiy, n); a.sz = s.out(wiz, n); a.spdf = s.out(pdf, n);
+  a.lambda = s.out(lambda, K * n);
+  a.kappa = s.out(kappa, K * n);
+  a.mu = s.out(mu, 3 * K * n);
+  if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
+  npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+  if (r != NPM_OK) return r;
+  r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query_tc(m->shape, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  CUDA_TRY(s.finish());
+  return NPM_OK;
+}
+
 npm_status npm_combined_sample(npm_model* m, const npm_query* q, const float* nx, const float* ny,
                                const float* nz, float alpha, const float* u, uint64_t seed, uint64_t offset,
                                int use_ema, float* wix, float* wiy, float* wiz, float* pdf, float* guide_pdf,

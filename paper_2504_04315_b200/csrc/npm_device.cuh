@@ -298,6 +298,31 @@ __device__ __forceinline__ void lobe_sample(float kap, float mux, float muy, flo
   wz = w * muz + r * (cp * t1z + sp * t2z);
 }
 
+// log C(kappa), C(kappa) = kappa / (2 pi (1 - e^{-2 kappa})) the vMF normaliser
+// of the stable form (C-O9); C(0) = 1 / (4 pi) (C-A28).
+__device__ __forceinline__ float vmf_log_c(float k) {
+  const float r = k > 0.0f ? k / -expm1f(-2.0f * k) : 0.5f;
+  return logf(r) - 1.8378770664093453f;   // log(2 pi)
+}
+
+// Closed-form product of lobe (mu, kappa) with (n, kc) (f-2):
+// kappa_p mu_p = kappa mu + kc n; returns log of the scale s in
+// v v_c = s v(. | mu_p, kappa_p) and overwrites (mu, kappa) with the product.
+__device__ __forceinline__ float vmf_product_inplace(float& mx, float& my, float& mz, float& kap, float nx, float ny,
+                                                     float nz, float kc, float log_c_kc) {
+  const float sx = kap * mx + kc * nx, sy = kap * my + kc * ny, sz = kap * mz + kc * nz;
+  const float kp = sqrtf(sx * sx + sy * sy + sz * sz);
+  const float ls = vmf_log_c(kap) + log_c_kc - vmf_log_c(kp) + (kp - kap - kc);
+  if (kp > 0.0f) {
+    const float inv = 1.0f / kp;
+    mx = sx * inv; my = sy * inv; mz = sz * inv;
+  } else {
+    mx = nx; my = ny; mz = nz;   // uniform product (C-A28)
+  }
+  kap = fmaxf(kp, 1e-30f);   // keeps the sampler's -log(.)/kappa finite at kappa_p = 0
+  return ls;
+}
+
 // BSDF stand-in (C-A24, f-1): Lambertian about the unit shading normal n.
 // pdf max(n.w, 0) / pi; cosine-weighted sample r = sqrt(u1), phi = 2 pi u2,
 // local (r cos phi, r sin phi, sqrt(1 - u1)) in the Duff ONB of n.

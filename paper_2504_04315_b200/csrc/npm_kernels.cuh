@@ -41,6 +41,10 @@ struct QueryArgs {
   const float *bnx, *bny, *bnz;       // unit shading normals (BSDF stand-in)
   float* gpdf;                        // V(w) at the returned direction (0 on fallback), optional
   int32_t* tech;                      // 0 BSDF, 1 guide, 2 fallback; optional
+  // cosine-lobe product (f-2, C-A28/C-A29): the decoded mixture times
+  // v(. | n, kappa_c), renormalised, before sampling / pdf; normals in bnx..
+  int cos_product;
+  float kappa_c, log_c_kc;            // kappa_c and log C(kappa_c) (host-computed)
 };
 
 struct TrainArgs {

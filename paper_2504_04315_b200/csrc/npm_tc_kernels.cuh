@@ -419,6 +419,18 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       float em;
       nrm[j] = lobe_norm(kap[j], em);
     }
+    if (a.cos_product) {   // f-2: times the cosine lobe about n, renormalised via the logits
+      const float nx = valid ? __ldg(a.bnx + ic) : 0.0f, ny = valid ? __ldg(a.bny + ic) : 0.0f,
+                  nz = valid ? __ldg(a.bnz + ic) : 1.0f;
+      mloc = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < KQ; ++j) {
+        lp[j] += vmf_product_inplace(mx[j], my[j], mz[j], kap[j], nx, ny, nz, a.kappa_c, a.log_c_kc);
+        float em;
+        nrm[j] = lobe_norm(fmaxf(kap[j], 1e-30f), em);
+        mloc = fmaxf(mloc, lp[j]);
+      }
+    }
     if (valid && a.kappa) {
 #pragma unroll
       for (int j = 0; j < KQ; ++j) a.kappa[(int64_t)(q * KQ + j) * n + i] = kap[j];

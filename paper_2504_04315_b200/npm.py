@@ -82,6 +82,8 @@ def _load():
         "npm_decode": (I32, [M, ctypes.POINTER(npm_query), V, I32, V, V, V, V, V]),
         "npm_pdf": (I32, [M, ctypes.POINTER(npm_query), V, V, V, I32, V, V]),
         "npm_sample": (I32, [M, ctypes.POINTER(npm_query), V, U64, U64, I32, V, V, V, V, V, V, V, V, V]),
+        "npm_sample_cosine_product": (I32, [M, ctypes.POINTER(npm_query), V, V, V, ctypes.c_float, V, U64, U64,
+                                            I32, V, V, V, V, V, V, V, V, V, V, V, V]),
         "npm_combined_sample": (I32, [M, ctypes.POINTER(npm_query), V, V, V, ctypes.c_float, V, U64, U64, I32,
                                       V, V, V, V, V, V, V]),
         "npm_unwind_records": (I32, [M, V, V, V, V, V, I32, I32, I64, I32, V, V]),
@@ -203,6 +205,14 @@ def npm_train_stream(h, q, wx, wy, wz, target, channels, spdf, micro_batch, want
     _check(_lib.npm_train_stream(h, ctypes.byref(q), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(target), int(channels),
                                  _ptr(spdf), int(micro_batch), arr, _stream(stream)))
     return [arr[i].as_dict() for i in range(steps)] if want_stats else None
+
+
+def npm_sample_cosine_product(h, q, nx, ny, nz, kappa_c, u, seed, offset, use_ema, wx, wy, wz, pdf, qx=None, qy=None,
+                              qz=None, pdf_q=None, lam=None, kappa=None, mu=None, stream=None):
+    _check(_lib.npm_sample_cosine_product(h, ctypes.byref(q), _ptr(nx), _ptr(ny), _ptr(nz), float(kappa_c), _ptr(u),
+                                          int(seed), int(offset), int(use_ema), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(pdf),
+                                          _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q), _ptr(lam), _ptr(kappa), _ptr(mu),
+                                          _stream(stream)))
 
 
 def npm_combined_sample(h, q, nx, ny, nz, alpha, u, seed, offset, use_ema, wx, wy, wz, pdf, guide_pdf=None,
@@ -434,6 +444,24 @@ class Model:
         npm_combined_sample(self.h, q, nrm[0], nrm[1], nrm[2], alpha, u, seed, offset, use_ema, wi[0], wi[1], wi[2],
                             pdf, gpdf, tech, stream=self._stream())
         return wi, pdf, gpdf, tech
+
+    def sample_cosine_product(self, q, nrm, kappa_c=2.1438, u=None, seed=0, offset=0, use_ema=False, wq=None):
+        """f-2: sample / pdf of the mixture times the cosine lobe about nrm.
+        Returns (wi [3, n], pdf [n], pdf_q [n] or None, lambda [K, n],
+        kappa [K, n], mu [3, K, n]) of the product mixture."""
+        n, K = q.n, self.K
+        nrm, u = self._f32(nrm), self._f32(u)
+        wi, pdf = self._empty(3, n), self._empty(n)
+        lam, kap, mu = self._empty(K, n), self._empty(K, n), self._empty(3, K, n)
+        pdf_q = None
+        qx = qy = qz = None
+        if wq is not None:
+            wq = self._f32(wq)
+            qx, qy, qz = wq[0], wq[1], wq[2]
+            pdf_q = self._empty(n)
+        npm_sample_cosine_product(self.h, q, nrm[0], nrm[1], nrm[2], kappa_c, u, seed, offset, use_ema, wi[0], wi[1],
+                                  wi[2], pdf, qx, qy, qz, pdf_q, lam, kap, mu, stream=self._stream())
+        return wi, pdf, pdf_q, lam, kap, mu
 
     def unwind_records(self, le, fs, cos_theta, pdf, depth, product=False):
         """f-1 training-record unwind: le, fs [C, D, n]; cos_theta, pdf [D, n];
