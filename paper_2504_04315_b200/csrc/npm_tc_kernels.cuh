@@ -240,8 +240,11 @@ __device__ __forceinline__ void teardown_cta(uint32_t tbase, int tcols) {
 // B_q = sum_{q'<q} S_q' (S_q = sum of the quarter's e^{lambda'-M}) are
 // computed identically by the 4 threads of a row, so exactly one quarter owns
 // u1 and picks its first lobe with u1 < C_i (its last lobe at C = B_{q+1}).
-template <class N, int TPR>
+template <class N, int TPR, int MODE>
 __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a) {
+  // MODE (compile time, so the plain query carries none of the variants' code):
+  // 0 guide sampling / pdf; 1 combined BSDF/guide MIS (f-1); 2 cosine product (f-2)
+  constexpr bool COMBINED = MODE == 1, COSPROD = MODE == 2;
   using T = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W;
   constexpr int KQ = K / TPR, WQ = W / TPR, LQ = N::L / TPR, GQ = 4 * LQ;
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       float em;
       nrm[j] = lobe_norm(kap[j], em);
     }
-    if (a.cos_product) {   // f-2: times the cosine lobe about n, renormalised via the logits
+    if (COSPROD) {   // f-2: times the cosine lobe about n, renormalised via the logits
       const float nx = valid ? __ldg(a.bnx + ic) : 0.0f, ny = valid ? __ldg(a.bny + ic) : 0.0f,
                   nz = valid ? __ldg(a.bnz + ic) : 1.0f;
       mloc = -INFINITY;
@@ -479,10 +482,10 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
     if (a.do_sample) {
       float4 u;
       if (a.u) u = make_float4(__ldg(a.u + ic), __ldg(a.u + n + ic), __ldg(a.u + 2 * n + ic),
-                               a.combined ? __ldg(a.u + 3 * n + ic) : 1.0f);
+                               COMBINED ? __ldg(a.u + 3 * n + ic) : 1.0f);
       else u = philox_uniforms4(a.seed, (uint64_t)ic + a.offset);
       // f-1: BSDF with probability alpha (C-A25), else the guide
-      const bool use_bsdf = a.combined && u.w < a.alpha;
+      const bool use_bsdf = COMBINED && u.w < a.alpha;
       const bool before = u.x < B[q] * invS;                 // an earlier quarter owns u1
       const bool after = u.x >= B[q + 1] * invS && q < TPR - 1;   // a later part owns u1
       if (use_bsdf) {
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
 #pragma unroll
         for (int qq = 0; qq < TPR; ++qq) Pt += RS(4, qq);
         float V = Pt * invS, ox = wx, oy = wy, oz = wz, p = V;
-        if (a.combined) {
+        if (COMBINED) {
           const float nx = __ldg(a.bnx + ic), ny = __ldg(a.bny + ic), nz = __ldg(a.bnz + ic);
           int32_t t = use_bsdf ? 0 : 1;
           if (!use_bsdf && !(isfinite(V) && V >= kVFloor)) {   // guide pdf underflow (C-A26)
@@ -1476,12 +1479,14 @@ struct TcLaunch {
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA
     // waits interleave); ~104 KB smem each.
     constexpr int TPR = 2;
-    cudaFuncSetAttribute(tc_query_kernel<N, TPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
+    auto kern = a.combined ? tc_query_kernel<N, TPR, 1> : a.cos_product ? tc_query_kernel<N, TPR, 2>
+                                                                          : tc_query_kernel<N, TPR, 0>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
     const int64_t ntiles = (a.n + R - 1) / R;
     const int per_sm = (int)((228u * 1024u) / (T::SMEM_QUERY + 1024u)) >= 2 ? 2 : 1;
     const int64_t cap = (int64_t)sms * per_sm;
     const int blocks = (int)(ntiles < cap ? ntiles : cap);
-    tc_query_kernel<N, TPR><<<blocks, TPR * R, T::SMEM_QUERY, st>>>(a);
+    kern<<<blocks, TPR * R, T::SMEM_QUERY, st>>>(a);
     return 1;
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
