@@ -5,14 +5,20 @@
 // few cache lines.  Results are independent of
 // the order up to fp32 summation order.
 //
-// Pass 1 (bin_count): each CTA histograms its contiguous chunk in smem and
+// Pass 1 (bin_count): each CTA histograms its contiguous span in smem and
 //   adds its non-zero bins to the global histogram (one atomic per
 //   (CTA, bin), not per sample: the samples lie on surfaces, so a few bins
 //   are hot and per-sample atomics serialise on them).
-// Pass 2 (bin_scan): exclusive scan of the 4096 bin totals (one CTA).
-// Pass 3 (bin_place): each CTA re-histograms its chunk, reserves its range in
+// Pass 2 (bin_scan): exclusive scan of the bin totals (one CTA).
+// Pass 3 (bin_place): each CTA re-histograms its span, reserves its range in
 //   every non-zero bin with one atomic, then places its samples with smem
 //   atomics.
+// Sort chunks: batches above kSortChunk samples are sorted in independent
+// consecutive chunks (histogram row = chunk, chunk-major scan), so that the
+// scattered per-sample input reads and output writes of a binned launch stay
+// inside one chunk's window (~44 MB of SoA I/O at 2^20 queries), which the
+// 126 MB L2 merges before write-back.  Measured on B200 (c3, 8.4 M queries):
+// one global sort made the query kernel 44 % slower per query than at c2.
 #include "npm_kernels.cuh"
 
 namespace npm {
@@ -42,8 +48,8 @@ __device__ __forceinline__ uint32_t bin_key(const float* px, const float* py, co
 __global__ void __launch_bounds__(kThreads) bin_count_kernel(const float* __restrict__ px,
                                                              const float* __restrict__ py,
                                                              const float* __restrict__ pz, int64_t n,
-                                                             int64_t chunk, GridDesc g, uint32_t* __restrict__ keys,
-                                                             uint32_t* __restrict__ hist) {
+                                                             int64_t chunk, int64_t sort_chunk, GridDesc g,
+                                                             uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[kBins];
   for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
   __syncthreads();
@@ -54,19 +60,20 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(const float* __rest
     atomicAdd(h + k, 1u);
   }
   __syncthreads();
+  hist += (i0 / sort_chunk) * kBins;   // this span's sort-chunk row
   for (int b = threadIdx.x; b < kBins; b += blockDim.x)
     if (h[b]) atomicAdd(hist + b, h[b]);
 }
 
-// Exclusive scan of kBins counters (one CTA of kThreads, kBins / kThreads each).
-__global__ void __launch_bounds__(kThreads) bin_scan_kernel(uint32_t* hist) {
-  constexpr int PER = kBins / kThreads;
+// Exclusive scan of nb counters (one CTA of kThreads; thread t owns the
+// contiguous run [t per, (t+1) per)).
+__global__ void __launch_bounds__(kThreads) bin_scan_kernel(uint32_t* hist, int nb) {
   __shared__ uint32_t warp_tot[kThreads / 32];
   const int t = threadIdx.x;
-  uint32_t v[PER];
+  const int per = (nb + kThreads - 1) / kThreads;
+  const int b0 = min(t * per, nb), b1 = min(b0 + per, nb);
   uint32_t s = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) { v[j] = hist[t * PER + j]; s += v[j]; }
+  for (int j = b0; j < b1; ++j) s += hist[j];
   uint32_t inc = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -87,12 +94,16 @@ __global__ void __launch_bounds__(kThreads) bin_scan_kernel(uint32_t* hist) {
   }
   __syncthreads();
   uint32_t run = warp_tot[t >> 5] + inc - s;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) { hist[t * PER + j] = run; run += v[j]; }
+  for (int j = b0; j < b1; ++j) {
+    const uint32_t v = hist[j];
+    hist[j] = run;
+    run += v;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __restrict__ keys, int64_t n,
-                                                             int64_t chunk, uint32_t* __restrict__ cursor,
+                                                             int64_t chunk, int64_t sort_chunk,
+                                                             uint32_t* __restrict__ cursor,
                                                              uint32_t* __restrict__ perm) {
   __shared__ uint32_t h[kBins];
   for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
@@ -100,6 +111,7 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
   const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(i0 + chunk, n);
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(h + keys[i], 1u);
   __syncthreads();
+  cursor += (i0 / sort_chunk) * kBins;
   for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
     const uint32_t c = h[b];
     h[b] = c ? atomicAdd(cursor + b, c) : 0u;   // this CTA's range in bin b
@@ -113,16 +125,30 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
 
 }  // namespace
 
-int launch_bin(const float* px, const float* py, const float* pz, int64_t n, const GridDesc& g, uint32_t* keys,
-               uint32_t* hist, uint32_t* perm, int sms, cudaStream_t st) {
+int bin_hist_entries(int64_t n, int64_t sort_chunk) {
+  const int64_t chunks = n <= sort_chunk ? 1 : (n + sort_chunk - 1) / sort_chunk;
+  return (int)(chunks * kBins);
+}
+
+// sort_chunk: n (one global sort) or kSortChunk (a multiple of 32 * 4096)
+int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int64_t sort_chunk, const GridDesc& g,
+               uint32_t* keys, uint32_t* hist, uint32_t* perm, int sms, cudaStream_t st) {
   if (n == 0) return 0;
-  cudaMemsetAsync(hist, 0, kBins * sizeof(uint32_t), st);
-  const int64_t want = (n + 4095) / 4096;
-  const int blocks = (int)(want < (int64_t)sms * 2 ? want : (int64_t)sms * 2);
-  const int64_t chunk = (n + blocks - 1) / blocks;
-  bin_count_kernel<<<blocks, kThreads, 0, st>>>(px, py, pz, n, chunk, g, keys, hist);
-  bin_scan_kernel<<<1, kThreads, 0, st>>>(hist);
-  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, chunk, hist, perm);
+  if (sort_chunk >= n) sort_chunk = n;
+  const int nb = bin_hist_entries(n, sort_chunk);
+  cudaMemsetAsync(hist, 0, (size_t)nb * sizeof(uint32_t), st);
+  int64_t span;
+  if (sort_chunk == n) {   // one sort over the whole batch
+    const int64_t want = (n + 4095) / 4096;
+    const int blocks = (int)(want < (int64_t)sms * 2 ? want : (int64_t)sms * 2);
+    span = (n + blocks - 1) / blocks;
+  } else {                 // chunks of sort_chunk; CTA spans never straddle a chunk
+    span = sort_chunk / 32;
+  }
+  const int blocks = (int)((n + span - 1) / span);
+  bin_count_kernel<<<blocks, kThreads, 0, st>>>(px, py, pz, n, span, sort_chunk, g, keys, hist);
+  bin_scan_kernel<<<1, kThreads, 0, st>>>(hist, nb);
+  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, span, sort_chunk, hist, perm);
   return 3;
 }
 

@@ -212,6 +212,15 @@ npm_status check_launch(npm_model* m, int r) {
   return NPM_OK;
 }
 
+// Sort-chunk of the binning (npm_bin.cu): with L2-resident grid tables the
+// scattered SoA I/O of a binned launch is the cost, so batches are sorted in
+// chunks of kSortChunk (B200, c3: query 3.47 -> 2.38 ms); with HBM-resident
+// tables (> 64 MB) the gathers dominate and one global sort keeps the most
+// coherence (c5: chunking cost +0.2 ms).
+static int64_t sort_chunk(const npm_model* m, int64_t n) {
+  return m->n_grid * 4 > ((int64_t)64 << 20) ? n : (n < kSortChunk ? n : kSortChunk);
+}
+
 // Spatial binning of a device-resident position batch (npm_bin.cu); returns
 // the processing order, or NULL (identity) for small batches / when disabled.
 npm_status maybe_bin(npm_model* m, const float* px, const float* py, const float* pz, int64_t n, cudaStream_t st,
@@ -221,11 +230,11 @@ npm_status maybe_bin(npm_model* m, const float* px, const float* py, const float
   cudaError_t e;
   if ((e = m->bin_keys.ensure(n * sizeof(uint32_t))) != cudaSuccess ||
       (e = m->bin_perm.ensure(n * sizeof(uint32_t))) != cudaSuccess ||
-      (e = m->bin_hist.ensure(((size_t)1 << kBinBits) * sizeof(uint32_t))) != cudaSuccess)
+      (e = m->bin_hist.ensure((size_t)bin_hist_entries(n, sort_chunk(m, n)) * sizeof(uint32_t))) != cudaSuccess)
     return fail(NPM_ERR_OOM, "binning scratch");
   uint32_t* p = static_cast<uint32_t*>(m->bin_perm.p);
   npm_status r = check_launch(m, timed(m, kKBin, st, [&] {
-    return launch_bin(px, py, pz, n, m->grid, static_cast<uint32_t*>(m->bin_keys.p),
+    return launch_bin(px, py, pz, n, sort_chunk(m, n), m->grid, static_cast<uint32_t*>(m->bin_keys.p),
                       static_cast<uint32_t*>(m->bin_hist.p), p, m->num_sms, st);
   }));
   if (r == NPM_OK) *perm = p;

@@ -115,6 +115,8 @@ namespace npm {
 // warp are spatially clustered and their grid gathers / scatter-adds touch
 // few cache lines.  perm[t] = original index of the t-th processed sample.
 constexpr int kBinBits = 12;
-int launch_bin(const float* px, const float* py, const float* pz, int64_t n, const GridDesc& g,
+constexpr int64_t kSortChunk = 1 << 20;   // sort-chunk for L2-resident tables (npm_capi.cu)
+int bin_hist_entries(int64_t n, int64_t sort_chunk);   // histogram entries launch_bin needs
+int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int64_t sort_chunk, const GridDesc& g,
                uint32_t* keys, uint32_t* hist, uint32_t* perm, int num_sms, cudaStream_t st);
 }  // namespace npm
