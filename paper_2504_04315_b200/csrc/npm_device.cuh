@@ -301,8 +301,10 @@ __device__ __forceinline__ void lobe_sample(float kap, float mux, float muy, flo
 // log C(kappa), C(kappa) = kappa / (2 pi (1 - e^{-2 kappa})) the vMF normaliser
 // of the stable form (C-O9); C(0) = 1 / (4 pi) (C-A28).
 __device__ __forceinline__ float vmf_log_c(float k) {
-  const float r = k > 0.0f ? k / -expm1f(-2.0f * k) : 0.5f;
-  return logf(r) - 1.8378770664093453f;   // log(2 pi)
+  // 1 - e^{-2k}: precise expm1 only where it matters (small k); MUFU elsewhere
+  const float em = k < 0.35f ? -expm1f(-2.0f * k) : 1.0f - __expf(-2.0f * k);
+  const float r = k > 0.0f ? __fdividef(k, em) : 0.5f;
+  return __logf(r) - 1.8378770664093453f;   // log(2 pi)
 }
 
 // Closed-form product of lobe (mu, kappa) with (n, kc) (f-2):
