@@ -1163,7 +1163,14 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
     float ux, uy, uz;
     float gf[4 * LJ];
   };
-  auto load_tile = [&](int64_t tl, TileIn& t) {
+  // Next-tile encode.  SPREAD: positions loaded under the last forward MMA
+  // (before the head) and level j's gathers issued under backward batch
+  // gstep(j); else all of it under the last backward batch.  Measured on B200:
+  // spreading helps the product shape (c4 train 4.11 -> 3.87 ms, more MMA
+  // latency to cover) and costs c2 / c5 2-3 % (their gathers are throughput-
+  // bound on L1TEX, so moving them only lengthens the other phases).
+  constexpr bool SPREAD = N::PRODUCT;
+  auto load_pos = [&](int64_t tl, TileIn& t) {
     const int64_t slot = tl * RT + re;
     t.valid = slot < n;
     t.i = t.valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
@@ -1172,18 +1179,22 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
       t.ux = normalize_axis(__ldg(a.px + t.i), a.grid.lo[0], a.grid.inv[0]);
       t.uy = normalize_axis(__ldg(a.py + t.i), a.grid.lo[1], a.grid.inv[1]);
       t.uz = normalize_axis(__ldg(a.pz + t.i), a.grid.lo[2], a.grid.inv[2]);
-#pragma unroll
-      for (int j = 0; j < LJ; ++j) {
-        const int l = h * (L / 2) + 2 * j + (c >> 1);
-        LevelCorners lc;
-        level_corners(a.grid, l, t.ux, t.uy, t.uz, lc);
-        const float4 gl = gather_level(tab, a.grid.off[l], lc);
-        t.gf[4 * j] = gl.x; t.gf[4 * j + 1] = gl.y; t.gf[4 * j + 2] = gl.z; t.gf[4 * j + 3] = gl.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4 * LJ; ++j) t.gf[j] = 0.0f;
     }
+  };
+  auto gather_lv = [&](TileIn& t, int j) {
+    float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t.valid) {
+      const int l = h * (L / 2) + 2 * j + (c >> 1);
+      LevelCorners lc;
+      level_corners(a.grid, l, t.ux, t.uy, t.uz, lc);
+      gl = gather_level(tab, a.grid.off[l], lc);
+    }
+    t.gf[4 * j] = gl.x; t.gf[4 * j + 1] = gl.y; t.gf[4 * j + 2] = gl.z; t.gf[4 * j + 3] = gl.w;
+  };
+  auto load_tile = [&](int64_t tl, TileIn& t) {
+    load_pos(tl, t);
+#pragma unroll
+    for (int j = 0; j < LJ; ++j) gather_lv(t, j);
   };
   const int64_t first_tile = (int64_t)blockIdx.x * 2 + g;
   const int64_t tstride = (int64_t)gridDim.x * 2;
@@ -1232,6 +1243,9 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
       }
     }
     // ---- forward
+    const bool has_next = tile + tstride < ntiles;
+    TileIn nxt;
+    nxt.valid = false;
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       handoff();
@@ -1243,6 +1257,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
           else issue_fwd_g(IC<1>{}, KC);
         });
       }
+      if (SPREAD && k == NL - 1 && has_next) load_pos(tile + tstride, nxt);
       gwait();
       NPM_STAMP64(2 + 2 * k);
       const float* b = bias + TB::boff(k) / 4;
@@ -1367,7 +1382,6 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
     }
     // ---- backward
     uint32_t dhi = dlast_hi, dlo = dlast_lo;
-    TileIn nxt;
 #pragma unroll
     for (int k = NL - 1; k >= 0; --k) {
       handoff();
@@ -1379,7 +1393,12 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
           else issue_bwd_g(IC<1>{}, KC);
         });
       }
-      if (k == 0 && tile + tstride < ntiles) load_tile(tile + tstride, nxt);
+      if (SPREAD && has_next) {
+#pragma unroll
+        for (int j = 0; j < LJ; ++j)
+          if ((NL - 1 - j > 0 ? NL - 1 - j : 0) == k) gather_lv(nxt, j);   // gstep(j)
+      }
+      if (!SPREAD && k == 0 && has_next) load_tile(tile + tstride, nxt);
       gwait();
       NPM_STAMP64(2 + 2 * NL + 2 * (NL - 1 - k));
       if (k > 0) {
