@@ -20,6 +20,7 @@ import numpy as np
 from . import grid, mlp, sh, vmf, adam
 
 RADIANCE, PRODUCT = 0, 1
+KL, CHI2 = 0, 1   # training divergence (f-4; "Other divergence metrics are also available")
 LUMA = np.array([0.2126, 0.7152, 0.0722])
 
 
@@ -44,6 +45,7 @@ class Config:
     ema_decay: float = 0.99
     kappa_min: float = 1e-5
     kappa_max: float = 1e5
+    divergence: int = KL
 
     @property
     def resolutions(self):
@@ -156,8 +158,25 @@ def gradient(cfg, flat, q, wi, target, sample_pdf, n_global):
     wi = np.asarray(wi, np.float64)
     tgt = np.asarray(target, np.float64)
     is_zero = (tgt == 0).all(axis=0) if tgt.ndim == 2 else (tgt == 0)
-    s, dropped, zero = vmf.record_scale(scalar_target(target), np.asarray(sample_pdf, np.float64), n_global,
-                                        is_zero)
+    t = scalar_target(target)
+    s, dropped, zero = vmf.record_scale(t, np.asarray(sample_pdf, np.float64), n_global, is_zero)
+    if cfg.divergence == CHI2:
+        # f-4 (C-A31): Pearson chi^2, D_chi2 = int D^2 / V - 1, MC estimate
+        # (1/N) sum (D^/p~) D^ / V; its gradient is -(1/N) sum (D^/p~)(D^/V) grad log V,
+        # i.e. Eq. 9's head with the record scale s multiplied by D^ / V
+        vbar = np.maximum(vmf.mixture_pdf(wi, vmf.activate(raw, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)),
+                          vmf.V_FLOOR)
+        tt = np.where(dropped | zero, 0.0, t)
+        chi = tt / vbar
+        s_chi = s * chi
+        draw, _ = vmf.grad_head(raw, wi, s_chi, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
+        mgrads, dz = mlp.backward(layers, pres, inputs, draw)
+        gl = cfg.n_levels * cfg.n_features
+        ggrads = grid.scatter_grad(q['x'], cfg.aabb_lo, cfg.aabb_hi, cfg.resolutions, cfg.table_sizes,
+                                   dz[:gl], cfg.n_features)
+        stats = dict(loss_proxy=float((-s * chi).sum()), n_used=int((~dropped & ~zero).sum()),
+                     n_zero_target=int(zero.sum()), n_dropped=int(dropped.sum()))
+        return pack(cfg, mgrads, ggrads), stats
     draw, logv = vmf.grad_head(raw, wi, s, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
     mgrads, dz = mlp.backward(layers, pres, inputs, draw)
     gl = cfg.n_levels * cfg.n_features

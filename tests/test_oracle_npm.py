@@ -120,3 +120,55 @@ def test_train_stream_is_a_sequence_of_slice_steps():
     assert np.array_equal(c.params, d.params) and np.array_equal(c.ema, d.ema)
     # the micro-steps differ from one step over the union (not a reordering)
     assert not np.allclose(c.params, a.params)
+
+
+def chi2_loss_from_forward(cfg, flat, q, wi, target, pdf, n_global):
+    # f-4: the MC estimate of int D^2 / V ("other divergence metrics"),
+    # (1/N) sum (D^/p~) D^ / max(V, 1e-30), written from the forward functions
+    t = npm.scalar_target(target)
+    v = np.maximum(npm.pdf(cfg, flat, q, wi), 1e-30)
+    return float((t / pdf * t / v).sum() / n_global)
+
+
+@pytest.mark.parametrize("mode", [npm.RADIANCE, npm.PRODUCT])
+def test_chi2_gradient_vs_fd(mode):
+    cfg = tiny_cfg(mode)
+    cfg.divergence = npm.CHI2
+    rng = np.random.default_rng(20 + mode)
+    flat = random_params(cfg, rng)
+    q, wi, tgt, pdf = random_batch(cfg, rng, 30)
+    g, stats = npm.gradient(cfg, flat, q, wi, tgt, pdf, 30)
+    assert np.isclose(stats['loss_proxy'], chi2_loss_from_forward(cfg, flat, q, wi, tgt, pdf, 30), rtol=1e-12)
+    # the 1/V of chi^2 is more curved than log V: Richardson-extrapolated central FD
+    L = lambda f: chi2_loss_from_forward(cfg, f, q, wi, tgt, pdf, 30)
+
+    def cfd(j, h):
+        fp, fm = flat.copy(), flat.copy()
+        fp[j] += h; fm[j] -= h
+        return (L(fp) - L(fm)) / (2 * h)
+    idx = list(rng.choice(cfg.n_mlp, 25, replace=False)) + list(np.flatnonzero(g[cfg.n_mlp:] != 0)[:20] + cfg.n_mlp)
+    for j in idx:
+        fd = (4 * cfd(j, 5e-6) - cfd(j, 1e-5)) / 3
+        assert abs(fd - g[j]) <= 1e-5 * max(abs(fd), 1e-3), (j, fd, g[j])
+
+
+def test_chi2_gradient_unbiased_at_the_target():
+    # with D = V (the target is the model itself) and p~ uniform, the expected
+    # chi^2 gradient is -int D^2 grad V / V^2 = -grad int V = 0: the
+    # quadrature-weighted mean of the per-record raw gradients vanishes
+    from tests.test_oracle_vmf import sphere_quadrature, random_raw
+    rng = np.random.default_rng(21)
+    raw1 = random_raw(rng, 8, 1, kscale=0.7)
+    w, qw = sphere_quadrature(300, 600)
+    m = w.shape[1]
+    raw = np.repeat(raw1, m, axis=1)
+    act = vmf.activate(raw, 8)
+    D = vmf.mixture_pdf(w, act)
+    pdf = np.full(m, 1 / (4 * np.pi))
+    s, _, _ = vmf.record_scale(D, pdf, 1.0)
+    draw, _ = vmf.grad_head(raw, w, s * D / D, 8)   # s * D^/V with V = D
+    mean = (draw * qw[None, :]).sum(axis=1) / (4 * np.pi)
+    assert np.abs(mean).max() < 1e-9, np.abs(mean).max()
+    # the KL head differs from it by the factor D^/V (here 1): sanity that the factor is applied
+    draw_kl, _ = vmf.grad_head(raw, w, s, 8)
+    assert np.allclose(draw, draw_kl)
