@@ -105,6 +105,8 @@ typedef struct {
   float ema_decay;           /* 0.99 (C-A15) */
   float kappa_min, kappa_max;/* clamp of kappa = exp(kappa') (C-A8): 1e-5, 1e5 */
   uint64_t init_seed;        /* parameter initialisation seed (C-A21) */
+  int32_t divergence;        /* training objective: 0 = KL (Eq. 8/9), 1 = Pearson chi^2
+                                (f-4; "other divergence metrics", C-A31) */
 } npm_config;
 
 /* One SoA queue of shading points. px/py/pz: world-space x.
@@ -309,6 +311,10 @@ npm_status npm_profile_read(npm_model* model, int kind, const char** name, int64
  * arguments, NPM_ERR_CUDA (npm_last_error unset) for CUDA failures. */
 npm_status npm_probe_grid_access(int cuda_device, int64_t table_entries, int64_t n_samples, int levels,
                                  int kind, int reps, double* ms_per_rep);
+
+/* sizeof(npm_config), sizeof(npm_query), sizeof(npm_step_stats) as compiled
+ * into the library (bindings check their struct mirrors against these). */
+void npm_abi_sizes(int32_t* config, int32_t* query, int32_t* stats);
 
 const char* npm_last_error(void);
 int npm_version(void);

@@ -262,6 +262,12 @@ extern "C" {
 int npm_version(void) { return NPM_VERSION; }
 const char* npm_last_error(void) { return g_err.c_str(); }
 
+void npm_abi_sizes(int32_t* config, int32_t* query, int32_t* stats) {
+  if (config) *config = (int32_t)sizeof(npm_config);
+  if (query) *query = (int32_t)sizeof(npm_query);
+  if (stats) *stats = (int32_t)sizeof(npm_step_stats);
+}
+
 void npm_default_config(npm_config* c) {
   memset(c, 0, sizeof(*c));
   c->mode = NPM_RADIANCE;
@@ -292,6 +298,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   if (c.base_res < 2 || c.max_res < c.base_res || (c.n_levels > 1 && c.max_res <= c.base_res))
     return fail(NPM_ERR_INVALID, "need 2 <= D_1 < D_L");
   if (c.log2_hashmap < 0 || c.log2_hashmap > 30) return fail(NPM_ERR_INVALID, "log2_hashmap out of range");
+  if (c.divergence != 0 && c.divergence != 1) return fail(NPM_ERR_INVALID, "divergence must be 0 (KL) or 1 (chi^2)");
   for (int a = 0; a < 3; ++a)
     if (!(c.aabb_hi[a] > c.aabb_lo[a]) || !std::isfinite(c.aabb_lo[a]) || !std::isfinite(c.aabb_hi[a]))
       return fail(NPM_ERR_INVALID, "degenerate AABB");
@@ -807,6 +814,9 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.counters = m->dcount;
   if (const char* e = getenv("NPM_DEBUG")) a.debug = atoi(e);   // measurement only
   if (const char* e = getenv("NPM_TRAIN128")) a.legacy = e[0] == '1';
+  a.divergence = m->cfg.divergence;
+  if (a.divergence != 0 && (a.legacy || !m->use_tc))
+    return fail(NPM_ERR_INVALID, "the chi^2 divergence is implemented in the default training kernel only");
   // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
   const NetShape& sh = m->shape;
   if (m->use_tc) {

@@ -54,6 +54,7 @@ struct TrainArgs {
   const float *wx, *wy, *wz;
   const float* target;      // [C][target_stride] (channel c at target + c * target_stride)
   int64_t target_stride;    // = n unless the batch is a slice of a longer one (micro-steps)
+  int divergence;           // 0 KL (Eq. 9), 1 Pearson chi^2 (f-4): record scale times D^ / V
   int channels;
   const float* spdf;        // p~
   double inv_n_global;

@@ -1348,6 +1348,9 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         const float invS = 1.0f / S;
         const float Vb = fmaxf(P * invS, kVFloor);
         const float invV = 1.0f / Vb;
+        // f-4 (C-A31): chi^2 scales Eq. 9's record weight by D^ / V
+        const float chi = a.divergence ? (use ? t * invV : 0.0f) : 1.0f;   // t may be NaN on dropped records
+        const float sd = s * chi;
 #pragma unroll
         for (int jj = 0; jj < KJ; ++jj) {
           float dl[2], dk[2], dt[2], dp[2];
@@ -1356,15 +1359,15 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
             const int m = 2 * jj + w;
             const float lam = e[m] * invS;
             const float gam = lam * vv[m] * invV;
-            dl[w] = s * (gam - lam);
+            dl[w] = sd * (gam - lam);
             const float dx = mx[m] - wx, dy = my[m] - wy, dz = mz[m] - wz;
             const float d2 = dx * dx + dy * dy + dz * dz;
             // 2 kappa e^{-2 kappa} / (1 - e^{-2 kappa}) with em = 1 - e^{-2 kappa}
-            const float dkk = s * gam * (1.0f - kap[m] * 0.5f * d2 - __fdividef(2.0f * kap[m] * (1.0f - emk[m]), emk[m]));
+            const float dkk = sd * gam * (1.0f - kap[m] * 0.5f * d2 - __fdividef(2.0f * kap[m] * (1.0f - emk[m]), emk[m]));
             dk[w] = (kp[m] < a.log_kmin || kp[m] > a.log_kmax) ? 0.0f : dkk;
             const float wdth = kPi * (cth[m] * cph[m] * wx + cth[m] * sph[m] * wy - sth[m] * wz);
             const float wdph = kTwoPi * (-sth[m] * sph[m] * wx + sth[m] * cph[m] * wy);
-            const float sgk = s * gam * kap[m];
+            const float sgk = sd * gam * kap[m];
             dt[w] = sgk * wdth * th[m] * (1.0f - th[m]);
             dp[w] = sgk * wdph * ph[m] * (1.0f - ph[m]);
           }
@@ -1376,7 +1379,10 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         }
         if (c == 0) {
           c_drop += drop; c_zero += zero;
-          if (use) { loss += (double)s * (double)logf(Vb); c_used += 1; }
+          if (use) {
+            loss += a.divergence ? -(double)sd : (double)s * (double)logf(Vb);   // chi^2: (D^/p~)(D^/V)/N
+            c_used += 1;
+          }
         }
       }
     }

@@ -40,7 +40,7 @@ class npm_config(ctypes.Structure):
                 ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
                 ("adam_eps", ctypes.c_float), ("ema_decay", ctypes.c_float),
                 ("kappa_min", ctypes.c_float), ("kappa_max", ctypes.c_float),
-                ("init_seed", ctypes.c_uint64)]
+                ("init_seed", ctypes.c_uint64), ("divergence", ctypes.c_int32)]
 
 
 _FP = ctypes.POINTER(ctypes.c_float)
@@ -102,10 +102,11 @@ def _load():
         "npm_profile_read": (I32, [M, I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(I64),
                                    ctypes.POINTER(ctypes.c_double)]),
         "npm_probe_grid_access": (I32, [I32, I64, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_double)]),
+        "npm_abi_sizes": (None, [ctypes.POINTER(I32)] * 3),
         "npm_last_error": (ctypes.c_char_p, []),
         "npm_version": (I32, []),
     }
-    optional = {"npm_probe_grid_access"}   # measurement only; absent in older A/B builds (NPM_LIB)
+    optional = {"npm_probe_grid_access", "npm_abi_sizes"}   # absent in older A/B builds (NPM_LIB)
     for name, (res, args) in sig.items():
         if name in optional and not hasattr(lib, name):
             continue
@@ -115,6 +116,17 @@ def _load():
 
 
 _lib = _load()
+
+
+def npm_abi_sizes():
+    c, q, s = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.npm_abi_sizes(ctypes.byref(c), ctypes.byref(q), ctypes.byref(s))
+    return c.value, q.value, s.value
+
+
+if hasattr(_lib, "npm_abi_sizes") and npm_abi_sizes() != (ctypes.sizeof(npm_config), ctypes.sizeof(npm_query),
+                                                           ctypes.sizeof(npm_step_stats)):
+    raise ImportError("libnpm.so struct layout does not match this binding (rebuild the library)")
 
 # ---------------------------------------------------------------------------
 # raw C-name wrappers
