@@ -80,6 +80,14 @@ struct npm_model {
   bool use_bin = true; // spatial binning of batches >= kBinMin samples (NPM_BIN=0 disables)
   bool bin_train = false;  // also bin training batches (NPM_BIN_TRAIN=1)
   DevBuf bin_keys, bin_perm, bin_hist;
+  // host-batch pipelining (HostPipe): a copy stream, staging buffers, events
+  cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
+  DevBuf pipe_in[2][16], pipe_out[8];   // input staging double-buffered across calls
+  int pipe_set = 0;
+  cudaEvent_t pipe_in_free[2] = {nullptr, nullptr};   // last kernel that read pipe_in[set]
+  std::vector<cudaEvent_t> sync_events;
+  bool pipeline = true;    // NPM_PIPELINE=0 disables
+  int pipe_chunks = 4;     // NPM_PIPE_CHUNKS
 };
 
 namespace {
@@ -168,6 +176,120 @@ void stage_query(Stager& s, const npm_model* m, const npm_query* q, npm_query& d
     d.wox = d.woy = d.woz = d.nx = d.ny = d.nz = d.rough = nullptr;
   }
 }
+
+// ---------------------------------------------------------------------------
+// HostPipe: a call whose arrays are ALL host pointers (and n >= 2 kPipeMin) is
+// processed in kPipeChunks chunks so that the host->device copy of chunk j+1
+// and the device->host copy of chunk j-1 (on the model's copy stream) overlap
+// the kernels of chunk j (on the caller's stream).  Every array is [comps][n]
+// on the host; chunk j of it is staged compactly as [comps][C_j] (one 2-D
+// copy), so the kernels see an ordinary batch of C_j samples.  Ordering: the
+// copy streams first wait for the caller's stream (earlier work may still
+// read the staging buffers); the caller's stream finally waits for the last
+// output copy.
+constexpr int64_t kPipeMin = 65536;
+
+struct PipeArr {
+  const float* host_in;   // inputs
+  float* host_out;        // outputs
+  int comps;
+};
+
+struct HostPipe {
+  npm_model* m;
+  cudaStream_t st;
+  int64_t n, C;
+  int nch;
+  std::vector<PipeArr> ins, outs;
+  cudaError_t err = cudaSuccess;
+  bool pageable = false;
+  int set = 0;
+
+  static bool usable(const npm_model* m, int64_t n, std::initializer_list<const void*> ptrs) {
+    if (!m->pipeline || n < 2 * kPipeMin) return false;
+    for (const void* p : ptrs)
+      if (p && Stager::kind(p) == 2) return false;   // a device array: the plain path
+    return true;
+  }
+  cudaEvent_t ev(int i) {
+    while ((int)m->sync_events.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      m->sync_events.push_back(e);
+    }
+    return m->sync_events[i];
+  }
+  // chunk j's device pointer of input / output array k
+  const float* din(int k, int j) const {
+    return static_cast<const float*>(m->pipe_in[set][k].p) + (size_t)j * C * ins[k].comps;
+  }
+  float* dout(int k, int j) const { return static_cast<float*>(m->pipe_out[k].p) + (size_t)j * C * outs[k].comps; }
+  int64_t cn(int j) const { return j == nch - 1 ? n - (int64_t)j * C : C; }
+
+  // Runs launch(j, cn) for every chunk; launch enqueues chunk j's kernels on st.
+  template <class F>
+  npm_status run(F&& launch) {
+    const int chunks = m->pipe_chunks;
+    C = (n + chunks - 1) / chunks;
+    if (C < kPipeMin) C = kPipeMin;
+    nch = (int)((n + C - 1) / C);
+    if (!m->copy_stream && cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return NPM_ERR_CUDA;
+    if (!m->d2h_stream && cudaStreamCreateWithFlags(&m->d2h_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return NPM_ERR_CUDA;
+    // input staging alternates between two buffer sets, so this call's input
+    // copies wait only for the kernels of the call before the previous one
+    set = m->pipe_set;
+    m->pipe_set ^= 1;
+    for (size_t k = 0; k < ins.size(); ++k) {
+      if ((err = m->pipe_in[set][k].ensure((size_t)n * ins[k].comps * sizeof(float))) != cudaSuccess)
+        return NPM_ERR_OOM;
+      pageable |= ins[k].host_in && Stager::kind(ins[k].host_in) == 0;
+    }
+    for (size_t k = 0; k < outs.size(); ++k) {
+      if ((err = m->pipe_out[k].ensure((size_t)n * outs[k].comps * sizeof(float))) != cudaSuccess) return NPM_ERR_OOM;
+      pageable |= outs[k].host_out && Stager::kind(outs[k].host_out) == 0;
+    }
+    // H2D on copy_stream, D2H on d2h_stream: a chunk's input copy never queues
+    // behind the previous chunk's output copy
+    cudaStream_t cs = m->copy_stream, ds = m->d2h_stream;
+    if (m->pipe_in_free[set]) cudaStreamWaitEvent(cs, m->pipe_in_free[set], 0);
+    else {
+      cudaEventCreateWithFlags(&m->pipe_in_free[set], cudaEventDisableTiming);
+      cudaEventRecord(ev(0), st);
+      cudaStreamWaitEvent(cs, ev(0), 0);
+    }
+    for (int j = 0; j < nch; ++j) {
+      const int64_t c = cn(j);
+      for (size_t k = 0; k < ins.size(); ++k)
+        if (ins[k].host_in)
+          err = cudaMemcpy2DAsync(const_cast<float*>(din((int)k, j)), (size_t)c * 4, ins[k].host_in + (size_t)j * C,
+                                  (size_t)n * 4, (size_t)c * 4, ins[k].comps, cudaMemcpyHostToDevice, cs);
+      cudaEventRecord(ev(1 + 2 * j), cs);
+    }
+    for (int j = 0; j < nch; ++j) {
+      const int64_t c = cn(j);
+      cudaStreamWaitEvent(st, ev(1 + 2 * j), 0);
+      npm_status r = launch(j, c);
+      if (r != NPM_OK) return r;
+      if (outs.empty()) continue;
+      cudaEventRecord(ev(2 + 2 * j), st);
+      cudaStreamWaitEvent(ds, ev(2 + 2 * j), 0);
+      for (size_t k = 0; k < outs.size(); ++k)
+        if (outs[k].host_out)
+          err = cudaMemcpy2DAsync(outs[k].host_out + (size_t)j * C, (size_t)n * 4, dout((int)k, j), (size_t)c * 4,
+                                  (size_t)c * 4, outs[k].comps, cudaMemcpyDeviceToHost, ds);
+    }
+    cudaEventRecord(m->pipe_in_free[set], st);   // after the last kernel reading pipe_in[set]
+    if (!outs.empty()) {
+      cudaEventRecord(ev(1 + 2 * nch), ds);
+      cudaStreamWaitEvent(st, ev(1 + 2 * nch), 0);
+    }
+    if (err != cudaSuccess) return NPM_ERR_CUDA;
+    if (pageable && cudaStreamSynchronize(ds) != cudaSuccess) return NPM_ERR_CUDA;
+    return NPM_OK;
+  }
+};
 
 void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryArgs& a) {
   memset(&a, 0, sizeof(a));
@@ -321,6 +443,8 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   m->shape = s;
   if (const char* e = getenv("NPM_CUDACORE")) m->use_tc = !(e[0] == '1');
   if (const char* e = getenv("NPM_BIN")) m->use_bin = !(e[0] == '0');
+  if (const char* e = getenv("NPM_PIPELINE")) m->pipeline = !(e[0] == '0');
+  if (const char* e = getenv("NPM_PIPE_CHUNKS")) m->pipe_chunks = atoi(e) > 0 ? atoi(e) : 4;
   if (cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     delete m;
     return fail(NPM_ERR_CUDA, "no CUDA device");
@@ -410,6 +534,12 @@ npm_status npm_destroy(npm_model* m) {
   m->bin_perm.release();
   m->bin_hist.release();
   for (auto& s : m->stage) s.release();
+  for (auto& set : m->pipe_in) for (auto& b : set) b.release();
+  for (auto e : m->pipe_in_free) if (e) cudaEventDestroy(e);
+  for (auto& b : m->pipe_out) b.release();
+  for (auto e : m->sync_events) cudaEventDestroy(e);
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  if (m->d2h_stream) cudaStreamDestroy(m->d2h_stream);
   for (auto& r : m->pending) { m->pool.push_back(r.a); m->pool.push_back(r.b); }
   for (auto e : m->pool) cudaEventDestroy(e);
   delete m;
@@ -629,6 +759,47 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   DeviceGuard g(m->device);
   std::lock_guard<std::mutex> lk(m->stage_mu);
   cudaStream_t st = (cudaStream_t)stream;
+  const bool prod = m->cfg.mode == NPM_PRODUCT;
+  if (HostPipe::usable(m, q->n, {q->px, q->py, q->pz, prod ? q->wox : nullptr, prod ? q->nx : nullptr,
+                                 prod ? q->rough : nullptr, u, qx, wix, pdf, pdf_q})) {
+    HostPipe hp{m, st, q->n};
+    for (const float* p : {q->px, q->py, q->pz}) hp.ins.push_back({p, nullptr, 1});
+    if (prod)
+      for (const float* p : {q->wox, q->woy, q->woz, q->nx, q->ny, q->nz, q->rough}) hp.ins.push_back({p, nullptr, 1});
+    const int ku = u ? (int)hp.ins.size() : -1;
+    if (u) hp.ins.push_back({u, nullptr, 3});
+    const int kq = fused ? (int)hp.ins.size() : -1;
+    if (fused) for (const float* p : {qx, qy, qz}) hp.ins.push_back({p, nullptr, 1});
+    for (float* p : {wix, wiy, wiz, pdf}) hp.outs.push_back({nullptr, p, 1});
+    if (fused) hp.outs.push_back({nullptr, pdf_q, 1});
+    const npm_status r = hp.run([&](int j, int64_t c) -> npm_status {
+      npm_query d{};
+      d.n = c;
+      d.px = hp.din(0, j); d.py = hp.din(1, j); d.pz = hp.din(2, j);
+      if (prod) {
+        d.wox = hp.din(3, j); d.woy = hp.din(4, j); d.woz = hp.din(5, j);
+        d.nx = hp.din(6, j); d.ny = hp.din(7, j); d.nz = hp.din(8, j); d.rough = hp.din(9, j);
+      }
+      QueryArgs a;
+      fill_query_args(m, d, use_ema, a);
+      a.do_sample = 1;
+      a.u = ku >= 0 ? hp.din(ku, j) : nullptr;
+      a.seed = seed;
+      a.offset = offset + (uint64_t)j * (uint64_t)hp.C;   // Philox counter = global sample index
+      if (fused) {
+        a.wx = hp.din(kq, j); a.wy = hp.din(kq + 1, j); a.wz = hp.din(kq + 2, j);
+        a.pdf = hp.dout(4, j);
+      }
+      a.sx = hp.dout(0, j); a.sy = hp.dout(1, j); a.sz = hp.dout(2, j); a.spdf = hp.dout(3, j);
+      npm_status rr = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+      if (rr != NPM_OK) return rr;
+      return check_launch(m, timed(m, kKQuery, st, [&] {
+        return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
+      }));
+    });
+    if (r != NPM_OK) return fail(r, hp.err != cudaSuccess ? cudaGetErrorString(hp.err) : "pipelined sample");
+    return NPM_OK;
+  }
   Stager s{m, st};
   npm_query d;
   stage_query(s, m, q, d);
@@ -789,7 +960,8 @@ static npm_status read_stats(npm_model* m, cudaStream_t st, npm_step_stats* out,
 
 static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
                              const float* wiz, const float* target, int channels, const float* spdf,
-                             int64_t n_global, cudaStream_t st, Stager& s, int64_t target_stride = -1) {
+                             int64_t n_global, cudaStream_t st, Stager& s, int64_t target_stride = -1,
+                             bool reset_stats = true) {
   const size_t n = (size_t)q->n;
   npm_query d;
   stage_query(s, m, q, d);
@@ -820,8 +992,10 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
   const NetShape& sh = m->shape;
   if (m->use_tc) {
-    CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
-    CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+    if (reset_stats) {
+      CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
+      CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+    }
     // Training batches are not binned by default: measured on B200 (c2) the
     // coherent gathers gain ~50 us but the scatter-adds then collide on the
     // same L2 lines (+54 us) and the binning pass costs ~85 us (NPM_BIN_TRAIN=1).
@@ -883,6 +1057,39 @@ static bool train_args_ok(const npm_model* m, const npm_query* q, const float* w
   return true;
 }
 
+// accumulate() over host arrays through HostPipe (all-host batches); returns
+// NPM_ERR_STATE when the batch does not qualify (caller takes the plain path).
+static npm_status accumulate_pipelined(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
+                                       const float* wiz, const float* target, int channels, const float* spdf,
+                                       int64_t n_global, cudaStream_t st) {
+  const bool prod = m->cfg.mode == NPM_PRODUCT;
+  if (!m->use_tc || !HostPipe::usable(m, q->n, {q->px, q->py, q->pz, prod ? q->wox : nullptr, prod ? q->nx : nullptr,
+                                                prod ? q->rough : nullptr, wix, wiy, wiz, target, spdf}))
+    return NPM_ERR_STATE;
+  HostPipe hp{m, st, q->n};
+  for (const float* p : {q->px, q->py, q->pz}) hp.ins.push_back({p, nullptr, 1});
+  if (prod)
+    for (const float* p : {q->wox, q->woy, q->woz, q->nx, q->ny, q->nz, q->rough}) hp.ins.push_back({p, nullptr, 1});
+  const int kw = (int)hp.ins.size();
+  for (const float* p : {wix, wiy, wiz}) hp.ins.push_back({p, nullptr, 1});
+  hp.ins.push_back({target, nullptr, channels});
+  hp.ins.push_back({spdf, nullptr, 1});
+  const npm_status r = hp.run([&](int j, int64_t c) -> npm_status {
+    npm_query d{};
+    d.n = c;
+    d.px = hp.din(0, j); d.py = hp.din(1, j); d.pz = hp.din(2, j);
+    if (prod) {
+      d.wox = hp.din(3, j); d.woy = hp.din(4, j); d.woz = hp.din(5, j);
+      d.nx = hp.din(6, j); d.ny = hp.din(7, j); d.nz = hp.din(8, j); d.rough = hp.din(9, j);
+    }
+    Stager s2{m, st};   // device chunk pointers: pass-through
+    return accumulate(m, &d, hp.din(kw, j), hp.din(kw + 1, j), hp.din(kw + 2, j), hp.din(kw + 3, j), channels,
+                      hp.din(kw + 4, j), n_global, st, s2, -1, j == 0);
+  });
+  if (r != NPM_OK) return fail(r, hp.err != cudaSuccess ? cudaGetErrorString(hp.err) : "pipelined accumulate");
+  return NPM_OK;
+}
+
 npm_status npm_accumulate_grads(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
                                 const float* wiz, const float* target, int channels, const float* spdf,
                                 int64_t n_global, npm_step_stats* stats, void* stream) {
@@ -893,8 +1100,11 @@ npm_status npm_accumulate_grads(npm_model* m, const npm_query* q, const float* w
   DeviceGuard g(m->device);
   std::lock_guard<std::mutex> lk(m->stage_mu);
   cudaStream_t st = (cudaStream_t)stream;
-  Stager s{m, st};
-  npm_status r = accumulate(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st, s);
+  npm_status r = accumulate_pipelined(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st);
+  if (r == NPM_ERR_STATE) {
+    Stager s{m, st};
+    r = accumulate(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st, s);
+  }
   if (r != NPM_OK) return r;
   if (stats) return read_stats(m, st, stats, true, false);
   return NPM_OK;
@@ -984,8 +1194,11 @@ npm_status npm_train_step(npm_model* m, const npm_query* q, const float* wix, co
   cudaStream_t st = (cudaStream_t)stream;
   if (q->n > 0) {
     std::lock_guard<std::mutex> lk(m->stage_mu);
-    Stager s{m, st};
-    npm_status r = accumulate(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st, s);
+    npm_status r = accumulate_pipelined(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st);
+    if (r == NPM_ERR_STATE) {
+      Stager s{m, st};
+      r = accumulate(m, q, wix, wiy, wiz, target, channels, spdf, n_global, st, s);
+    }
     if (r != NPM_OK) return r;
   } else {
     CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));

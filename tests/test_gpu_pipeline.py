@@ -1,0 +1,60 @@
+"""Host-batch pipelining (npm_capi.cu HostPipe): when every array of a
+npm_sample / npm_accumulate_grads / npm_train_step call is a host pointer and
+n >= 131,072, the batch is processed in 4 chunks with the host<->device copies
+of neighbouring chunks overlapping the kernels.  The results must equal the
+device-pointer path: sample outputs bit for bit (each query is independent of
+the others), gradients up to fp32 summation order, statistics exactly."""
+import numpy as np
+import pytest
+
+from workloads import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2504_04315_b200 import npm  # noqa: E402
+from tests.helpers import rel_l2  # noqa: E402
+from tests.test_gpu_parity import make_pair  # noqa: E402
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("philox", [True, False])
+def test_pipelined_sample_equals_device_path(pinned, philox):
+    m, _, _ = make_pair("c2", seed=41)
+    n = 300007                                   # ragged last chunk
+    b = synth.query_batch(n, seed=42)
+    u = None if philox else np.random.default_rng(43).uniform(size=(3, n)).astype(np.float32)
+    H = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()) if pinned else \
+        (lambda a: torch.from_numpy(np.ascontiguousarray(a)))
+    hx, hw = H(b["x"]), H(b["wq"])
+    hu = H(u) if u is not None else None
+    hq = npm.make_query(n, hx[0], hx[1], hx[2])
+    hwi, hp, hpq = H(np.zeros((3, n), np.float32)), H(np.zeros(n, np.float32)), H(np.zeros(n, np.float32))
+    npm.npm_sample(m.h, hq, hu, 99, 1234, 1, hwi[0], hwi[1], hwi[2], hp, hw[0], hw[1], hw[2], hpq)
+    torch.cuda.synchronize()
+    dq = m.query(b["x"])
+    wi, pdf, pdf_q = (t.cpu().numpy() for t in m.sample(dq, u=u, seed=99, offset=1234, use_ema=True, wq=b["wq"]))
+    assert np.array_equal(hwi.numpy(), wi) and np.array_equal(hp.numpy(), pdf) and np.array_equal(hpq.numpy(), pdf_q)
+
+
+@pytest.mark.parametrize("rgb", [False, True])
+def test_pipelined_accumulate_equals_device_path(rgb):
+    m1, _, p = make_pair("c2", seed=44)
+    m2, _, _ = make_pair("c2", seed=44)
+    n = 262147
+    tb = synth.training_batch(n, seed=45, rgb=rgb, nan_rate=1e-4)
+    P = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hx, hwi, ht, hp = P(tb["x"]), P(tb["wi"]), P(tb["target"]), P(tb["pdf"])
+    hq = npm.make_query(n, hx[0], hx[1], hx[2])
+    C = ht.shape[0] if ht.dim() == 2 else 1
+    s1 = npm.npm_accumulate_grads(m1.h, hq, hwi[0], hwi[1], hwi[2], ht, C, hp, n, True)
+    s2 = m2.accumulate_grads(m2.query(tb["x"]), tb["wi"], tb["target"], tb["pdf"], n_global=n)
+    for k in ("n_used", "n_zero_target", "n_dropped"):
+        assert s1[k] == s2[k], k
+    assert abs(s1["loss_proxy"] - s2["loss_proxy"]) <= 1e-6 * abs(s2["loss_proxy"])
+    g1 = m1.get(npm.BUF_GRADS).cpu().numpy().astype(np.float64)
+    g2 = m2.get(npm.BUF_GRADS).cpu().numpy().astype(np.float64)
+    assert rel_l2(g1, g2) <= 1e-5
