@@ -265,6 +265,46 @@ int launch_encode(int L, const QueryArgs& a, int sms, cudaStream_t st) {
   }
 }
 
+// thread (e, s): entry e, copies b = s, s + S, ... (all loads in flight),
+// then one v4 reduction into the gradient; copies re-zeroed in the same pass
+constexpr int kFoldSlices = 8;
+__global__ void __launch_bounds__(256) fold_priv_kernel(FoldArgs a) {
+  const int64_t total = a.priv_stride * kFoldSlices;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / kFoldSlices;
+    const int sl = (int)(t % kFoldSlices);
+    float4* __restrict__ base = a.priv + e;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int U = 8;
+    for (int b0 = sl; b0 < a.ctas; b0 += U * kFoldSlices) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u * kFoldSlices;
+        v[u] = b < a.ctas ? base[(int64_t)b * a.priv_stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u * kFoldSlices;
+        if (b < a.ctas) base[(int64_t)b * a.priv_stride] = make_float4(0.f, 0.f, 0.f, 0.f);
+        acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+      }
+    }
+    int l = 0;
+    while (l + 1 < a.nlev && e >= a.lev_priv_off[l + 1]) ++l;
+    float4* g = reinterpret_cast<float4*>(a.grads) + a.lev_grid_off[l] + (e - a.lev_priv_off[l]);
+    atomicAdd(g, acc);
+  }
+}
+
+int launch_fold_priv(const FoldArgs& a, int sms, cudaStream_t st) {
+  if (a.priv_stride == 0) return 0;
+  const int64_t need = (a.priv_stride * kFoldSlices + 255) / 256;
+  const int blocks = (int)(need < (int64_t)sms * 8 ? need : (int64_t)sms * 8);
+  fold_priv_kernel<<<blocks, 256, 0, st>>>(a);
+  return 1;
+}
+
 int launch_unwind(const UnwindArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0 || a.max_depth == 0) return 0;
   const int64_t need = (a.n + 255) / 256;

@@ -69,6 +69,14 @@ struct TrainArgs {
                             // bit2 record per-phase clock64 stamps of CTA 0 into dbg_clock
   long long* dbg_clock;     // [64 tiles][16 stamps] (debug only)
   int legacy;               // 1: one 128-sample tile per CTA (tc_train_kernel) instead of two 64-sample tiles
+  // Privatised coarse levels: levels in priv_mask scatter into the CTA's own
+  // copy (priv + blockIdx.x * priv_stride + priv_off[l] entries) instead of
+  // the shared gradient: every sample touches 8 of their few entries, and all
+  // SMs' reductions on the same L2 lines serialise.  fold_priv adds the copies.
+  float4* priv;
+  uint32_t priv_mask;
+  int64_t priv_stride;
+  int64_t priv_off[16];
   double* stats;            // [0] loss, [1] unused, then int counters as double
   unsigned long long* counters;  // [0] used, [1] zero, [2] dropped
 };
@@ -91,6 +99,18 @@ int launch_train_forward(const NetShape& s, const TrainArgs& a, int num_sms, cud
 int launch_train_backward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_weight_grads(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_adam(const AdamArgs& a, int num_sms, cudaStream_t st);
+
+// Adds the per-CTA private copies of the privatised levels into the gradient
+// (entry e of privatised block: grads[n_mlp + 4 goff(e) + f]) and re-zeroes them.
+struct FoldArgs {
+  float4* priv;
+  int64_t priv_stride;      // entries per CTA copy
+  int ctas;
+  float* grads;             // + n_mlp: grid section
+  int nlev;
+  int64_t lev_priv_off[16], lev_grid_off[16], lev_entries[16];
+};
+int launch_fold_priv(const FoldArgs& a, int num_sms, cudaStream_t st);
 
 // Training-record unwind (f-1, C-A27): one thread per path.
 struct UnwindArgs {

@@ -1441,11 +1441,17 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
           float gq[4];
           if (!odd) { gq[0] = v[4 * j]; gq[1] = v[4 * j + 1]; gq[2] = r0v; gq[3] = r1v; }
           else { gq[0] = r0v; gq[1] = r1v; gq[2] = v[4 * j + 2]; gq[3] = v[4 * j + 3]; }
-          if (evalid && !(a.debug & 1) && (gq[0] != 0.0f || gq[1] != 0.0f || gq[2] != 0.0f || gq[3] != 0.0f)) {
-            const int l = h * (L / 2) + 2 * j + (c >> 1);
+          const int lsc = h * (L / 2) + 2 * j + (c >> 1);
+          // measurement knobs (NPM_DEBUG): bit 3 skips the two coarsest levels' scatter, bit 4 the two finest
+          const bool dbg_skip = ((a.debug & 8) && lsc < 2) || ((a.debug & 16) && lsc >= L - 2);
+          if (evalid && !(a.debug & 1) && !dbg_skip &&
+              (gq[0] != 0.0f || gq[1] != 0.0f || gq[2] != 0.0f || gq[3] != 0.0f)) {
+            const int l = lsc;
             LevelCorners lc;
             level_corners(a.grid, l, ux, uy, uz, lc);
-            float4* tg = gtab + a.grid.off[l];
+            float4* tg = ((a.priv_mask >> l) & 1u)
+                             ? a.priv + (int64_t)blockIdx.x * a.priv_stride + a.priv_off[l]
+                             : gtab + a.grid.off[l];
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) {
               const float w = lc.w[cc];
