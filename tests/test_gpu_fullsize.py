@@ -105,3 +105,33 @@ def test_full_size_train_properties_and_subset_parity(name):
     assert rel_l2(gs, og) <= 2e-3
     assert abs(stq["loss_proxy"] - ost["loss_proxy"]) <= 1e-4 * abs(ost["loss_proxy"])
     m.set(npm.BUF_GRADS, np.zeros(m.n_params, np.float32))
+
+
+def test_maximum_size_query_and_train():
+    """Largest batch the configurations name for one step (c5: 2^25 samples per
+    iteration) on ONE GPU, ragged (+3): 64-bit sample indices, tile counts and
+    Philox counters past 2^25; sampled rows (incl. the last) against the oracle.
+    Training at 2^24 + 5 records: counters partition the batch, gradient finite."""
+    m, ocfg, p = make("c2")
+    n = (1 << 25) + 3
+    b = synth.query_batch(n, seed=51)
+    off = (1 << 32) - 7                      # Philox counters cross 2^32
+    wi, pdf, pdf_q = (t.cpu().numpy() for t in m.sample(gq(m, b), seed=9, offset=off, wq=b["wq"], use_ema=True))
+    sel = np.concatenate([np.random.default_rng(5).choice(n, 1500, replace=False), [0, n - 2, n - 1]])
+    bs = sub(b, sel)
+    _, act = onpm.decode(ocfg, p.astype(np.float64), oq(bs, False))
+    u = ophilox.sample_uniforms(n, 9, off)[:, sel]
+    ow, opdf, _ = ovmf.sample(act, u, ocfg.n_lobes)
+    ok = ~boundary(act, u[0], ocfg.n_lobes)
+    assert np.abs(wi[:, sel][:, ok] - ow[:, ok]).max() <= 1e-4
+    assert (np.abs(pdf[sel][ok] - opdf[ok]) / opdf[ok]).max() <= 1e-3
+    opq = ovmf.mixture_pdf(bs["wq"].astype(np.float64), act)
+    assert (np.abs(pdf_q[sel] - opq) / opq).max() <= 1e-3
+    del b, wi, pdf, pdf_q
+    nt = (1 << 24) + 5
+    tb = synth.training_batch(nt, seed=52, nan_rate=1e-6)
+    st = m.accumulate_grads(gq(m, tb), tb["wi"], tb["target"], tb["pdf"], n_global=nt)
+    assert st["n_used"] + st["n_zero_target"] + st["n_dropped"] == nt
+    g = m.get(npm.BUF_GRADS).cpu().numpy()
+    assert np.all(np.isfinite(g)) and np.abs(g).max() > 0
+    m.set(npm.BUF_GRADS, np.zeros(m.n_params, np.float32))
