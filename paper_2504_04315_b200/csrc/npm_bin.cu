@@ -9,10 +9,9 @@
 //   adds its non-zero bins to the global histogram (one atomic per
 //   (CTA, bin), not per sample: the samples lie on surfaces, so a few bins
 //   are hot and per-sample atomics serialise on them).
-// Pass 2 (bin_scan): exclusive scan of the bin totals (one CTA).
-// Pass 3 (bin_place): each CTA re-histograms its span, reserves its range in
-//   every non-zero bin with one atomic, then places its samples with smem
-//   atomics.
+// Pass 2 (bin_place): each CTA scans its chunk's histogram row in smem,
+//   re-histograms its span, reserves its range in every non-zero bin with one
+//   atomic, then places its samples with smem atomics.
 // Sort chunks: batches above kSortChunk samples are sorted in independent
 // consecutive chunks (histogram row = chunk, chunk-major scan), so that the
 // scattered per-sample input reads and output writes of a binned launch stay
@@ -65,59 +64,60 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(const float* __rest
     if (h[b]) atomicAdd(hist + b, h[b]);
 }
 
-// Exclusive scan of nb counters (one CTA of kThreads; thread t owns the
-// contiguous run [t per, (t+1) per)).
-__global__ void __launch_bounds__(kThreads) bin_scan_kernel(uint32_t* hist, int nb) {
-  __shared__ uint32_t warp_tot[kThreads / 32];
-  const int t = threadIdx.x;
-  const int per = (nb + kThreads - 1) / kThreads;
-  const int b0 = min(t * per, nb), b1 = min(b0 + per, nb);
-  uint32_t s = 0;
-  for (int j = b0; j < b1; ++j) s += hist[j];
-  uint32_t inc = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if ((t & 31) >= o) inc += y;
-  }
-  if ((t & 31) == 31) warp_tot[t >> 5] = inc;
-  __syncthreads();
-  if (t < 32) {
-    const uint32_t w = t < kThreads / 32 ? warp_tot[t] : 0u;
-    uint32_t wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (t >= o) wi += y;
-    }
-    if (t < kThreads / 32) warp_tot[t] = wi - w;
-  }
-  __syncthreads();
-  uint32_t run = warp_tot[t >> 5] + inc - s;
-  for (int j = b0; j < b1; ++j) {
-    const uint32_t v = hist[j];
-    hist[j] = run;
-    run += v;
-  }
-}
-
+// Pass 2+3 fused: every CTA scans its sort-chunk's histogram row itself (4096
+// counts, block scan in smem) instead of a separate single-CTA scan launch,
+// then reserves its range in each non-zero bin (cursor atomics) and places.
 __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __restrict__ keys, int64_t n,
                                                              int64_t chunk, int64_t sort_chunk,
+                                                             const uint32_t* __restrict__ hist,
                                                              uint32_t* __restrict__ cursor,
                                                              uint32_t* __restrict__ perm) {
+  constexpr int PER = kBins / kThreads;
   __shared__ uint32_t h[kBins];
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
-  __syncthreads();
+  __shared__ uint32_t base[kBins];
+  __shared__ uint32_t warp_tot[kThreads / 32];
+  const int t = threadIdx.x;
   const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(i0 + chunk, n);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(h + keys[i], 1u);
-  __syncthreads();
-  cursor += (i0 / sort_chunk) * kBins;
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
-    const uint32_t c = h[b];
-    h[b] = c ? atomicAdd(cursor + b, c) : 0u;   // this CTA's range in bin b
+  const int64_t row = i0 / sort_chunk;
+  // exclusive scan of this chunk's counts; chunk row r starts at slot r * sort_chunk
+  {
+    uint32_t v[PER], sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { v[j] = hist[row * kBins + t * PER + j]; sum += v[j]; }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if ((t & 31) >= o) inc += y;
+    }
+    if ((t & 31) == 31) warp_tot[t >> 5] = inc;
+    for (int b2 = t; b2 < kBins; b2 += blockDim.x) h[b2] = 0;
+    __syncthreads();
+    if (t < 32) {
+      const uint32_t w = t < kThreads / 32 ? warp_tot[t] : 0u;
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (t >= o) wi += y;
+      }
+      if (t < kThreads / 32) warp_tot[t] = wi - w;
+    }
+    __syncthreads();
+    uint32_t run = (uint32_t)(row * sort_chunk) + warp_tot[t >> 5] + inc - sum;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { base[t * PER + j] = run; run += v[j]; }
   }
   __syncthreads();
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+  for (int64_t i = i0 + t; i < i1; i += blockDim.x) atomicAdd(h + keys[i], 1u);
+  __syncthreads();
+  cursor += row * kBins;
+  for (int b2 = t; b2 < kBins; b2 += blockDim.x) {
+    const uint32_t c = h[b2];
+    h[b2] = c ? base[b2] + atomicAdd(cursor + b2, c) : 0u;   // this CTA's range in bin b2
+  }
+  __syncthreads();
+  for (int64_t i = i0 + t; i < i1; i += blockDim.x) {
     const uint32_t slot = atomicAdd(h + keys[i], 1u);
     perm[slot] = (uint32_t)i;
   }
@@ -125,9 +125,10 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
 
 }  // namespace
 
+// counts [chunks][kBins] followed by cursors [chunks][kBins]
 int bin_hist_entries(int64_t n, int64_t sort_chunk) {
   const int64_t chunks = n <= sort_chunk ? 1 : (n + sort_chunk - 1) / sort_chunk;
-  return (int)(chunks * kBins);
+  return (int)(2 * chunks * kBins);
 }
 
 // sort_chunk: n (one global sort) or kSortChunk (a multiple of 32 * 4096)
@@ -135,8 +136,8 @@ int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int
                uint32_t* keys, uint32_t* hist, uint32_t* perm, int sms, cudaStream_t st) {
   if (n == 0) return 0;
   if (sort_chunk >= n) sort_chunk = n;
-  const int nb = bin_hist_entries(n, sort_chunk);
-  cudaMemsetAsync(hist, 0, (size_t)nb * sizeof(uint32_t), st);
+  const int nb2 = bin_hist_entries(n, sort_chunk), nb = nb2 / 2;
+  cudaMemsetAsync(hist, 0, (size_t)nb2 * sizeof(uint32_t), st);
   int64_t span;
   if (sort_chunk == n) {   // one sort over the whole batch
     const int64_t want = (n + 4095) / 4096;
@@ -147,9 +148,8 @@ int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int
   }
   const int blocks = (int)((n + span - 1) / span);
   bin_count_kernel<<<blocks, kThreads, 0, st>>>(px, py, pz, n, span, sort_chunk, g, keys, hist);
-  bin_scan_kernel<<<1, kThreads, 0, st>>>(hist, nb);
-  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, span, sort_chunk, hist, perm);
-  return 3;
+  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, span, sort_chunk, hist, hist + nb, perm);
+  return 2;
 }
 
 }  // namespace npm
