@@ -89,6 +89,7 @@ struct npm_model {
   DevBuf pipe_in[2][16], pipe_out[8];   // input staging double-buffered across calls
   int pipe_set = 0;
   cudaEvent_t pipe_in_free[2] = {nullptr, nullptr};   // last kernel that read pipe_in[set]
+  cudaEvent_t pipe_out_free = nullptr;                 // last device->host copy out of pipe_out
   std::vector<cudaEvent_t> sync_events;
   bool pipeline = true;    // NPM_PIPELINE=0 disables
   int pipe_chunks = 4;     // NPM_PIPE_CHUNKS
@@ -271,6 +272,9 @@ struct HostPipe {
                                   (size_t)n * 4, (size_t)c * 4, ins[k].comps, cudaMemcpyHostToDevice, cs);
       cudaEventRecord(ev(1 + 2 * j), cs);
     }
+    // the kernels write pipe_out: the previous call's output copies (possibly
+    // issued for another caller stream) must have drained
+    if (!outs.empty() && m->pipe_out_free) cudaStreamWaitEvent(st, m->pipe_out_free, 0);
     for (int j = 0; j < nch; ++j) {
       const int64_t c = cn(j);
       cudaStreamWaitEvent(st, ev(1 + 2 * j), 0);
@@ -286,8 +290,9 @@ struct HostPipe {
     }
     cudaEventRecord(m->pipe_in_free[set], st);   // after the last kernel reading pipe_in[set]
     if (!outs.empty()) {
-      cudaEventRecord(ev(1 + 2 * nch), ds);
-      cudaStreamWaitEvent(st, ev(1 + 2 * nch), 0);
+      if (!m->pipe_out_free) cudaEventCreateWithFlags(&m->pipe_out_free, cudaEventDisableTiming);
+      cudaEventRecord(m->pipe_out_free, ds);
+      cudaStreamWaitEvent(st, m->pipe_out_free, 0);
     }
     if (err != cudaSuccess) return NPM_ERR_CUDA;
     if (pageable && cudaStreamSynchronize(ds) != cudaSuccess) return NPM_ERR_CUDA;
@@ -566,6 +571,7 @@ npm_status npm_destroy(npm_model* m) {
   for (auto& s : m->stage) s.release();
   for (auto& set : m->pipe_in) for (auto& b : set) b.release();
   for (auto e : m->pipe_in_free) if (e) cudaEventDestroy(e);
+  if (m->pipe_out_free) cudaEventDestroy(m->pipe_out_free);
   for (auto& b : m->pipe_out) b.release();
   for (auto e : m->sync_events) cudaEventDestroy(e);
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
