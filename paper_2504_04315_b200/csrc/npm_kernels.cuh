@@ -45,6 +45,7 @@ struct QueryArgs {
   // v(. | n, kappa_c), renormalised, before sampling / pdf; normals in bnx..
   int cos_product;
   float kappa_c, log_c_kc;            // kappa_c and log C(kappa_c) (host-computed)
+  int query_groups;                   // 1: two 256-thread CTAs per SM; 2: one CTA, two groups (NPM_QUERY_GROUPS)
 };
 
 struct TrainArgs {

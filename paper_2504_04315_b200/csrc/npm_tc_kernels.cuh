@@ -99,6 +99,13 @@ struct TC {
   static constexpr uint32_t RED_Q = (BOFF_Q + BBYTES + 127u) & ~127u;   // head reductions [5][4][R] f32
   static constexpr uint32_t MISC_Q = RED_Q + 5u * 4u * R * 4u;
   static constexpr uint32_t SMEM_QUERY = MISC_Q + 64;
+  // ---- two-group query map (one 512-thread CTA per SM, one weight copy):
+  // weights, bias | group g: buffer A, buffer B, head reductions | misc
+  static constexpr uint32_t QRED_BYTES = (3u * 2u + 3u + 2u) * R * 4u;   // TPR = 2 slots
+  static constexpr uint32_t QG0 = (WBYTES + BBYTES + 1023u) & ~1023u;
+  static constexpr uint32_t QGB = (QB + 2u * (W / 8) * CH + QRED_BYTES + 1023u) & ~1023u;
+  static constexpr uint32_t MISC_Q2 = QG0 + 2u * QGB;
+  static constexpr uint32_t SMEM_QUERY2 = MISC_Q2 + 64;
 };
 
 // Convert fp32 weights (global, [out][in]) into split-bf16 chunk-major smem and
@@ -240,27 +247,51 @@ __device__ __forceinline__ void teardown_cta(uint32_t tbase, int tcols) {
 // B_q = sum_{q'<q} S_q' (S_q = sum of the quarter's e^{lambda'-M}) are
 // computed identically by the 4 threads of a row, so exactly one quarter owns
 // u1 and picks its first lobe with u1 < C_i (its last lobe at C = B_{q+1}).
-template <class N, int TPR, int MODE>
-__global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a) {
+template <class N, int TPR, int MODE, int GROUPS>
+__global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) tc_query_kernel(QueryArgs a) {
   // MODE (compile time, so the plain query carries none of the variants' code):
   // 0 guide sampling / pdf; 1 combined BSDF/guide MIS (f-1); 2 cosine product (f-2)
+  // GROUPS = 2: one 512-thread CTA per SM runs two independent tiles (one per
+  // 256-thread group, own buffers / mbarrier / TMEM columns / named barrier)
+  // over ONE copy of the weights; the smem saved goes to L1 for the gathers.
   constexpr bool COMBINED = MODE == 1, COSPROD = MODE == 2;
+  static_assert(GROUPS == 1 || TPR == 2, "two-group query uses 2 threads per row");
   using T = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W;
   constexpr int KQ = K / TPR, WQ = W / TPR, LQ = N::L / TPR, GQ = 4 * LQ;
   static_assert(K % TPR == 0 && N::L % TPR == 0, "parts");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = tc::smem_u32(smem);
-  const int tid = threadIdx.x, warp = tid >> 5, q = warp >> 2;   // q: part of the row
+  const int g = GROUPS == 2 ? (int)(threadIdx.x >> 8) : 0;
+  const int tid = GROUPS == 2 ? (int)(threadIdx.x & 255) : (int)threadIdx.x;   // thread within the group
+  const int warp = tid >> 5, q = warp >> 2;   // q: part of the row
   const int r = ((warp & 3) << 5) | (tid & 31);
   const uint32_t lane_addr = (uint32_t)((warp & 3) << 21);
   uint64_t* mbar;
   uint32_t tbase;
-  setup_cta<N>(smem, T::MISC_Q, T::TCOLS_QUERY, mbar, tbase);
-  stage_weights_tc<N>(a.params, smem, T::WOFF_Q, T::BOFF_Q);
+  constexpr uint32_t MISC = GROUPS == 2 ? T::MISC_Q2 : T::MISC_Q;
+  setup_cta<N>(smem, MISC, GROUPS * T::TCOLS_QUERY, mbar, tbase);
+  mbar += g;
+  tbase += (uint32_t)(g * T::TCOLS_QUERY);
+  constexpr uint32_t WOFF = GROUPS == 2 ? 0u : T::WOFF_Q, BOFF = GROUPS == 2 ? T::WBYTES : T::BOFF_Q;
+  stage_weights_tc<N>(a.params, smem, WOFF, BOFF);
+  if (GROUPS == 2) {   // weights staged by all 512 threads before either group's first MMA
+    tc::fence_proxy_async();
+    __syncthreads();
+  }
+  const uint32_t gbase = GROUPS == 2 ? T::QG0 + (uint32_t)g * T::QGB : 0u;
+  auto qsync = [&]() {
+    if (GROUPS == 2) tc::named_sync(1u + (uint32_t)g, 256u);
+    else __syncthreads();
+  };
+  auto handoff = [&]() {
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    qsync();
+  };
   const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
-  const float* bias = reinterpret_cast<const float*>(smem + T::BOFF_Q);
-  float* red = reinterpret_cast<float*>(smem + T::RED_Q);   // [slot][TPR][R]
+  const float* bias = reinterpret_cast<const float*>(smem + BOFF);
+  float* red = reinterpret_cast<float*>(smem + (GROUPS == 2 ? gbase + T::QB + 2u * (W / 8) * CH : T::RED_Q));
   // slots 0..2: per-part partials; omega (3 floats) at 3 TPR R; slot 4 after it
   auto RS = [&](int slot, int qq) -> float& {
     return red[((slot < 3 ? slot * TPR : 3 * TPR + 3) + qq) * R + r];
@@ -268,7 +299,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
   const int64_t n = a.n;
   const int64_t ntiles = (n + R - 1) / R;
   uint32_t phase = 0;
-  const uint32_t xbuf[2] = {sb + T::QA, sb + T::QB};
+  const uint32_t xbuf[2] = {sb + gbase + T::QA, sb + gbase + T::QB};
   const uint32_t xlo[2] = {(uint32_t)(T::QAF / 8) * CH, (uint32_t)(W / 8) * CH};
   // index + normalised position of this thread's row, prefetched one tile
   // ahead (issued while the current tile's first MMA runs): the
@@ -290,8 +321,9 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
     }
   };
   RowIn nx_row;
-  if (blockIdx.x < ntiles) load_row(blockIdx.x, nx_row);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int64_t tile0 = (int64_t)blockIdx.x * GROUPS + g, tstep = (int64_t)gridDim.x * GROUPS;
+  if (tile0 < ntiles) load_row(tile0, nx_row);
+  for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
     const RowIn row = nx_row;
     const bool valid = row.valid;
     const int64_t i = row.i;
@@ -350,14 +382,14 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
 #pragma unroll
     for (int k = 0; k < NL - 1; ++k) {
       const int src = k & 1, dst = (k + 1) & 1;
-      handoff_to_mma();
+      handoff();
       if (tid == 0) {
         tc::fence_after_sync();
-        const uint32_t w = sb + T::WOFF_Q + T::woff(k);
+        const uint32_t w = sb + WOFF + T::woff(k);
         issue_fwd(tbase, xbuf[src], xbuf[src] + xlo[src], w, w + T::wbytes(k), T::in_p(k), T::out(k));
         tc::mma_commit(mbar);
       }
-      if (k == 0 && tile + gridDim.x < ntiles) load_row(tile + gridDim.x, nx_row);
+      if (k == 0 && tile + tstep < ntiles) load_row(tile + tstep, nx_row);
       wait_mma(mbar, phase);
       float h[WQ];
       tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), h);
@@ -375,10 +407,10 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
     }
     {
       constexpr int k = NL - 1, src = k & 1;
-      handoff_to_mma();
+      handoff();
       if (tid == 0) {
         tc::fence_after_sync();
-        const uint32_t w = sb + T::WOFF_Q + T::woff(k);
+        const uint32_t w = sb + WOFF + T::woff(k);
         issue_fwd(tbase, xbuf[src], xbuf[src] + xlo[src], w, w + T::wbytes(k), T::in_p(k), T::out(k));
         tc::mma_commit(mbar);
       }
@@ -447,7 +479,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       }
     }
     RS(0, q) = mloc;
-    __syncthreads();
+    qsync();
     float M = RS(0, 0);
 #pragma unroll
     for (int qq = 1; qq < TPR; ++qq) M = fmaxf(M, RS(0, qq));
@@ -463,7 +495,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
     }
     RS(1, q) = S;
     RS(2, q) = P;
-    __syncthreads();
+    qsync();
     float B[TPR + 1];
     B[0] = 0.0f;
 #pragma unroll
@@ -510,13 +542,13 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
         lobe_sample(kk, mmx, mmy, mmz, u.y, u.z, wx, wy, wz);
         red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
       }
-      __syncthreads();
+      qsync();
       const float wx = red[(3 * TPR) * R + r], wy = red[(3 * TPR) * R + R + r], wz = red[(3 * TPR) * R + 2 * R + r];
       float P2 = 0.0f;
 #pragma unroll
       for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
       RS(4, q) = P2;
-      __syncthreads();
+      qsync();
       if (q == 0 && valid) {
         float Pt = 0.0f;
 #pragma unroll
@@ -542,7 +574,7 @@ __global__ void __launch_bounds__(TPR * R, 4 / TPR) tc_query_kernel(QueryArgs a)
       }
     }
   }
-  teardown_cta(tbase, T::TCOLS_QUERY);
+  teardown_cta(tbase - (uint32_t)(g * T::TCOLS_QUERY), GROUPS * T::TCOLS_QUERY);
 }
 
 // ---------------------------------------------------------------------------
@@ -1510,10 +1542,19 @@ struct TcLaunch {
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA
     // waits interleave); ~104 KB smem each.
     constexpr int TPR = 2;
-    auto kern = a.combined ? tc_query_kernel<N, TPR, 1> : a.cos_product ? tc_query_kernel<N, TPR, 2>
-                                                                          : tc_query_kernel<N, TPR, 0>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
     const int64_t ntiles = (a.n + R - 1) / R;
+    if (a.query_groups == 2) {   // one CTA per SM, two tile groups over one weight copy
+      auto kern = a.combined ? tc_query_kernel<N, TPR, 1, 2> : a.cos_product ? tc_query_kernel<N, TPR, 2, 2>
+                                                                             : tc_query_kernel<N, TPR, 0, 2>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY2);
+      const int64_t pairs = (ntiles + 1) / 2;
+      const int blocks = (int)(pairs < (int64_t)sms ? pairs : (int64_t)sms);
+      kern<<<blocks, 2 * TPR * R, T::SMEM_QUERY2, st>>>(a);
+      return 1;
+    }
+    auto kern = a.combined ? tc_query_kernel<N, TPR, 1, 1> : a.cos_product ? tc_query_kernel<N, TPR, 2, 1>
+                                                                           : tc_query_kernel<N, TPR, 0, 1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_QUERY);
     const int per_sm = (int)((228u * 1024u) / (T::SMEM_QUERY + 1024u)) >= 2 ? 2 : 1;
     const int64_t cap = (int64_t)sms * per_sm;
     const int blocks = (int)(ntiles < cap ? ntiles : cap);
