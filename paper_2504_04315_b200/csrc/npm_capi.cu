@@ -368,7 +368,8 @@ npm_status maybe_bin(npm_model* m, const float* px, const float* py, const float
     return fail(NPM_ERR_OOM, "binning scratch");
   uint32_t* p = static_cast<uint32_t*>(m->bin_perm.p);
   npm_status r = check_launch(m, timed(m, kKBin, st, [&] {
-    return launch_bin(px, py, pz, n, sort_chunk(m, n), m->grid, static_cast<uint32_t*>(m->bin_keys.p),
+    return launch_bin(px, py, pz, n, sort_chunk(m, n), m->n_grid * 4 > ((int64_t)64 << 20), m->grid,
+                      static_cast<uint32_t*>(m->bin_keys.p),
                       static_cast<uint32_t*>(m->bin_hist.p), p, m->num_sms, st);
   }));
   if (r == NPM_OK) *perm = p;

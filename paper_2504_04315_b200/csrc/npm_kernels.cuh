@@ -139,6 +139,7 @@ namespace npm {
 constexpr int kBinBits = 12;
 constexpr int64_t kSortChunk = 1 << 20;   // sort-chunk for L2-resident tables (npm_capi.cu)
 int bin_hist_entries(int64_t n, int64_t sort_chunk);   // histogram entries launch_bin needs
-int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int64_t sort_chunk, const GridDesc& g,
+int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int64_t sort_chunk, bool refine,
+               const GridDesc& g,
                uint32_t* keys, uint32_t* hist, uint32_t* perm, int num_sms, cudaStream_t st);
 }  // namespace npm
