@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
                                                              const uint32_t* __restrict__ hist,
                                                              uint32_t* __restrict__ cursor,
                                                              uint32_t* __restrict__ bstart,
-                                                             uint32_t* __restrict__ perm) {
+                                                             uint32_t* __restrict__ perm, bool pack) {
   constexpr int PER = kBins / kThreads;
   __shared__ uint32_t h[kBins];
   __shared__ uint32_t base[kBins];
@@ -126,8 +126,10 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
   }
   __syncthreads();
   for (int64_t i = i0 + t; i < i1; i += blockDim.x) {
-    const uint32_t slot = atomicAdd(h + (keys[i] >> 3), 1u);
-    perm[slot] = (uint32_t)i;
+    const uint32_t k = keys[i];
+    const uint32_t slot = atomicAdd(h + (k >> 3), 1u);
+    // pack: the sub-cell rides in the top 3 bits for bin_refine (n < 2^29)
+    perm[slot] = (uint32_t)i | (pack ? (k & 7u) << 29 : 0u);
   }
 }
 
@@ -138,24 +140,28 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
 // 5.10 -> 4.80 ms for +89 us of refinement; with L2-resident tables (c2, c3)
 // the refinement costs more than the queries gain (c2 +26 us vs -11 us).
 constexpr int kRefineMax = 8192;   // larger bins keep the place order
-__global__ void __launch_bounds__(256) bin_refine_kernel(const uint32_t* __restrict__ keys,
-                                                         const uint32_t* __restrict__ hist,
+__global__ void __launch_bounds__(256) bin_refine_kernel(const uint32_t* __restrict__ hist,
                                                          const uint32_t* __restrict__ bstart, int nb,
                                                          uint32_t* __restrict__ perm) {
   __shared__ uint32_t sp[kRefineMax];
   __shared__ uint32_t cnt[8], off[8];
+  constexpr uint32_t kIdx = (1u << 29) - 1u;
   const int b = blockIdx.x;
   if (b >= nb) return;
   const uint32_t c = hist[b];
-  if (c <= 128 || c > (uint32_t)kRefineMax) return;   // a bin within one tile needs no order
+  if (c == 0) return;
   const uint32_t s0 = bstart[b];
   const int t = threadIdx.x;
+  if (c <= 128 || c > (uint32_t)kRefineMax) {   // keep the place order; strip the packed sub-cells
+    for (uint32_t j = t; j < c; j += blockDim.x) perm[s0 + j] &= kIdx;
+    return;
+  }
   if (t < 8) cnt[t] = 0;
   __syncthreads();
   for (uint32_t j = t; j < c; j += blockDim.x) {
-    const uint32_t i = perm[s0 + j];
-    sp[j] = i;
-    atomicAdd(cnt + (__ldg(keys + i) & 7u), 1u);
+    const uint32_t v = perm[s0 + j];
+    sp[j] = v;
+    atomicAdd(cnt + (v >> 29), 1u);
   }
   __syncthreads();
   if (t == 0) {
@@ -164,8 +170,8 @@ __global__ void __launch_bounds__(256) bin_refine_kernel(const uint32_t* __restr
   }
   __syncthreads();
   for (uint32_t j = t; j < c; j += blockDim.x) {
-    const uint32_t i = sp[j];
-    perm[s0 + atomicAdd(off + (__ldg(keys + i) & 7u), 1u)] = i;
+    const uint32_t v = sp[j];
+    perm[s0 + atomicAdd(off + (v >> 29), 1u)] = v & kIdx;
   }
 }
 
@@ -194,9 +200,11 @@ int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int
   }
   const int blocks = (int)((n + span - 1) / span);
   bin_count_kernel<<<blocks, kThreads, 0, st>>>(px, py, pz, n, span, sort_chunk, g, keys, hist);
-  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, span, sort_chunk, hist, hist + nb, hist + 2 * nb, perm);
+  refine = refine && n < (int64_t(1) << 29);
+  bin_place_kernel<<<blocks, kThreads, 0, st>>>(keys, n, span, sort_chunk, hist, hist + nb, hist + 2 * nb, perm,
+                                                refine);
   if (!refine) return 2;
-  bin_refine_kernel<<<nb, 256, 0, st>>>(keys, hist, hist + 2 * nb, nb, perm);
+  bin_refine_kernel<<<nb, 256, 0, st>>>(hist, hist + 2 * nb, nb, perm);
   return 3;
 }
 
