@@ -231,6 +231,27 @@ struct HostPipe {
   }
   float* dout(int k, int j) const { return static_cast<float*>(m->pipe_out[k].p) + (size_t)j * C * outs[k].comps; }
   int64_t cn(int j) const { return j == nch - 1 ? n - (int64_t)j * C : C; }
+  // Three component arrays (x/y/z): when they are the rows of one [3][n]
+  // host array they move as one 2-D copy per chunk (fewer API calls).
+  struct Tri { int k; bool packed; };
+  Tri in3(const float* a, const float* b, const float* c) {
+    Tri t{(int)ins.size(), a && b == a + n && c == a + 2 * n};
+    if (t.packed) ins.push_back({a, nullptr, 3});
+    else for (const float* p : {a, b, c}) ins.push_back({p, nullptr, 1});
+    return t;
+  }
+  Tri out3(float* a, float* b, float* c) {
+    Tri t{(int)outs.size(), a && b == a + n && c == a + 2 * n};
+    if (t.packed) outs.push_back({nullptr, a, 3});
+    else for (float* p : {a, b, c}) outs.push_back({nullptr, p, 1});
+    return t;
+  }
+  const float* din3(Tri t, int comp, int j) const {
+    return t.packed ? din(t.k, j) + (size_t)comp * cn(j) : din(t.k + comp, j);
+  }
+  float* dout3(Tri t, int comp, int j) const {
+    return t.packed ? dout(t.k, j) + (size_t)comp * cn(j) : dout(t.k + comp, j);
+  }
 
   // Runs launch(j, cn) for every chunk; launch enqueues chunk j's kernels on st.
   template <class F>
@@ -808,22 +829,31 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   if (HostPipe::usable(m, q->n, {q->px, q->py, q->pz, prod ? q->wox : nullptr, prod ? q->nx : nullptr,
                                  prod ? q->rough : nullptr, u, qx, wix, pdf, pdf_q})) {
     HostPipe hp{m, st, q->n};
-    for (const float* p : {q->px, q->py, q->pz}) hp.ins.push_back({p, nullptr, 1});
-    if (prod)
-      for (const float* p : {q->wox, q->woy, q->woz, q->nx, q->ny, q->nz, q->rough}) hp.ins.push_back({p, nullptr, 1});
+    const HostPipe::Tri tx = hp.in3(q->px, q->py, q->pz);
+    HostPipe::Tri two{}, tn{};
+    int kr = -1;
+    if (prod) {
+      two = hp.in3(q->wox, q->woy, q->woz);
+      tn = hp.in3(q->nx, q->ny, q->nz);
+      kr = (int)hp.ins.size();
+      hp.ins.push_back({q->rough, nullptr, 1});
+    }
     const int ku = u ? (int)hp.ins.size() : -1;
     if (u) hp.ins.push_back({u, nullptr, 3});
-    const int kq = fused ? (int)hp.ins.size() : -1;
-    if (fused) for (const float* p : {qx, qy, qz}) hp.ins.push_back({p, nullptr, 1});
-    for (float* p : {wix, wiy, wiz, pdf}) hp.outs.push_back({nullptr, p, 1});
+    HostPipe::Tri tq{};
+    if (fused) tq = hp.in3(qx, qy, qz);
+    const HostPipe::Tri tw = hp.out3(wix, wiy, wiz);
+    const int kp = (int)hp.outs.size();
+    hp.outs.push_back({nullptr, pdf, 1});
+    const int kpq = (int)hp.outs.size();
     if (fused) hp.outs.push_back({nullptr, pdf_q, 1});
     const npm_status r = hp.run([&](int j, int64_t c) -> npm_status {
       npm_query d{};
       d.n = c;
-      d.px = hp.din(0, j); d.py = hp.din(1, j); d.pz = hp.din(2, j);
+      d.px = hp.din3(tx, 0, j); d.py = hp.din3(tx, 1, j); d.pz = hp.din3(tx, 2, j);
       if (prod) {
-        d.wox = hp.din(3, j); d.woy = hp.din(4, j); d.woz = hp.din(5, j);
-        d.nx = hp.din(6, j); d.ny = hp.din(7, j); d.nz = hp.din(8, j); d.rough = hp.din(9, j);
+        d.wox = hp.din3(two, 0, j); d.woy = hp.din3(two, 1, j); d.woz = hp.din3(two, 2, j);
+        d.nx = hp.din3(tn, 0, j); d.ny = hp.din3(tn, 1, j); d.nz = hp.din3(tn, 2, j); d.rough = hp.din(kr, j);
       }
       QueryArgs a;
       fill_query_args(m, d, use_ema, a);
@@ -832,10 +862,10 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
       a.seed = seed;
       a.offset = offset + (uint64_t)j * (uint64_t)hp.C;   // Philox counter = global sample index
       if (fused) {
-        a.wx = hp.din(kq, j); a.wy = hp.din(kq + 1, j); a.wz = hp.din(kq + 2, j);
-        a.pdf = hp.dout(4, j);
+        a.wx = hp.din3(tq, 0, j); a.wy = hp.din3(tq, 1, j); a.wz = hp.din3(tq, 2, j);
+        a.pdf = hp.dout(kpq, j);
       }
-      a.sx = hp.dout(0, j); a.sy = hp.dout(1, j); a.sz = hp.dout(2, j); a.spdf = hp.dout(3, j);
+      a.sx = hp.dout3(tw, 0, j); a.sy = hp.dout3(tw, 1, j); a.sz = hp.dout3(tw, 2, j); a.spdf = hp.dout(kp, j);
       npm_status rr = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
       if (rr != NPM_OK) return rr;
       return check_launch(m, timed(m, kKQuery, st, [&] {
@@ -1139,24 +1169,30 @@ static npm_status accumulate_pipelined(npm_model* m, const npm_query* q, const f
                                                 prod ? q->rough : nullptr, wix, wiy, wiz, target, spdf}))
     return NPM_ERR_STATE;
   HostPipe hp{m, st, q->n};
-  for (const float* p : {q->px, q->py, q->pz}) hp.ins.push_back({p, nullptr, 1});
-  if (prod)
-    for (const float* p : {q->wox, q->woy, q->woz, q->nx, q->ny, q->nz, q->rough}) hp.ins.push_back({p, nullptr, 1});
-  const int kw = (int)hp.ins.size();
-  for (const float* p : {wix, wiy, wiz}) hp.ins.push_back({p, nullptr, 1});
+  const HostPipe::Tri tx = hp.in3(q->px, q->py, q->pz);
+  HostPipe::Tri two{}, tn{};
+  int kr = -1;
+  if (prod) {
+    two = hp.in3(q->wox, q->woy, q->woz);
+    tn = hp.in3(q->nx, q->ny, q->nz);
+    kr = (int)hp.ins.size();
+    hp.ins.push_back({q->rough, nullptr, 1});
+  }
+  const HostPipe::Tri tw = hp.in3(wix, wiy, wiz);
+  const int kt = (int)hp.ins.size();
   hp.ins.push_back({target, nullptr, channels});
   hp.ins.push_back({spdf, nullptr, 1});
   const npm_status r = hp.run([&](int j, int64_t c) -> npm_status {
     npm_query d{};
     d.n = c;
-    d.px = hp.din(0, j); d.py = hp.din(1, j); d.pz = hp.din(2, j);
+    d.px = hp.din3(tx, 0, j); d.py = hp.din3(tx, 1, j); d.pz = hp.din3(tx, 2, j);
     if (prod) {
-      d.wox = hp.din(3, j); d.woy = hp.din(4, j); d.woz = hp.din(5, j);
-      d.nx = hp.din(6, j); d.ny = hp.din(7, j); d.nz = hp.din(8, j); d.rough = hp.din(9, j);
+      d.wox = hp.din3(two, 0, j); d.woy = hp.din3(two, 1, j); d.woz = hp.din3(two, 2, j);
+      d.nx = hp.din3(tn, 0, j); d.ny = hp.din3(tn, 1, j); d.nz = hp.din3(tn, 2, j); d.rough = hp.din(kr, j);
     }
     Stager s2{m, st};   // device chunk pointers: pass-through
-    return accumulate(m, &d, hp.din(kw, j), hp.din(kw + 1, j), hp.din(kw + 2, j), hp.din(kw + 3, j), channels,
-                      hp.din(kw + 4, j), n_global, st, s2, -1, j == 0);
+    return accumulate(m, &d, hp.din3(tw, 0, j), hp.din3(tw, 1, j), hp.din3(tw, 2, j), hp.din(kt, j), channels,
+                      hp.din(kt + 1, j), n_global, st, s2, -1, j == 0);
   });
   if (r != NPM_OK) return fail(r, hp.err != cudaSuccess ? cudaGetErrorString(hp.err) : "pipelined accumulate");
   return NPM_OK;
