@@ -286,6 +286,13 @@ npm_status npm_accumulate_grads(npm_model* model, const npm_query* q, const floa
                                 npm_step_stats* stats, void* stream);
 npm_status npm_optimizer_step(npm_model* model, npm_step_stats* stats, void* stream);
 
+/* Asynchronous form of the statistics read: enqueues on `stream` the copy of
+ * the last training step's statistics (loss proxy, gradient norm, record
+ * counters; as npm_train_step's stats) into `out`, which should be pinned
+ * host memory; valid once `stream` has synchronised.  Lets a caller read
+ * every step's loss without a host synchronisation per step. */
+npm_status npm_step_stats_async(npm_model* model, npm_step_stats* out, void* stream);
+
 /* Raw device pointer of a model buffer (for zero-copy collectives by the
  * caller's process group). */
 npm_status npm_buffer_device_ptr(npm_model* model, npm_buffer which, float** ptr, int64_t* count);

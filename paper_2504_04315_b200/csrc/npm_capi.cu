@@ -86,9 +86,12 @@ struct npm_model {
   int64_t priv_stride = 0, priv_off[16] = {};
   // host-batch pipelining (HostPipe): a copy stream, staging buffers, events
   cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
-  DevBuf pipe_in[2][16], pipe_out[8];   // input staging double-buffered across calls
-  int pipe_set = 0;
-  cudaEvent_t pipe_in_free[2] = {nullptr, nullptr};   // last kernel that read pipe_in[set]
+  // input staging: double-buffered per call kind (0 queries, 1 training), so a
+  // call's input copies never wait for the kernels of the previous call of
+  // the same kind (nor of the other kind)
+  DevBuf pipe_in[4][16], pipe_out[8];
+  int pipe_parity[2] = {0, 0};
+  cudaEvent_t pipe_in_free[4] = {nullptr, nullptr, nullptr, nullptr};   // last kernel that read pipe_in[set]
   cudaEvent_t pipe_out_free = nullptr;                 // last device->host copy out of pipe_out
   std::vector<cudaEvent_t> sync_events;
   bool pipeline = true;    // NPM_PIPELINE=0 disables
@@ -205,6 +208,7 @@ struct HostPipe {
   npm_model* m;
   cudaStream_t st;
   int64_t n, C;
+  int kind = 0;   // 0 query-type call, 1 training call (separate staging sets)
   int nch;
   std::vector<PipeArr> ins, outs;
   cudaError_t err = cudaSuccess;
@@ -266,8 +270,8 @@ struct HostPipe {
       return NPM_ERR_CUDA;
     // input staging alternates between two buffer sets, so this call's input
     // copies wait only for the kernels of the call before the previous one
-    set = m->pipe_set;
-    m->pipe_set ^= 1;
+    set = 2 * kind + m->pipe_parity[kind];
+    m->pipe_parity[kind] ^= 1;
     for (size_t k = 0; k < ins.size(); ++k) {
       if ((err = m->pipe_in[set][k].ensure((size_t)n * ins[k].comps * sizeof(float))) != cudaSuccess)
         return NPM_ERR_OOM;
@@ -1169,6 +1173,7 @@ static npm_status accumulate_pipelined(npm_model* m, const npm_query* q, const f
                                                 prod ? q->rough : nullptr, wix, wiy, wiz, target, spdf}))
     return NPM_ERR_STATE;
   HostPipe hp{m, st, q->n};
+  hp.kind = 1;
   const HostPipe::Tri tx = hp.in3(q->px, q->py, q->pz);
   HostPipe::Tri two{}, tn{};
   int kr = -1;
@@ -1276,6 +1281,17 @@ npm_status npm_train_stream(npm_model* m, const npm_query* q, const float* wix, 
       if ((r = read_stats(m, st, per_step + j, true, true)) != NPM_OK) return r;
     }
   }
+  return NPM_OK;
+}
+
+npm_status npm_step_stats_async(npm_model* m, npm_step_stats* out, void* stream) {
+  if (!m || !out) return fail(NPM_ERR_INVALID, "bad argument");
+  static_assert(sizeof(npm_step_stats) == 2 * sizeof(double) + 4 * sizeof(int64_t), "stats layout");
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  // device: dstats = {loss, grad_norm_sq}, dcount = {used, zero, dropped, nonfinite}: the struct's order
+  CUDA_TRY(cudaMemcpyAsync(&out->loss_proxy, m->dstats, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&out->n_used, m->dcount, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   return NPM_OK;
 }
 

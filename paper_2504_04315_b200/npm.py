@@ -94,6 +94,7 @@ def _load():
         "npm_train_stream": (I32, [M, ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64,
                                    ctypes.POINTER(npm_step_stats), V]),
         "npm_optimizer_step": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
+        "npm_step_stats_async": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
         "npm_buffer_device_ptr": (I32, [M, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(I64)]),
         "npm_launch_count": (I64, [M]),
         "npm_profile_kinds": (I32, []),
@@ -106,7 +107,7 @@ def _load():
         "npm_last_error": (ctypes.c_char_p, []),
         "npm_version": (I32, []),
     }
-    optional = {"npm_probe_grid_access", "npm_abi_sizes"}   # absent in older A/B builds (NPM_LIB)
+    optional = {"npm_probe_grid_access", "npm_abi_sizes", "npm_step_stats_async"}   # absent in older A/B builds
     for name, (res, args) in sig.items():
         if name in optional and not hasattr(lib, name):
             continue
@@ -225,6 +226,12 @@ def npm_sample_cosine_product(h, q, nx, ny, nz, kappa_c, u, seed, offset, use_em
                                           int(seed), int(offset), int(use_ema), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(pdf),
                                           _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q), _ptr(lam), _ptr(kappa), _ptr(mu),
                                           _stream(stream)))
+
+
+def npm_step_stats_async(h, out_ptr, stream=None):
+    """out_ptr: address of an npm_step_stats in pinned host memory (e.g. a
+    pinned torch uint8 tensor of ctypes.sizeof(npm_step_stats) bytes)."""
+    _check(_lib.npm_step_stats_async(h, ctypes.cast(out_ptr, ctypes.POINTER(npm_step_stats)), _stream(stream)))
 
 
 def npm_combined_sample(h, q, nx, ny, nz, alpha, u, seed, offset, use_ema, wx, wy, wz, pdf, guide_pdf=None,

@@ -58,3 +58,15 @@ def test_pipelined_accumulate_equals_device_path(rgb):
     g1 = m1.get(npm.BUF_GRADS).cpu().numpy().astype(np.float64)
     g2 = m2.get(npm.BUF_GRADS).cpu().numpy().astype(np.float64)
     assert rel_l2(g1, g2) <= 1e-5
+
+
+def test_step_stats_async_equals_sync_read():
+    import ctypes
+    m, _, _ = make_pair("c2", seed=46)
+    tb = synth.training_batch(5000, seed=47, nan_rate=1e-3)
+    st = m.train_step(m.query(tb["x"]), tb["wi"], tb["target"], tb["pdf"])
+    buf = torch.zeros(ctypes.sizeof(npm.npm_step_stats), dtype=torch.uint8).pin_memory()
+    npm.npm_step_stats_async(m.h, buf.data_ptr())
+    torch.cuda.synchronize()
+    got = npm.npm_step_stats.from_buffer_copy(buf.numpy().tobytes()).as_dict()
+    assert got == st
