@@ -156,6 +156,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD, choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--native-comm", action="store_true",
+                    help="GRADS allreduce through the library's own NCCL communicator (npm_comm_init)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -177,7 +179,7 @@ def main():
     cfg = CONFIGS[name]
     n = cfg["n"] if name != "c3" else cfg["n_global"] // world
     m = npm.Model(local, **cfg["model"])
-    dp = DataParallel(m, world, force_allreduce=distributed)
+    dp = DataParallel(m, world, force_allreduce=distributed, native=args.native_comm and distributed)
     # inputs resident in HBM (device-timed value)
     qb = synth.query_batch(n, seed=100 + rank, product=m.product)
     tb = synth.training_batch(n, seed=200 + rank, product=m.product)

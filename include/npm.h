@@ -286,6 +286,18 @@ npm_status npm_accumulate_grads(npm_model* model, const npm_query* q, const floa
                                 npm_step_stats* stats, void* stream);
 npm_status npm_optimizer_step(npm_model* model, npm_step_stats* stats, void* stream);
 
+/* Multi-GPU (A11): rank 0 calls npm_get_unique_id and shares
+ * the 128-byte id with the other ranks (e.g. over the torch process group);
+ * every rank then attaches a communicator with npm_comm_init (one process per
+ * GPU, `model` on that GPU).  From then on npm_optimizer_step and
+ * npm_train_step / npm_train_stream sum GRADS over the ranks (ncclAllReduce
+ * on the call's stream) before Adam + EMA, so replicas stay identical; each
+ * rank passes n_global = the records of all ranks (1/N scaling, C-A13).
+ * NCCL is resolved at run time (libnccl.so.2); without it these return
+ * NPM_ERR_NCCL.  A second npm_comm_init on a model -> NPM_ERR_STATE. */
+npm_status npm_get_unique_id(uint8_t out[128]);
+npm_status npm_comm_init(npm_model* model, int rank, int world, const uint8_t uid[128]);
+
 /* Asynchronous form of the statistics read: enqueues on `stream` the copy of
  * the last training step's statistics (loss proxy, gradient norm, record
  * counters; as npm_train_step's stats) into `out`, which should be pinned

@@ -5,6 +5,8 @@
 #include "npm_kernels.cuh"
 
 #include <cmath>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: the functions are resolved at run time (dlopen), see Nccl below
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -94,6 +96,8 @@ struct npm_model {
   cudaEvent_t pipe_in_free[4] = {nullptr, nullptr, nullptr, nullptr};   // last kernel that read pipe_in[set]
   cudaEvent_t pipe_out_free = nullptr;                 // last device->host copy out of pipe_out
   std::vector<cudaEvent_t> sync_events;
+  ncclComm_t comm = nullptr;   // npm_comm_init: GRADS allreduced inside npm_optimizer_step
+  int comm_world = 1;
   bool pipeline = true;    // NPM_PIPELINE=0 disables
   int pipe_chunks = 4;     // NPM_PIPE_CHUNKS
   int query_groups = 1;    // NPM_QUERY_GROUPS
@@ -416,11 +420,77 @@ struct DeviceGuard {
 
 }  // namespace
 
+// NCCL, resolved at run time: the process may already hold the library (e.g.
+// through torch); dlopen("libnccl.so.2") then returns that same copy, and a
+// process without NCCL still loads libnpm (the calls return NPM_ERR_NCCL).
+namespace {
+struct Nccl {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return r;
+    r.get_unique_id = reinterpret_cast<decltype(r.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    r.comm_init_rank = reinterpret_cast<decltype(r.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    r.all_reduce = reinterpret_cast<decltype(r.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
+    r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy;
+    return r;
+  }();
+  return n;
+}
+npm_status nccl_fail(ncclResult_t e, const char* what) {
+  const Nccl& n = nccl();
+  return fail(NPM_ERR_NCCL, std::string(what) + ": " + (n.error_string ? n.error_string(e) : "NCCL error"));
+}
+
+void nccl_destroy(ncclComm_t c) {
+  if (nccl().ok && c) nccl().comm_destroy(c);
+}
+}  // namespace
+
 // ===========================================================================
 extern "C" {
 
 int npm_version(void) { return NPM_VERSION; }
 const char* npm_last_error(void) { return g_err.c_str(); }
+
+
+npm_status npm_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(NPM_ERR_INVALID, "null argument");
+  const Nccl& n = nccl();
+  if (!n.ok) return fail(NPM_ERR_NCCL, "libnccl.so.2 not available");
+  ncclUniqueId id;
+  const ncclResult_t e = n.get_unique_id(&id);
+  if (e != ncclSuccess) return nccl_fail(e, "ncclGetUniqueId");
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return NPM_OK;
+}
+
+npm_status npm_comm_init(npm_model* m, int rank, int world, const uint8_t uid[128]) {
+  if (!m || !uid || world < 1 || rank < 0 || rank >= world) return fail(NPM_ERR_INVALID, "bad argument");
+  if (m->comm) return fail(NPM_ERR_STATE, "communicator already attached");
+  const Nccl& n = nccl();
+  if (!n.ok) return fail(NPM_ERR_NCCL, "libnccl.so.2 not available");
+  DeviceGuard g(m->device);
+  ncclUniqueId id;
+  memcpy(&id, uid, 128);
+  const ncclResult_t e = n.comm_init_rank(&m->comm, world, id, rank);
+  if (e != ncclSuccess) { m->comm = nullptr; return nccl_fail(e, "ncclCommInitRank"); }
+  m->comm_world = world;
+  return NPM_OK;
+}
 
 void npm_abi_sizes(int32_t* config, int32_t* query, int32_t* stats) {
   if (config) *config = (int32_t)sizeof(npm_config);
@@ -608,6 +678,7 @@ npm_status npm_destroy(npm_model* m) {
   if (m->pipe_out_free) cudaEventDestroy(m->pipe_out_free);
   for (auto& b : m->pipe_out) b.release();
   for (auto e : m->sync_events) cudaEventDestroy(e);
+  if (m->comm) nccl_destroy(m->comm);
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
   if (m->d2h_stream) cudaStreamDestroy(m->d2h_stream);
   for (auto& r : m->pending) { m->pool.push_back(r.a); m->pool.push_back(r.b); }
@@ -1224,6 +1295,11 @@ npm_status npm_accumulate_grads(npm_model* m, const npm_query* q, const float* w
 }
 
 static npm_status optimizer(npm_model* m, cudaStream_t st) {
+  if (m->comm) {   // A11: the one exchange step -- sum of the ranks' GRADS (each already / N_global)
+    const ncclResult_t e = nccl().all_reduce(m->buf[NPM_BUF_GRADS], m->buf[NPM_BUF_GRADS], (size_t)m->n_total,
+                                             ncclFloat32, ncclSum, m->comm, st);
+    if (e != ncclSuccess) return nccl_fail(e, "ncclAllReduce(GRADS)");
+  }
   m->t += 1;
   const npm_config& c = m->cfg;
   AdamArgs a;

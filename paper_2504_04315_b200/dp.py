@@ -56,11 +56,23 @@ class NpmTrainer:
 
 
 class DataParallel:
-    def __init__(self, model, world=None, group=None, force_allreduce=False):
+    def __init__(self, model, world=None, group=None, force_allreduce=False, native=False):
+        """native=True (CUDA model only): the library's own NCCL communicator
+        (npm_get_unique_id / npm_comm_init, id broadcast over the process
+        group) sums GRADS inside npm_optimizer_step; otherwise GRADS are
+        allreduced here through torch.distributed."""
         self.t = model if hasattr(model, "accumulate") else NpmTrainer(model)
         self.world = world if world is not None else (dist.get_world_size() if dist.is_initialized() else 1)
         self.group = group
         self.reduce = self.world > 1 or force_allreduce   # force: exercise the collective at world size 1
+        if native:
+            from . import npm
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+            uid = [npm.npm_get_unique_id() if rank == 0 else None]
+            if dist.is_initialized():
+                dist.broadcast_object_list(uid, src=0, group=group)
+            npm.npm_comm_init(self.t.m.h, rank, self.world, uid[0])
+            self.reduce = False
 
     def allreduce_grads(self):
         if self.reduce:

@@ -95,6 +95,8 @@ def _load():
                                    ctypes.POINTER(npm_step_stats), V]),
         "npm_optimizer_step": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
         "npm_step_stats_async": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
+        "npm_get_unique_id": (I32, [V]),
+        "npm_comm_init": (I32, [M, I32, I32, V]),
         "npm_buffer_device_ptr": (I32, [M, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(I64)]),
         "npm_launch_count": (I64, [M]),
         "npm_profile_kinds": (I32, []),
@@ -107,7 +109,8 @@ def _load():
         "npm_last_error": (ctypes.c_char_p, []),
         "npm_version": (I32, []),
     }
-    optional = {"npm_probe_grid_access", "npm_abi_sizes", "npm_step_stats_async"}   # absent in older A/B builds
+    optional = {"npm_probe_grid_access", "npm_abi_sizes", "npm_step_stats_async", "npm_get_unique_id",
+                "npm_comm_init"}   # absent in older A/B builds
     for name, (res, args) in sig.items():
         if name in optional and not hasattr(lib, name):
             continue
@@ -226,6 +229,18 @@ def npm_sample_cosine_product(h, q, nx, ny, nz, kappa_c, u, seed, offset, use_em
                                           int(seed), int(offset), int(use_ema), _ptr(wx), _ptr(wy), _ptr(wz), _ptr(pdf),
                                           _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q), _ptr(lam), _ptr(kappa), _ptr(mu),
                                           _stream(stream)))
+
+
+def npm_get_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it, every rank passes it to npm_comm_init)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.npm_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def npm_comm_init(h, rank, world, uid):
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(_lib.npm_comm_init(h, int(rank), int(world), ctypes.cast(buf, ctypes.c_void_p)))
 
 
 def npm_step_stats_async(h, out_ptr, stream=None):

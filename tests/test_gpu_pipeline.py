@@ -70,3 +70,24 @@ def test_step_stats_async_equals_sync_read():
     torch.cuda.synchronize()
     got = npm.npm_step_stats.from_buffer_copy(buf.numpy().tobytes()).as_dict()
     assert got == st
+
+
+def test_native_nccl_communicator_single_rank():
+    # npm_comm_init at world size 1: the allreduce inside npm_optimizer_step is
+    # the identity, so the step equals the one without a communicator
+    m1, _, _ = make_pair("c1", seed=48)
+    m2, _, _ = make_pair("c1", seed=48)
+    npm.npm_comm_init(m2.h, 0, 1, npm.npm_get_unique_id())
+    with pytest.raises(npm.NpmError):
+        npm.npm_comm_init(m2.h, 0, 1, npm.npm_get_unique_id())       # already attached
+    with pytest.raises(npm.NpmError):
+        npm.npm_comm_init(m1.h, 1, 1, npm.npm_get_unique_id())       # rank out of range
+    tb = synth.training_batch(4096, seed=49)
+    s1 = m1.train_step(m1.query(tb["x"]), tb["wi"], tb["target"], tb["pdf"])
+    s2 = m2.train_step(m2.query(tb["x"]), tb["wi"], tb["target"], tb["pdf"])
+    assert s1["n_used"] == s2["n_used"]
+    assert abs(s1["loss_proxy"] - s2["loss_proxy"]) <= 1e-6 * abs(s1["loss_proxy"])
+    p1 = m1.get(npm.BUF_PARAMS).cpu().numpy()
+    p2 = m2.get(npm.BUF_PARAMS).cpu().numpy()
+    assert np.abs(p1 - p2).max() <= 2 * 5e-3   # Adam amplification of fp32 atomic-order noise only
+    assert (p1 == p2).mean() > 0.99
