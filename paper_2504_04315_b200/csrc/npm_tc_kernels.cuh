@@ -284,6 +284,11 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     if (GROUPS == 2) tc::named_sync(1u + (uint32_t)g, 256u);
     else __syncthreads();
   };
+  // The head's exchanges (softmax max / sums, lobe choice, sampled direction)
+  // are between the TPR threads of one row only: warps w and w + 4 -- a
+  // 64-thread named barrier per warp pair instead of the whole CTA.
+  static_assert(TPR == 2, "pair barrier assumes 2 threads per row");
+  auto psync = [&]() { tc::named_sync(3u + 4u * (uint32_t)g + (uint32_t)(warp & 3), 64u); };
   auto handoff = [&]() {
     tc::fence_proxy_async();
     tc::fence_before_sync();
@@ -479,7 +484,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
       }
     }
     RS(0, q) = mloc;
-    qsync();
+    psync();
     float M = RS(0, 0);
 #pragma unroll
     for (int qq = 1; qq < TPR; ++qq) M = fmaxf(M, RS(0, qq));
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     }
     RS(1, q) = S;
     RS(2, q) = P;
-    qsync();
+    psync();
     float B[TPR + 1];
     B[0] = 0.0f;
 #pragma unroll
@@ -542,13 +547,13 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
         lobe_sample(kk, mmx, mmy, mmz, u.y, u.z, wx, wy, wz);
         red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
       }
-      qsync();
+      psync();
       const float wx = red[(3 * TPR) * R + r], wy = red[(3 * TPR) * R + R + r], wz = red[(3 * TPR) * R + 2 * R + r];
       float P2 = 0.0f;
 #pragma unroll
       for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
       RS(4, q) = P2;
-      qsync();
+      psync();
       if (q == 0 && valid) {
         float Pt = 0.0f;
 #pragma unroll
