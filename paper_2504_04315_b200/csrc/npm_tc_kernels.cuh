@@ -1365,7 +1365,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
           __sincosf(kPi * th[m], &sth[m], &cth[m]);
           __sincosf(kTwoPi * ph[m], &sph[m], &cph[m]);
           mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
-          const float nrm = lobe_norm(kap[m], emk[m]);
+          const float nrm = lobe_norm_fast(kap[m], emk[m]);
           vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);
         }
         // the 4 threads of a row are lanes 4i..4i+3: reduce with xor 1, 2
