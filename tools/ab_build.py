@@ -27,7 +27,7 @@ def main(rev, out):
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         list(ex.map(lambda so: subprocess.run(["nvcc"] + flags + ["-c", so[0], "-o", so[1]], check=True),
                     zip(srcs, objs)))
-    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out] + objs + ["-lcudart"],
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out] + objs + ["-lcudart", "-ldl"],
                    check=True)
     print(out)
 
