@@ -309,8 +309,10 @@ def main():
         dist.barrier()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ee0.record()
+    th0 = time.perf_counter()
     for i in range(K):
         e2e_step(i)
+    host_enqueue_ms = (time.perf_counter() - th0) * 1e3 / K   # host time to enqueue one step (diagnostic)
     ee1.record()
     torch.cuda.synchronize()
     te = torch.tensor([ee0.elapsed_time(ee1) / 1e3], dtype=torch.float64, device=dev)
@@ -432,7 +434,8 @@ def main():
                            "n_per_gpu": n, "l2": "flushed between timed steps (512 MB write)",
                            "parallelism": "dp%d" % world},
                 "train_samples_per_s": n * world * K / t_t, "queries_per_s": n * world * K / t_q,
-                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "host_enqueue_ms_per_step": host_enqueue_ms},
                 "gpu_launches": launches, "gpu_launches_per_step": launches / K,
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
                 "clocks": clk.summary(), "cpu_baseline": cpu, "paper_context": paper_ctx, "f1_guided_mis": f1,
