@@ -99,7 +99,7 @@ struct npm_model {
   ncclComm_t comm = nullptr;   // npm_comm_init: GRADS allreduced inside npm_optimizer_step
   int comm_world = 1;
   bool pipeline = true;    // NPM_PIPELINE=0 disables
-  int pipe_chunks = 4;     // NPM_PIPE_CHUNKS
+  int pipe_chunks = 3;     // NPM_PIPE_CHUNKS (c2 e2e: 2 -> 1.31, 3 -> 1.32, 4 -> 1.28, 8 -> 1.13 G/s)
   int query_groups = 1;    // NPM_QUERY_GROUPS
 };
 
@@ -552,7 +552,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   if (const char* e = getenv("NPM_CUDACORE")) m->use_tc = !(e[0] == '1');
   if (const char* e = getenv("NPM_BIN")) m->use_bin = !(e[0] == '0');
   if (const char* e = getenv("NPM_PIPELINE")) m->pipeline = !(e[0] == '0');
-  if (const char* e = getenv("NPM_PIPE_CHUNKS")) m->pipe_chunks = atoi(e) > 0 ? atoi(e) : 4;
+  if (const char* e = getenv("NPM_PIPE_CHUNKS")) m->pipe_chunks = atoi(e) > 0 ? atoi(e) : 3;
   // Query kernel layout: two 256-thread CTAs per SM, or one CTA running two
   // tile groups over a single copy of the weights (frees one weight copy of
   // smem for L1).  Measured on B200: the product shape (53 KB of split-bf16

@@ -1,6 +1,6 @@
 """Host-batch pipelining (npm_capi.cu HostPipe): when every array of a
 npm_sample / npm_accumulate_grads / npm_train_step call is a host pointer and
-n >= 131,072, the batch is processed in 4 chunks with the host<->device copies
+n >= 131,072, the batch is processed in NPM_PIPE_CHUNKS (default 3) chunks with the host<->device copies
 of neighbouring chunks overlapping the kernels.  The results must equal the
 device-pointer path: sample outputs bit for bit (each query is independent of
 the others), gradients up to fp32 summation order, statistics exactly."""
