@@ -42,13 +42,18 @@
  *   - Concurrency: queries (encode/decode/pdf/sample) only read the model and
  *     may run concurrently with each other; a training call must not overlap
  *     queries on the same model (training happens between render waves).
+ *     Batches of >= 65,536 samples are processed in a spatially binned order
+ *     whose permutation lives in per-model scratch: a binning pass on one
+ *     stream waits (cudaStreamWaitEvent) for the kernel that consumed the
+ *     previous permutation, so device-pointer queries on different streams
+ *     stay correct (their binned parts serialise on the GPU).
  *     Calls with HOST pointers stage through the model's scratch: issued on
  *     different streams, the caller must order them (one stream, or events).
  *   - Host batches: when every array of npm_sample / npm_accumulate_grads /
- *     npm_train_step is a host pointer and n >= 131,072, the call runs in 4
- *     chunks whose host<->device copies (two internal copy streams) overlap
- *     the kernels of the neighbouring chunks; results equal the device path
- *     (NPM_PIPELINE=0 disables).
+ *     npm_train_step is a host pointer and n >= 131,072, the call runs in
+ *     NPM_PIPE_CHUNKS chunks (default 3) whose host<->device copies (two
+ *     internal copy streams) overlap the kernels of the neighbouring chunks;
+ *     results equal the device path (NPM_PIPELINE=0 disables).
  *
  * Supported configurations (validated by npm_create; the decoder kernels are
  * compiled per shape): n_features = 4 and

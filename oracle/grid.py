@@ -57,13 +57,15 @@ def inv_extent(lo, hi):
 
 def normalize_position(x, lo, hi):
     """C-O1: u_a = min(max(fl32(fl32(x_a - lo_a) * inv_ext_a), 0), fl32(1-1e-6)).
-    x: [3, n] float32.  Returns u [3, n] float32."""
+    C-A32 (the paper is silent on non-finite positions): min / max are IEEE-754
+    minNum / maxNum, so a NaN coordinate becomes the lower face (max(NaN, 0) =
+    0) and +-inf clamp to the faces.  x: [3, n] float32.  Returns u [3, n] float32."""
     x = np.asarray(x, np.float32)
     lo32 = np.asarray(lo, np.float32).reshape(3, 1)
     inv = inv_extent(lo, hi).reshape(3, 1)
     d = (x - lo32).astype(np.float32)          # fp32 subtract
     u = (d * inv).astype(np.float32)           # fp32 multiply
-    u = np.minimum(np.maximum(u, np.float32(0.0)), U_MAX)
+    u = np.fmin(np.fmax(u, np.float32(0.0)), U_MAX)
     return u.astype(np.float32)
 
 

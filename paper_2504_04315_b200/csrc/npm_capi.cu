@@ -67,7 +67,7 @@ struct npm_model {
   // device statistics: [0] loss, [1] grad norm^2 ; counters [0] used [1] zero [2] dropped [3] nonfinite
   double* dstats = nullptr;
   unsigned long long* dcount = nullptr;
-  DevBuf scratch_train;            // act / delta rows
+  DevBuf dbg_clock;                // NPM_DEBUG=4 phase stamps (measurement only)
   DevBuf stage[24];                // host-pointer staging slots
   std::mutex stage_mu;
   int64_t launches = 0;
@@ -78,10 +78,14 @@ struct npm_model {
   std::vector<cudaEvent_t> pool;
   int64_t prof_launches[16] = {};
   double prof_ms[16] = {};
-  bool use_tc = true;  // fused tcgen05 decoder (NPM_CUDACORE=1 selects the CUDA-core debug path)
   bool use_bin = true; // spatial binning of batches >= kBinMin samples (NPM_BIN=0 disables)
   bool bin_train = false;  // also bin training batches (NPM_BIN_TRAIN=1)
   DevBuf bin_keys, bin_perm, bin_hist;
+  // The binning scratch is one set per model; calls on different streams are
+  // ordered through it: a binning pass waits for bin_free, recorded after the
+  // kernel that consumed the previous permutation (two device-
+  // pointer queries on different streams raced on bin_perm).
+  cudaEvent_t bin_free = nullptr;
   // privatised coarse-level gradients (TrainArgs::priv): one copy per SM
   DevBuf priv;
   uint32_t priv_mask = 0;
@@ -131,8 +135,12 @@ struct Stager {
     if (at.type == cudaMemoryTypeHost) return 1;
     return 0;
   }
+  // Errors are sticky: once a staging allocation or copy failed, every later
+  // in()/out() returns NULL without touching err, so the caller's err check
+  // sees the first failure (and no kernel runs on a NULL or stale input).
   template <class T>
   const T* in(const T* p, size_t count) {
+    if (err != cudaSuccess) return nullptr;
     if (!p || count == 0) return p;
     const int k = kind(p);
     if (k == 2) return p;
@@ -145,6 +153,7 @@ struct Stager {
   }
   template <class T>
   T* out(T* p, size_t count) {
+    if (err != cudaSuccess) return nullptr;
     if (!p || count == 0) return p;
     const int k = kind(p);
     if (k == 2) return p;
@@ -215,9 +224,14 @@ struct HostPipe {
   int kind = 0;   // 0 query-type call, 1 training call (separate staging sets)
   int nch;
   std::vector<PipeArr> ins, outs;
-  cudaError_t err = cudaSuccess;
+  cudaError_t err = cudaSuccess;   // the FIRST failure (keep())
   bool pageable = false;
   int set = 0;
+
+  bool keep(cudaError_t e) {
+    if (e != cudaSuccess && err == cudaSuccess) err = e;
+    return err == cudaSuccess;
+  }
 
   static bool usable(const npm_model* m, int64_t n, std::initializer_list<const void*> ptrs) {
     if (!m->pipeline || n < 2 * kPipeMin) return false;
@@ -288,44 +302,45 @@ struct HostPipe {
     // H2D on copy_stream, D2H on d2h_stream: a chunk's input copy never queues
     // behind the previous chunk's output copy
     cudaStream_t cs = m->copy_stream, ds = m->d2h_stream;
-    if (m->pipe_in_free[set]) cudaStreamWaitEvent(cs, m->pipe_in_free[set], 0);
-    else {
-      cudaEventCreateWithFlags(&m->pipe_in_free[set], cudaEventDisableTiming);
-      cudaEventRecord(ev(0), st);
-      cudaStreamWaitEvent(cs, ev(0), 0);
-    }
-    for (int j = 0; j < nch; ++j) {
+    // every copy / event call is checked (keep()): a failed input copy must
+    // not be followed by kernels reading stale staging data
+    if (m->pipe_in_free[set]) keep(cudaStreamWaitEvent(cs, m->pipe_in_free[set], 0));
+    else if (keep(cudaEventCreateWithFlags(&m->pipe_in_free[set], cudaEventDisableTiming)) &&
+             keep(cudaEventRecord(ev(0), st)))
+      keep(cudaStreamWaitEvent(cs, ev(0), 0));
+    for (int j = 0; j < nch && err == cudaSuccess; ++j) {
       const int64_t c = cn(j);
       for (size_t k = 0; k < ins.size(); ++k)
         if (ins[k].host_in)
-          err = cudaMemcpy2DAsync(const_cast<float*>(din((int)k, j)), (size_t)c * 4, ins[k].host_in + (size_t)j * C,
-                                  (size_t)n * 4, (size_t)c * 4, ins[k].comps, cudaMemcpyHostToDevice, cs);
-      cudaEventRecord(ev(1 + 2 * j), cs);
+          keep(cudaMemcpy2DAsync(const_cast<float*>(din((int)k, j)), (size_t)c * 4, ins[k].host_in + (size_t)j * C,
+                                 (size_t)n * 4, (size_t)c * 4, ins[k].comps, cudaMemcpyHostToDevice, cs));
+      keep(cudaEventRecord(ev(1 + 2 * j), cs));
     }
+    if (err != cudaSuccess) return NPM_ERR_CUDA;
     // the kernels write pipe_out: the previous call's output copies (possibly
     // issued for another caller stream) must have drained
-    if (!outs.empty() && m->pipe_out_free) cudaStreamWaitEvent(st, m->pipe_out_free, 0);
+    if (!outs.empty() && m->pipe_out_free) keep(cudaStreamWaitEvent(st, m->pipe_out_free, 0));
     for (int j = 0; j < nch; ++j) {
       const int64_t c = cn(j);
-      cudaStreamWaitEvent(st, ev(1 + 2 * j), 0);
+      if (!keep(cudaStreamWaitEvent(st, ev(1 + 2 * j), 0))) return NPM_ERR_CUDA;
       npm_status r = launch(j, c);
       if (r != NPM_OK) return r;
       if (outs.empty()) continue;
-      cudaEventRecord(ev(2 + 2 * j), st);
-      cudaStreamWaitEvent(ds, ev(2 + 2 * j), 0);
+      keep(cudaEventRecord(ev(2 + 2 * j), st));
+      keep(cudaStreamWaitEvent(ds, ev(2 + 2 * j), 0));
       for (size_t k = 0; k < outs.size(); ++k)
         if (outs[k].host_out)
-          err = cudaMemcpy2DAsync(outs[k].host_out + (size_t)j * C, (size_t)n * 4, dout((int)k, j), (size_t)c * 4,
-                                  (size_t)c * 4, outs[k].comps, cudaMemcpyDeviceToHost, ds);
+          keep(cudaMemcpy2DAsync(outs[k].host_out + (size_t)j * C, (size_t)n * 4, dout((int)k, j), (size_t)c * 4,
+                                 (size_t)c * 4, outs[k].comps, cudaMemcpyDeviceToHost, ds));
+      if (err != cudaSuccess) return NPM_ERR_CUDA;
     }
-    cudaEventRecord(m->pipe_in_free[set], st);   // after the last kernel reading pipe_in[set]
+    keep(cudaEventRecord(m->pipe_in_free[set], st));   // after the last kernel reading pipe_in[set]
     if (!outs.empty()) {
-      if (!m->pipe_out_free) cudaEventCreateWithFlags(&m->pipe_out_free, cudaEventDisableTiming);
-      cudaEventRecord(m->pipe_out_free, ds);
-      cudaStreamWaitEvent(st, m->pipe_out_free, 0);
+      if (!m->pipe_out_free) keep(cudaEventCreateWithFlags(&m->pipe_out_free, cudaEventDisableTiming));
+      if (keep(cudaEventRecord(m->pipe_out_free, ds))) keep(cudaStreamWaitEvent(st, m->pipe_out_free, 0));
     }
     if (err != cudaSuccess) return NPM_ERR_CUDA;
-    if (pageable && cudaStreamSynchronize(ds) != cudaSuccess) return NPM_ERR_CUDA;
+    if (pageable && !keep(cudaStreamSynchronize(ds))) return NPM_ERR_CUDA;
     return NPM_OK;
   }
 };
@@ -389,7 +404,8 @@ static int64_t sort_chunk(const npm_model* m, int64_t n) {
 npm_status maybe_bin(npm_model* m, const float* px, const float* py, const float* pz, int64_t n, cudaStream_t st,
                      const uint32_t** perm) {
   *perm = nullptr;
-  if (!m->use_tc || !m->use_bin || n < kBinMin) return NPM_OK;
+  if (!m->use_bin || n < kBinMin) return NPM_OK;
+  if (m->bin_free) CUDA_TRY(cudaStreamWaitEvent(st, m->bin_free, 0));
   cudaError_t e;
   if ((e = m->bin_keys.ensure(n * sizeof(uint32_t))) != cudaSuccess ||
       (e = m->bin_perm.ensure(n * sizeof(uint32_t))) != cudaSuccess ||
@@ -403,6 +419,22 @@ npm_status maybe_bin(npm_model* m, const float* px, const float* py, const float
   }));
   if (r == NPM_OK) *perm = p;
   return r;
+}
+
+// After the launch that read a permutation from maybe_bin: later binning
+// passes (on any stream) wait for it.
+npm_status bin_release(npm_model* m, cudaStream_t st, const uint32_t* perm) {
+  if (!perm) return NPM_OK;
+  if (!m->bin_free) CUDA_TRY(cudaEventCreateWithFlags(&m->bin_free, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(m->bin_free, st));
+  return NPM_OK;
+}
+
+// The fused query kernel (+ releasing the binning scratch it read).
+npm_status query_launch(npm_model* m, const QueryArgs& a, cudaStream_t st) {
+  npm_status r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query_tc(m->shape, a, m->num_sms, st); }));
+  if (r != NPM_OK) return r;
+  return bin_release(m, st, a.perm);
 }
 
 struct DeviceGuard {
@@ -549,7 +581,6 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   m->cfg = c;
   m->device = dev;
   m->shape = s;
-  if (const char* e = getenv("NPM_CUDACORE")) m->use_tc = !(e[0] == '1');
   if (const char* e = getenv("NPM_BIN")) m->use_bin = !(e[0] == '0');
   if (const char* e = getenv("NPM_PIPELINE")) m->pipeline = !(e[0] == '0');
   if (const char* e = getenv("NPM_PIPE_CHUNKS")) m->pipe_chunks = atoi(e) > 0 ? atoi(e) : 3;
@@ -667,10 +698,11 @@ npm_status npm_destroy(npm_model* m) {
   for (auto& b : m->buf) if (b) cudaFree(b);
   if (m->dstats) cudaFree(m->dstats);
   if (m->dcount) cudaFree(m->dcount);
-  m->scratch_train.release();
+  m->dbg_clock.release();
   m->bin_keys.release();
   m->bin_perm.release();
   m->bin_hist.release();
+  if (m->bin_free) cudaEventDestroy(m->bin_free);
   m->priv.release();
   for (auto& s : m->stage) s.release();
   for (auto& set : m->pipe_in) for (auto& b : set) b.release();
@@ -854,9 +886,7 @@ npm_status npm_decode(npm_model* m, const npm_query* q, const float* feat, int u
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
   npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
   if (r != NPM_OK) return r;
-  r = check_launch(m, timed(m, kKQuery, st, [&] {
-    return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
-  }));
+  r = query_launch(m, a, st);
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -881,9 +911,7 @@ npm_status npm_pdf(npm_model* m, const npm_query* q, const float* wix, const flo
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
   npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
   if (r != NPM_OK) return r;
-  r = check_launch(m, timed(m, kKQuery, st, [&] {
-    return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
-  }));
+  r = query_launch(m, a, st);
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -943,9 +971,7 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
       a.sx = hp.dout3(tw, 0, j); a.sy = hp.dout3(tw, 1, j); a.sz = hp.dout3(tw, 2, j); a.spdf = hp.dout(kp, j);
       npm_status rr = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
       if (rr != NPM_OK) return rr;
-      return check_launch(m, timed(m, kKQuery, st, [&] {
-        return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
-      }));
+      return query_launch(m, a, st);
     });
     if (r != NPM_OK) return fail(r, hp.err != cudaSuccess ? cudaGetErrorString(hp.err) : "pipelined sample");
     return NPM_OK;
@@ -968,9 +994,7 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
   npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
   if (r != NPM_OK) return r;
-  r = check_launch(m, timed(m, kKQuery, st, [&] {
-    return m->use_tc ? launch_query_tc(m->shape, a, m->num_sms, st) : launch_query(m->shape, a, m->num_sms, st);
-  }));
+  r = query_launch(m, a, st);
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -986,7 +1010,6 @@ npm_status npm_sample_cosine_product(npm_model* m, const npm_query* q, const flo
     return fail(NPM_ERR_INVALID, "bad argument");
   const bool fused = qx && qy && qz && pdf_q;
   if ((qx || qy || qz || pdf_q) && !fused) return fail(NPM_ERR_INVALID, "fused query needs qx, qy, qz, pdf_q");
-  if (!m->use_tc) return fail(NPM_ERR_INVALID, "the cosine product needs the tensor-core query kernel");
   if (q->n == 0) return NPM_OK;
   DeviceGuard g(m->device);
   std::lock_guard<std::mutex> lk(m->stage_mu);
@@ -1021,7 +1044,7 @@ npm_status npm_sample_cosine_product(npm_model* m, const npm_query* q, const flo
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
   npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
   if (r != NPM_OK) return r;
-  r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query_tc(m->shape, a, m->num_sms, st); }));
+  r = query_launch(m, a, st);
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -1034,7 +1057,6 @@ npm_status npm_combined_sample(npm_model* m, const npm_query* q, const float* nx
   if (!m || !query_ok(m, q) || !(alpha >= 0.0f && alpha <= 1.0f) ||
       (q->n > 0 && (!nx || !ny || !nz || !wix || !wiy || !wiz || !pdf)))
     return fail(NPM_ERR_INVALID, "bad argument");
-  if (!m->use_tc) return fail(NPM_ERR_INVALID, "combined sampling needs the tensor-core query kernel");
   if (q->n == 0) return NPM_OK;
   DeviceGuard g(m->device);
   std::lock_guard<std::mutex> lk(m->stage_mu);
@@ -1058,7 +1080,7 @@ npm_status npm_combined_sample(npm_model* m, const npm_query* q, const float* nx
   if (s.err != cudaSuccess) return fail(NPM_ERR_CUDA, cudaGetErrorString(s.err));
   npm_status r = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
   if (r != NPM_OK) return r;
-  r = check_launch(m, timed(m, kKQuery, st, [&] { return launch_query_tc(m->shape, a, m->num_sms, st); }));
+  r = query_launch(m, a, st);
   if (r != NPM_OK) return r;
   CUDA_TRY(s.finish());
   return NPM_OK;
@@ -1153,19 +1175,15 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.stats = m->dstats;
   a.counters = m->dcount;
   if (const char* e = getenv("NPM_DEBUG")) a.debug = atoi(e);   // measurement only
-  if (const char* e = getenv("NPM_TRAIN128")) a.legacy = e[0] == '1';
   a.divergence = m->cfg.divergence;
-  if (m->use_tc && !a.legacy && m->priv_mask) {
+  if (m->priv_mask) {
     a.priv = static_cast<float4*>(m->priv.p);
     a.priv_mask = m->priv_mask;
     a.priv_stride = m->priv_stride;
     for (int l = 0; l < 16; ++l) a.priv_off[l] = m->priv_off[l];
   }
-  if (a.divergence != 0 && (a.legacy || !m->use_tc))
-    return fail(NPM_ERR_INVALID, "the chi^2 divergence is implemented in the default training kernel only");
-  // scratch rows: act[0] n_in, act[1..] width; delta[0..NL-2] width, delta[NL-1] n_out
   const NetShape& sh = m->shape;
-  if (m->use_tc) {
+  {
     if (reset_stats) {
       CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
       CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
@@ -1178,11 +1196,12 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       if (r != NPM_OK) return r;
     }
     if (a.debug & 4) {   // measurement only: per-phase clock stamps of CTA 0
-      static long long* dclk = nullptr;
-      if (!dclk) cudaMalloc(&dclk, 64 * 16 * sizeof(long long));
+      CUDA_TRY(m->dbg_clock.ensure(64 * 16 * sizeof(long long)));
+      long long* dclk = static_cast<long long*>(m->dbg_clock.p);
       cudaMemsetAsync(dclk, 0, 64 * 16 * sizeof(long long), st);
       a.dbg_clock = dclk;
       npm_status r = check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
+      if (r == NPM_OK) r = bin_release(m, st, a.perm);
       long long h[64 * 16];
       cudaMemcpyAsync(h, dclk, sizeof(h), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
@@ -1205,24 +1224,10 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       return fold_priv(m, st);
     }
     npm_status r = check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
+    if (r == NPM_OK) r = bin_release(m, st, a.perm);
     if (r != NPM_OK || !a.priv_mask) return r;
     return fold_priv(m, st);
   }
-  const size_t rows = (size_t)sh.n_in + (size_t)(sh.n_layers - 1) * sh.width  // acts
-                      + (size_t)(sh.n_layers - 1) * sh.width + sh.n_out;       // deltas
-  CUDA_TRY(m->scratch_train.ensure(rows * n * sizeof(float)));
-  float* p = static_cast<float*>(m->scratch_train.p);
-  a.act[0] = p; p += (size_t)sh.n_in * n;
-  for (int k = 1; k < sh.n_layers; ++k) { a.act[k] = p; p += (size_t)sh.width * n; }
-  for (int k = 0; k < sh.n_layers - 1; ++k) { a.delta[k] = p; p += (size_t)sh.width * n; }
-  a.delta[sh.n_layers - 1] = p;
-  CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
-  CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
-  npm_status r;
-  if ((r = check_launch(m, timed(m, kKTrainFwd, st, [&] { return launch_train_forward(sh, a, m->num_sms, st); }))) != NPM_OK) return r;
-  if ((r = check_launch(m, timed(m, kKTrainBwd, st, [&] { return launch_train_backward(sh, a, m->num_sms, st); }))) != NPM_OK) return r;
-  if ((r = check_launch(m, timed(m, kKWgrad, st, [&] { return launch_weight_grads(sh, a, m->num_sms, st); }))) != NPM_OK) return r;
-  return NPM_OK;
 }
 
 static bool train_args_ok(const npm_model* m, const npm_query* q, const float* wix, const float* wiy,
@@ -1240,7 +1245,7 @@ static npm_status accumulate_pipelined(npm_model* m, const npm_query* q, const f
                                        const float* wiz, const float* target, int channels, const float* spdf,
                                        int64_t n_global, cudaStream_t st) {
   const bool prod = m->cfg.mode == NPM_PRODUCT;
-  if (!m->use_tc || !HostPipe::usable(m, q->n, {q->px, q->py, q->pz, prod ? q->wox : nullptr, prod ? q->nx : nullptr,
+  if (!HostPipe::usable(m, q->n, {q->px, q->py, q->pz, prod ? q->wox : nullptr, prod ? q->nx : nullptr,
                                                 prod ? q->rough : nullptr, wix, wiy, wiz, target, spdf}))
     return NPM_ERR_STATE;
   HostPipe hp{m, st, q->n};

@@ -180,10 +180,6 @@ using namespace detail;
 
 // Per-shape entry points, defined in npm_net_*.cu.
 #define NPM_DECLARE_NET(TAG)                                                         \
-  int net_query_##TAG(const QueryArgs&, int, cudaStream_t);                        \
-  int net_train_fwd_##TAG(const TrainArgs&, int, cudaStream_t);                    \
-  int net_train_bwd_##TAG(const TrainArgs&, int, cudaStream_t);                    \
-  int net_dw_##TAG(const TrainArgs&, int, cudaStream_t);                           \
   int net_smem_##TAG();                                                             \
   int net_query_tc_##TAG(const QueryArgs&, int, cudaStream_t);                     \
   int net_train_tc_##TAG(const TrainArgs&, int, cudaStream_t);
@@ -194,19 +190,15 @@ NPM_DECLARE_NET(p16)
 #undef NPM_DECLARE_NET
 
 namespace {
-enum Op { kQuery, kTrainFwd, kTrainBwd, kDw, kSmem, kQueryTc, kTrainTc };
+enum Op { kSmem, kQueryTc, kTrainTc };
 
 template <class Args>
 int call(const NetShape& s, Op op, const Args* a, int sms, cudaStream_t st) {
 #define NPM_CASE(TAG, NIN, W, NL, NOUT, PROD)                                                          \
   if (s.n_in == NIN && s.width == W && s.n_layers == NL && s.n_out == NOUT && s.product == PROD) {     \
     if constexpr (std::is_same<Args, QueryArgs>::value) {                                              \
-      if (op == kQuery) return net_query_##TAG(*a, sms, st);                                           \
       if (op == kQueryTc) return net_query_tc_##TAG(*a, sms, st);                                      \
     } else if constexpr (std::is_same<Args, TrainArgs>::value) {                                       \
-      if (op == kTrainFwd) return net_train_fwd_##TAG(*a, sms, st);                                    \
-      if (op == kTrainBwd) return net_train_bwd_##TAG(*a, sms, st);                                    \
-      if (op == kDw) return net_dw_##TAG(*a, sms, st);                                                 \
       if (op == kTrainTc) return net_train_tc_##TAG(*a, sms, st);                                      \
     }                                                                                                  \
     if (op == kSmem) return net_smem_##TAG();                                                          \
@@ -227,10 +219,6 @@ size_t weight_smem_bytes(const NetShape& s) {
   return r < 0 ? 0 : (size_t)r;
 }
 
-int launch_query(const NetShape& s, const QueryArgs& a, int sms, cudaStream_t st) {
-  if (a.n == 0) return 0;
-  return call(s, kQuery, &a, sms, st);
-}
 int launch_query_tc(const NetShape& s, const QueryArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return 0;
   return call(s, kQueryTc, &a, sms, st);
@@ -238,18 +226,6 @@ int launch_query_tc(const NetShape& s, const QueryArgs& a, int sms, cudaStream_t
 int launch_train_tc(const NetShape& s, const TrainArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return 0;
   return call(s, kTrainTc, &a, sms, st);
-}
-int launch_train_forward(const NetShape& s, const TrainArgs& a, int sms, cudaStream_t st) {
-  if (a.n == 0) return 0;
-  return call(s, kTrainFwd, &a, sms, st);
-}
-int launch_train_backward(const NetShape& s, const TrainArgs& a, int sms, cudaStream_t st) {
-  if (a.n == 0) return 0;
-  return call(s, kTrainBwd, &a, sms, st);
-}
-int launch_weight_grads(const NetShape& s, const TrainArgs& a, int sms, cudaStream_t st) {
-  if (a.n == 0) return 0;
-  return call(s, kDw, &a, sms, st);
 }
 
 int launch_encode(int L, const QueryArgs& a, int sms, cudaStream_t st) {

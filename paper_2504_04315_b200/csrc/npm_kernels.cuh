@@ -63,13 +63,9 @@ struct TrainArgs {
   float* grads;
   GridDesc grid;
   float log_kmin, log_kmax;
-  // scratch, feature-major [rows][n]
-  float* act[3];            // inputs of layer k: z, h1, h2
-  float* delta[3];          // d loss / d pre-activation of layer k
   int debug;                // measurement knob (NPM_DEBUG): bit0 skip scatter, bit1 skip gathers,
                             // bit2 record per-phase clock64 stamps of CTA 0 into dbg_clock
   long long* dbg_clock;     // [64 tiles][16 stamps] (debug only)
-  int legacy;               // 1: one 128-sample tile per CTA (tc_train_kernel) instead of two 64-sample tiles
   // Privatised coarse levels: levels in priv_mask scatter into the CTA's own
   // copy (priv + blockIdx.x * priv_stride + priv_off[l] entries) instead of
   // the shared gradient: every sample touches 8 of their few entries, and all
@@ -94,11 +90,7 @@ bool shape_supported(const NetShape& s);
 size_t weight_smem_bytes(const NetShape& s);
 
 // Every launcher returns the number of kernels launched (>= 1) or -1 on error.
-int launch_query(const NetShape& s, const QueryArgs& a, int num_sms, cudaStream_t st);
 int launch_encode(int L, const QueryArgs& a, int num_sms, cudaStream_t st);  // a.params = grid section
-int launch_train_forward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
-int launch_train_backward(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
-int launch_weight_grads(const NetShape& s, const TrainArgs& a, int num_sms, cudaStream_t st);
 int launch_adam(const AdamArgs& a, int num_sms, cudaStream_t st);
 
 // Adds the per-CTA private copies of the privatised levels into the gradient

@@ -5,10 +5,6 @@
 
 namespace npm {
 using NetT = detail::Net<32, 64, 3, 32>;
-int net_query_c2(const QueryArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::query(a, sms, st); }
-int net_train_fwd_c2(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::train_fwd(a, sms, st); }
-int net_train_bwd_c2(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::train_bwd(a, sms, st); }
-int net_dw_c2(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::dw(a, sms, st); }
 int net_smem_c2() { return NetT::SMEM_FLOATS * (int)sizeof(float); }
 int net_query_tc_c2(const QueryArgs& a, int sms, cudaStream_t st) { return tck::TcLaunch<NetT>::query(a, sms, st); }
 int net_train_tc_c2(const TrainArgs& a, int sms, cudaStream_t st) { return tck::TcLaunch<NetT>::train(a, sms, st); }

@@ -5,10 +5,6 @@
 
 namespace npm {
 using NetT = detail::Net<65, 64, 3, 64>;
-int net_query_p16(const QueryArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::query(a, sms, st); }
-int net_train_fwd_p16(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::train_fwd(a, sms, st); }
-int net_train_bwd_p16(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::train_bwd(a, sms, st); }
-int net_dw_p16(const TrainArgs& a, int sms, cudaStream_t st) { return detail::Launch<NetT>::dw(a, sms, st); }
 int net_smem_p16() { return NetT::SMEM_FLOATS * (int)sizeof(float); }
 int net_query_tc_p16(const QueryArgs& a, int sms, cudaStream_t st) { return tck::TcLaunch<NetT>::query(a, sms, st); }
 int net_train_tc_p16(const TrainArgs& a, int sms, cudaStream_t st) { return tck::TcLaunch<NetT>::train(a, sms, st); }

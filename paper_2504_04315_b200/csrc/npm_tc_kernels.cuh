@@ -54,43 +54,9 @@ struct TC {
   static constexpr uint32_t WBYTES = woff(NL);
   __host__ __device__ static constexpr uint32_t boff(int k) { return 4u * (uint32_t)osum(k); }
   static constexpr uint32_t BBYTES = boff(NL);
-  // TMEM columns: scratch [0, 64), dW^T accumulators after it
-  static constexpr int SCR = 64;
-  __host__ __device__ static constexpr int dwcol(int k) { return SCR + osum(k); }
-  static constexpr int TCOLS_TRAIN = 256;
   static constexpr int TCOLS_QUERY = 64;
-  // ---- train smem map: X_0 (ZF), X_1..X_{NL-1} (HF), D_last (NOUT), weights, bias
+  // train X_k features
   __host__ __device__ static constexpr uint32_t xfeat(int k) { return k == 0 ? ZF : HF; }
-  __host__ __device__ static constexpr uint32_t xoff(int k) {  // hi at xoff, lo at xoff + xfeat/8*CH
-    return k == 0 ? 0u : 2u * (ZF / 8) * CH + (uint32_t)(k - 1) * 2u * (HF / 8) * CH;
-  }
-  static constexpr uint32_t DOFF = xoff(NL);
-  // hidden-layer deltas D_0..D_{NL-2} get their own buffers when smem allows
-  // (SEP_D): each dW_k^T MMA batch then runs behind the next dX while the
-  // threads compute the next delta; otherwise D_{k-1} overwrites X_k.
-  static constexpr uint32_t DHOFF = DOFF + 2u * (NOUT / 8) * CH;
-  static constexpr uint32_t DH_ONE = 2u * (W / 8) * CH;
-  // Measured on B200 (c2): the deferred-dW overlap (SEP_D) costs +64 KB smem,
-  // which shrinks L1 (unified with smem) and the gathers' L1 hit rate (28 % of
-  // sectors at 150 KB smem): 0.97 ms vs 0.82 ms per train step. Kept off; the
-  // code path stays for configurations with small activation tiles.
-  static constexpr bool SEP_D = false &&
-      DHOFF + (NL - 1) * DH_ONE + WBYTES + BBYTES + 3u * 4u * R * 4u + 512u <= 227u * 1024u;
-  __host__ __device__ static constexpr uint32_t dhoff(int k) { return DHOFF + (uint32_t)k * DH_ONE; }
-  static constexpr uint32_t WOFF_T = DHOFF + (SEP_D ? (NL - 1) * DH_ONE : 0u);
-  static constexpr uint32_t BOFF_T = WOFF_T + WBYTES;
-  static constexpr uint32_t RED_T = (BOFF_T + BBYTES + 127u) & ~127u;   // head reductions [3][4][R] f32
-  static constexpr uint32_t MISC_T = RED_T + 3u * 4u * R * 4u;
-  // every X_k^T MMA reads 16 chunks from its lo base: keep them inside the allocation
-  __host__ __device__ static constexpr uint32_t overread(int k) {
-    return xoff(k) + (xfeat(k) / 8) * CH + 16u * CH;
-  }
-  __host__ __device__ static constexpr uint32_t max_overread(int k) {
-    return k < 0 ? 0u : (overread(k) > max_overread(k - 1) ? overread(k) : max_overread(k - 1));
-  }
-  static constexpr uint32_t SMEM_TRAIN_RAW = MISC_T + 64;
-  static constexpr uint32_t SMEM_TRAIN =
-      SMEM_TRAIN_RAW > max_overread(NL - 1) ? SMEM_TRAIN_RAW : max_overread(NL - 1);
   // ---- query smem map: buffer A (max(KIN, W) feats), buffer B (W feats), weights, bias
   static constexpr int QAF = KIN > W ? KIN : W;
   static constexpr uint32_t QA = 0, QB = 2u * (QAF / 8) * CH;
@@ -163,49 +129,6 @@ __device__ __forceinline__ void issue_fwd(uint32_t d, uint32_t xhi, uint32_t xlo
     const uint64_t xa = (uint64_t)(s * 2 * (int)CH) >> 4, wa = (uint64_t)(s * 2 * out * 16) >> 4;
     mma3(d, ah + xa, al + xa, bh + wa, bl + wa, idesc, s > 0 ? 1u : 0u);
   }
-}
-
-// dX MMA: D[R x nin] = delta[R x out] W[out x nin]: A K-major, B MN-major.
-__device__ __forceinline__ void issue_dx(uint32_t d, uint32_t dhi, uint32_t dlo, uint32_t whi, uint32_t wlo,
-                                         int out, int nin) {
-  const uint32_t idesc = tc::idesc_bf16(R, nin, false, true);
-  const uint64_t ah = tc::sdesc(dhi, CH, 128), al = tc::sdesc(dlo, CH, 128);
-  const uint64_t bh = tc::sdesc(whi, 128, out * 16), bl = tc::sdesc(wlo, 128, out * 16);
-#pragma unroll
-  for (int s = 0; s < out / 16; ++s) {
-    const uint64_t da = (uint64_t)(s * 2 * (int)CH) >> 4, wa = (uint64_t)(s * 256) >> 4;
-    mma3(d, ah + da, al + da, bh + wa, bl + wa, idesc, s > 0 ? 1u : 0u);
-  }
-}
-
-// dW^T MMA: D[128 x out] += X^T[128 feats x R] delta[R x out]: both MN-major.
-__device__ __forceinline__ void issue_dw(uint32_t d, uint32_t xhi, uint32_t xlo, uint32_t dhi, uint32_t dlo,
-                                         int out, uint32_t first) {
-  const uint32_t idesc = tc::idesc_bf16(128, out, true, true);
-  const uint64_t ah = tc::sdesc(xhi, 128, CH), al = tc::sdesc(xlo, 128, CH);
-  const uint64_t bh = tc::sdesc(dhi, 128, CH), bl = tc::sdesc(dlo, 128, CH);
-#pragma unroll
-  for (int s = 0; s < R / 16; ++s) {
-    const uint64_t ra = (uint64_t)(s * 256) >> 4;
-    mma3(d, ah + ra, al + ra, bh + ra, bl + ra, idesc, (first && s == 0) ? 0u : 1u);
-  }
-}
-
-// Read `cols` fp32 TMEM columns of this thread's lane starting at col.
-template <int COLS>
-__device__ __forceinline__ void tmem_row(uint32_t tbase, int col, float* v) {
-  const uint32_t lane = (uint32_t)((threadIdx.x & ~31) << 16);
-#pragma unroll
-  for (int c = 0; c < COLS; c += 16) tc::tmem_ld16(tbase + lane + (uint32_t)(col + c), v + c);
-  tc::tmem_wait_ld();
-}
-
-// Make this thread's smem writes visible to the tensor core and its TMEM
-// reads ordered before the next MMA, then CTA barrier.
-__device__ __forceinline__ void handoff_to_mma() {
-  tc::fence_proxy_async();
-  tc::fence_before_sync();
-  __syncthreads();
 }
 
 __device__ __forceinline__ void wait_mma(uint64_t* mbar, uint32_t& phase) {
@@ -580,386 +503,6 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     }
   }
   teardown_cta(tbase - (uint32_t)(g * T::TCOLS_QUERY), GROUPS * T::TCOLS_QUERY);
-}
-
-// ---------------------------------------------------------------------------
-// Fused training kernel, 4 threads per sample row (512 threads, 16 warps):
-// thread (q, r): quarter q = warp / 4 in [0, 4), row r = 32 (warp % 4) + lane,
-// i.e. TMEM lane r.  Quarter q owns grid levels [q L/4, (q+1) L/4) in the
-// encode and the scatter, columns [q C/4, (q+1) C/4) of every accumulator in
-// the epilogues, and lobes [q K/4, (q+1) K/4) in the Eq. 9 head (cross-quarter
-// softmax / mixture sums through smem).  Phases per 128-sample tile:
-//   encode -> X0;  forward k: MMA, epilogue -> X_{k+1};  head -> delta_L;
-//   backward k = L..0: MMA batch {dX, dW_k^T += X_k^T delta_k}, epilogue
-//   delta_{k-1} (or dz -> red.global.add.v4.f32 on the grid gradient).
-template <class N>
-__global__ void __launch_bounds__(4 * R, 1) tc_train_kernel(TrainArgs a) {
-  using T = TC<N>;
-  constexpr int NL = N::NL, K = N::K, W = N::W, NOUT = N::NOUT;
-  constexpr int KQ = K / 4, WQ = W / 4, LQ = N::L / 4, GQ = 4 * LQ;
-  static_assert(K % 4 == 0 && N::L % 4 == 0 && W % 32 == 0, "quartered kernel shape");
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t sb = tc::smem_u32(smem);
-  const int tid = threadIdx.x, warp = tid >> 5, q = warp >> 2;
-  const int r = ((warp & 3) << 5) | (tid & 31);
-  const uint32_t lane_addr = (uint32_t)((warp & 3) << 21);   // (32 * (warp % 4)) << 16
-  uint64_t* mbar;
-  uint32_t tbase;
-  setup_cta<N>(smem, T::MISC_T, T::TCOLS_TRAIN, mbar, tbase);
-  stage_weights_tc<N>(a.params, smem, T::WOFF_T, T::BOFF_T);
-  const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
-  float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
-  const float* bias = reinterpret_cast<const float*>(smem + T::BOFF_T);
-  float* red = reinterpret_cast<float*>(smem + T::RED_T);   // [3][4][R]
-  const int64_t n = a.n;
-  const int64_t ntiles = (n + R - 1) / R;
-  uint32_t phase = 0, phase_dw = 0, first = 1;
-  double loss = 0.0;
-  unsigned c_used = 0, c_zero = 0, c_drop = 0;
-  uint32_t xhi[NL], xlo[NL];
-#pragma unroll
-  for (int k = 0; k < NL; ++k) {
-    xhi[k] = sb + T::xoff(k);
-    xlo[k] = xhi[k] + (T::xfeat(k) / 8) * CH;
-  }
-  const uint32_t dlast_hi = sb + T::DOFF, dlast_lo = dlast_hi + (NOUT / 8) * CH;
-  int tile_no = 0;
-  const bool stamp = (a.debug & 4) && blockIdx.x == 0 && tid == 0;
-#define NPM_STAMP(idx) \
-  do { if (stamp && tile_no < 64) a.dbg_clock[tile_no * 16 + (idx)] = clock64(); } while (0)
-  // Per-tile record inputs of this thread (its row, its levels).  The encode of
-  // tile t+1 (index, position, gathers) is issued while tile t's last backward
-  // MMA batch runs; only the smem stores wait for that batch.
-  struct TileIn {
-    int64_t i;
-    bool valid;
-    float ux, uy, uz;
-    float g[GQ];
-  };
-  auto load_tile = [&](int64_t tl, TileIn& t) {
-    const int64_t slot = tl * R + r;                  // processing slot (binned order if perm)
-    t.valid = slot < n;
-    t.i = t.valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
-    t.ux = t.uy = t.uz = 0.f;
-    if (t.valid) {
-      t.ux = normalize_axis(__ldg(a.px + t.i), a.grid.lo[0], a.grid.inv[0]);
-      t.uy = normalize_axis(__ldg(a.py + t.i), a.grid.lo[1], a.grid.inv[1]);
-      t.uz = normalize_axis(__ldg(a.pz + t.i), a.grid.lo[2], a.grid.inv[2]);
-#pragma unroll
-      for (int ll = 0; ll < LQ; ++ll) {
-        const int l = q * LQ + ll;
-        LevelCorners lc;
-        level_corners(a.grid, l, t.ux, t.uy, t.uz, lc);
-        const float4* tb = tab + a.grid.off[l];
-        float4 v[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          v[c] = (a.debug & 2) ? make_float4(lc.w[c], 0.f, 0.f, 0.f) : __ldg(tb + lc.idx[c]);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
-          a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
-        }
-        t.g[4 * ll] = a0; t.g[4 * ll + 1] = a1; t.g[4 * ll + 2] = a2; t.g[4 * ll + 3] = a3;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < GQ; ++j) t.g[j] = 0.0f;
-    }
-  };
-  TileIn cur;
-  if (blockIdx.x < ntiles) load_tile(blockIdx.x, cur);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_no) {
-    NPM_STAMP(0);
-    const bool valid = cur.valid;
-    const int64_t i = cur.i;
-    const int64_t ic = i;
-    const float ux = cur.ux, uy = cur.uy, uz = cur.uz;
-    // head inputs: issued now, consumed after the forward MMAs
-    const float h_wx = __ldg(a.wx + ic), h_wy = __ldg(a.wy + ic), h_wz = __ldg(a.wz + ic);
-    const float h_t0 = __ldg(a.target + ic);
-    const float h_t1 = a.channels == 3 ? __ldg(a.target + a.target_stride + ic) : 0.f;
-    const float h_t2 = a.channels == 3 ? __ldg(a.target + 2 * a.target_stride + ic) : 0.f;
-    const float h_p = __ldg(a.spdf + ic);
-    uint32_t mask[NL];   // ReLU mask bits of this quarter's WQ columns of X_1..X_{NL-1}
-    // ---- encode: levels [q LQ, (q+1) LQ) -> features [q GQ, (q+1) GQ) of X0
-    {
-      float* g = cur.g;
-      // SEP_D: the previous tile's deferred dW batch reads X_0 .. X_{NL-1} and the
-      // deltas; the gathers above overlapped it, wait before overwriting.
-      if constexpr (T::SEP_D) {
-        if (!first) wait_mma(mbar + 1, phase_dw);
-      }
-      tc::store_feats<GQ>(xhi[0], xlo[0], R, r, q * GQ, g);
-      // conditioning / ones features [NGRID, ZF)
-      if constexpr (N::PRODUCT) {
-        float e[16];
-        if (q == 0 || q == 1) {
-          if (valid) {
-            if (q == 0) sh4(__ldg(a.wox + i), __ldg(a.woy + i), __ldg(a.woz + i), e);
-            else sh4(__ldg(a.nx + i), __ldg(a.ny + i), __ldg(a.nz + i), e);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) e[j] = 0.0f;
-          }
-          tc::store_feats<16>(xhi[0], xlo[0], R, r, 32 + 16 * q, e);
-        } else if (q == 2) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) e[j] = 0.0f;
-          e[0] = valid ? __ldg(a.rough + i) : 0.0f;   // feature 64
-          e[1] = 1.0f;                                  // feature 65 = NIN: ones (bias row)
-          tc::store_feats<16>(xhi[0], xlo[0], R, r, 64, e);
-        }
-      } else {
-        if (q == 3) {
-          float e[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int f = N::NGRID; f < T::ZF; f += 8) {
-            tc::store_chunk(xhi[0], xlo[0], R, r, f / 8, e);
-            e[0] = 0.f;
-          }
-        }
-      }
-    }
-    // ---- forward
-#pragma unroll
-    for (int k = 0; k < NL; ++k) {
-      handoff_to_mma();
-      NPM_STAMP(1 + 2 * k);
-      if (tid == 0) {
-        tc::fence_after_sync();
-        const uint32_t w = sb + T::WOFF_T + T::woff(k);
-        issue_fwd(tbase, xhi[k], xlo[k], w, w + T::wbytes(k), T::in_p(k), T::out(k));
-        tc::mma_commit(mbar);
-      }
-      wait_mma(mbar, phase);
-      NPM_STAMP(2 + 2 * k);
-      const float* b = bias + T::boff(k) / 4;
-      if (k < NL - 1) {
-        float h[WQ];
-        tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), h);
-        tc::tmem_wait_ld();
-        uint32_t mk = 0;
-#pragma unroll
-        for (int j = 0; j < WQ; ++j) {
-          h[j] = fmaxf(h[j] + b[q * WQ + j], 0.0f);
-          mk |= (h[j] > 0.0f ? 1u : 0u) << j;
-        }
-        mask[k + 1] = mk;
-        tc::store_feats<WQ>(xhi[k + 1], xlo[k + 1], R, r, q * WQ, h);
-        if (q == 3) {   // ones feature at W (bias row of dW_{k+1}^T)
-          const float e[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          tc::store_chunk(xhi[k + 1], xlo[k + 1], R, r, W / 8, e);
-        }
-      } else {
-        // ---- Eq. 9 head, lobes [q KQ, (q+1) KQ) (C-O12, C-O13)
-        float lp[KQ], kp[KQ], tp[KQ], pp[KQ];
-        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(q * KQ), lp);
-        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(K + q * KQ), kp);
-        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(2 * K + q * KQ), tp);
-        tc::tmem_ldn<KQ>(tbase + lane_addr + (uint32_t)(3 * K + q * KQ), pp);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < KQ; ++j) {
-          lp[j] += b[q * KQ + j]; kp[j] += b[K + q * KQ + j];
-          tp[j] += b[2 * K + q * KQ + j]; pp[j] += b[3 * K + q * KQ + j];
-        }
-        // record scale (every quarter evaluates it for its row; inputs prefetched)
-        float t = h_t0;
-        bool all_zero = t == 0.0f;
-        if (a.channels == 3) {
-          all_zero = all_zero && h_t1 == 0.0f && h_t2 == 0.0f;
-          t = 0.2126f * t + 0.7152f * h_t1 + 0.0722f * h_t2;
-        }
-        const float p = h_p;
-        const float ratio = t / p;
-        const bool drop = valid && (!isfinite(ratio) || !isfinite(p) || !(p > 0.0f));
-        const bool zero = valid && !drop && all_zero;
-        const bool use = valid && !drop && !zero;
-        const float s = use ? (float)(-(double)ratio * a.inv_n_global) : 0.0f;
-        const float wx = h_wx, wy = h_wy, wz = h_wz;
-        // own lobes: kappa, mu, v_i(w)
-        float kap[KQ], mx[KQ], my[KQ], mz[KQ], th[KQ], ph[KQ], v[KQ];
-        float sth[KQ], cth[KQ], sph[KQ], cph[KQ];
-        float mloc = lp[0];
-#pragma unroll
-        for (int j = 0; j < KQ; ++j) {
-          mloc = fmaxf(mloc, lp[j]);
-          kap[j] = expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
-          th[j] = 1.0f / (1.0f + expf(-tp[j]));
-          ph[j] = 1.0f / (1.0f + expf(-pp[j]));
-          sincospif(th[j], &sth[j], &cth[j]);
-          sincospif(2.0f * ph[j], &sph[j], &cph[j]);
-          mx[j] = sth[j] * cph[j]; my[j] = sth[j] * sph[j]; mz[j] = cth[j];
-          v[j] = lobe_pdf(kap[j], mx[j], my[j], mz[j], wx, wy, wz);
-        }
-        // softmax max over all K lambda' (cross-quarter)
-        red[(0 * 4 + q) * R + r] = mloc;
-        __syncthreads();
-        const float M = fmaxf(fmaxf(red[0 * R + r], red[1 * R + r]), fmaxf(red[2 * R + r], red[3 * R + r]));
-        float e[KQ], S = 0.0f, P = 0.0f;
-#pragma unroll
-        for (int j = 0; j < KQ; ++j) {
-          e[j] = expf(lp[j] - M);
-          S += e[j];
-          P += e[j] * v[j];
-        }
-        red[(1 * 4 + q) * R + r] = S;
-        red[(2 * 4 + q) * R + r] = P;
-        __syncthreads();
-        const float Ssum = red[4 * R + r] + red[5 * R + r] + red[6 * R + r] + red[7 * R + r];
-        const float Psum = red[8 * R + r] + red[9 * R + r] + red[10 * R + r] + red[11 * R + r];
-        const float invS = 1.0f / Ssum;
-        const float Vb = fmaxf(Psum * invS, kVFloor);
-        const float invV = 1.0f / Vb;
-        float dl[KQ], dk[KQ], dt[KQ], dp[KQ];
-#pragma unroll
-        for (int j = 0; j < KQ; ++j) {
-          const float lam = e[j] * invS;
-          const float gam = lam * v[j] * invV;
-          dl[j] = s * (gam - lam);
-          const float dx = mx[j] - wx, dy = my[j] - wy, dz = mz[j] - wz;
-          const float d2 = dx * dx + dy * dy + dz * dz;
-          const float em = -expm1f(-2.0f * kap[j]);
-          const float dkk = s * gam * (1.0f - kap[j] * 0.5f * d2 - 2.0f * kap[j] * expf(-2.0f * kap[j]) / em);
-          dk[j] = (kp[j] < a.log_kmin || kp[j] > a.log_kmax) ? 0.0f : dkk;
-          const float st = sth[j], ct = cth[j], sp = sph[j], cp = cph[j];
-          const float wdth = kPi * (ct * cp * wx + ct * sp * wy - st * wz);
-          const float wdph = kTwoPi * (-st * sp * wx + st * cp * wy);
-          const float sgk = s * gam * kap[j];
-          dt[j] = sgk * wdth * th[j] * (1.0f - th[j]);
-          dp[j] = sgk * wdph * ph[j] * (1.0f - ph[j]);
-        }
-        if (q == 0) {
-          c_drop += drop; c_zero += zero;
-          if (use) { loss += (double)s * (double)logf(Vb); c_used += 1; }
-        }
-        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, q * KQ, dl);
-        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, K + q * KQ, dk);
-        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, 2 * K + q * KQ, dt);
-        tc::store_feats<KQ>(dlast_hi, dlast_lo, R, r, 3 * K + q * KQ, dp);
-      }
-    }
-    // ---- backward
-    uint32_t dhi = dlast_hi, dlo = dlast_lo;
-    TileIn nxt;
-#pragma unroll
-    for (int k = NL - 1; k >= 0; --k) {
-      handoff_to_mma();
-      NPM_STAMP(1 + 2 * NL + 2 * (NL - 1 - k));
-      if (tid == 0) {
-        tc::fence_after_sync();
-        const uint32_t w = sb + T::WOFF_T + T::woff(k);
-        issue_dx(tbase, dhi, dlo, w, w + T::wbytes(k), T::out(k), k > 0 ? W : N::NGRID);
-        if constexpr (T::SEP_D) {
-          // commit the dX alone; dW_k^T runs behind it while the threads build delta_{k-1}
-          tc::mma_commit(mbar);
-          issue_dw(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, T::out(k), first);
-          if (k == 0) tc::mma_commit(mbar + 1);
-        } else {
-          issue_dw(tbase + (uint32_t)T::dwcol(k), xhi[k], xlo[k], dhi, dlo, T::out(k), first);
-          tc::mma_commit(mbar);
-        }
-      }
-      // next tile's encode (index, position, gathers) overlaps the last MMA batch
-      if (k == 0 && tile + gridDim.x < ntiles) load_tile(tile + gridDim.x, nxt);
-      wait_mma(mbar, phase);
-      NPM_STAMP(2 + 2 * NL + 2 * (NL - 1 - k));
-      if (k > 0) {
-        float d[WQ];
-        tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), d);
-        tc::tmem_wait_ld();
-        const uint32_t mk = mask[k];
-#pragma unroll
-        for (int j = 0; j < WQ; ++j) d[j] = ((mk >> j) & 1u) ? d[j] : 0.0f;
-        if constexpr (T::SEP_D) {
-          dhi = sb + T::dhoff(k - 1);
-        } else {
-          dhi = xhi[k];                     // delta_{k-1} overwrites X_k (its dW MMA completed)
-        }
-        dlo = dhi + (W / 8) * CH;
-        tc::store_feats<WQ>(dhi, dlo, R, r, q * WQ, d);
-      } else {
-        float dz[GQ];
-        tc::tmem_ldn<GQ>(tbase + lane_addr + (uint32_t)(q * GQ), dz);
-        tc::tmem_wait_ld();
-        if (!(a.debug & 1)) {
-#pragma unroll
-          for (int ll = 0; ll < LQ; ++ll) {
-            const int l = q * LQ + ll;
-            const float g0 = dz[4 * ll], g1 = dz[4 * ll + 1], g2 = dz[4 * ll + 2], g3 = dz[4 * ll + 3];
-            LevelCorners lc;
-            level_corners(a.grid, l, ux, uy, uz, lc);
-            float4* t = gtab + a.grid.off[l];
-            // Warp-uniform cell (spatially binned batches, coarse levels): reduce
-            // the 8 weighted corner updates over the warp, one RED per corner.
-            const uint32_t c0 = valid ? lc.idx[0] : 0xFFFFFFFFu;
-            const bool uniform = __all_sync(0xffffffffu, c0 == __shfl_sync(0xffffffffu, c0, 0) && valid);
-            if (uniform) {
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                const float w = lc.w[c];
-                float s0 = w * g0, s1 = w * g1, s2 = w * g2, s3 = w * g3;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                  s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-                  s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                  s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-                  s3 += __shfl_xor_sync(0xffffffffu, s3, o);
-                }
-                if ((tid & 31) == 0 && (s0 != 0.0f || s1 != 0.0f || s2 != 0.0f || s3 != 0.0f))
-                  atomicAdd(t + lc.idx[c], make_float4(s0, s1, s2, s3));
-              }
-            } else if (valid && (g0 != 0.0f || g1 != 0.0f || g2 != 0.0f || g3 != 0.0f)) {
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                const float w = lc.w[c];
-                atomicAdd(t + lc.idx[c], make_float4(w * g0, w * g1, w * g2, w * g3));
-              }
-            }
-          }
-        }
-      }
-    }
-    first = 0;
-    NPM_STAMP(15);
-    cur = nxt;
-  }
-#undef NPM_STAMP
-  // ---- flush dW^T / db: lane r = input feature r (r == in: bias); quarter q
-  // takes columns [q out/4, (q+1) out/4)
-  if (!first) {
-    if constexpr (T::SEP_D) wait_mma(mbar + 1, phase_dw);   // last tile's deferred dW batch
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-#pragma unroll
-    for (int k = 0; k < NL; ++k) {
-      constexpr int MAXO = (NOUT > W ? NOUT : W) / 4;
-      float v[MAXO];
-      const int out = T::out(k), in = T::in(k), oq = out / 4;
-      if (out == NOUT) tc::tmem_ldn<NOUT / 4>(tbase + lane_addr + (uint32_t)(T::dwcol(k) + q * (NOUT / 4)), v);
-      else tc::tmem_ldn<W / 4>(tbase + lane_addr + (uint32_t)(T::dwcol(k) + q * (W / 4)), v);
-      tc::tmem_wait_ld();
-      if (r < in) {
-        float* g = a.grads + N::gw_off(k) + r;
-        for (int o = 0; o < oq; ++o) atomicAdd(g + (q * oq + o) * in, v[o]);
-      } else if (r == in) {
-        float* g = a.grads + N::gb_off(k);
-        for (int o = 0; o < oq; ++o) atomicAdd(g + q * oq + o, v[o]);
-      }
-    }
-  }
-  loss = warp_sum_d(loss);
-  c_used = warp_sum_u(c_used); c_zero = warp_sum_u(c_zero); c_drop = warp_sum_u(c_drop);
-  if ((threadIdx.x & 31) == 0 && q == 0) {
-    atomicAdd(a.stats, loss);
-    atomicAdd(a.counters + 0, (unsigned long long)c_used);
-    atomicAdd(a.counters + 1, (unsigned long long)c_zero);
-    atomicAdd(a.counters + 2, (unsigned long long)c_drop);
-  }
-  teardown_cta(tbase, T::TCOLS_TRAIN);
 }
 
 // ---------------------------------------------------------------------------
@@ -1567,21 +1110,12 @@ struct TcLaunch {
     return 1;
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
-    using T = TC<N>;
-    if (!a.legacy) {   // two 64-sample tiles per CTA (tc_train64_kernel)
-      using T64 = TC64<N>;
-      cudaFuncSetAttribute(tc_train64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T64::SMEM);
-      const int64_t pairs = (a.n + 2 * T64::RT - 1) / (2 * T64::RT);
-      const int blocks = (int)(pairs < (int64_t)sms ? pairs : (int64_t)sms);
-      tc_train64_kernel<N><<<blocks, 512, T64::SMEM, st>>>(a);
-      return 1;
-    }
-    cudaFuncSetAttribute(tc_train_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_TRAIN);
-    const int64_t ntiles = (a.n + R - 1) / R;
-    // 512 threads, ~150 KB smem: one CTA per SM
-    const int64_t cap = (int64_t)sms;
-    const int blocks = (int)(ntiles < cap ? ntiles : cap);
-    tc_train_kernel<N><<<blocks, 4 * R, T::SMEM_TRAIN, st>>>(a);
+    // two 64-sample tiles per CTA (tc_train64_kernel)
+    using T64 = TC64<N>;
+    cudaFuncSetAttribute(tc_train64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T64::SMEM);
+    const int64_t pairs = (a.n + 2 * T64::RT - 1) / (2 * T64::RT);
+    const int blocks = (int)(pairs < (int64_t)sms ? pairs : (int64_t)sms);
+    tc_train64_kernel<N><<<blocks, 512, T64::SMEM, st>>>(a);
     return 1;
   }
 };

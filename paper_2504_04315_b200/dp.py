@@ -62,7 +62,8 @@ class DataParallel:
         group) sums GRADS inside npm_optimizer_step; otherwise GRADS are
         allreduced here through torch.distributed."""
         self.t = model if hasattr(model, "accumulate") else NpmTrainer(model)
-        self.world = world if world is not None else (dist.get_world_size() if dist.is_initialized() else 1)
+        # rank and world are taken within `group` (the default group if None)
+        self.world = world if world is not None else (dist.get_world_size(group) if dist.is_initialized() else 1)
         self.group = group
         self.reduce = self.world > 1 or force_allreduce   # force: exercise the collective at world size 1
         if native:
@@ -70,7 +71,9 @@ class DataParallel:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
             uid = [npm.npm_get_unique_id() if rank == 0 else None]
             if dist.is_initialized():
-                dist.broadcast_object_list(uid, src=0, group=group)
+                # broadcast_object_list takes a GLOBAL source rank: group rank 0's
+                src = dist.get_global_rank(group, 0) if group is not None else 0
+                dist.broadcast_object_list(uid, src=src, group=group)
             npm.npm_comm_init(self.t.m.h, rank, self.world, uid[0])
             self.reduce = False
 
@@ -78,11 +81,21 @@ class DataParallel:
         if self.reduce:
             dist.all_reduce(self.t.grad_tensor(), op=dist.ReduceOp.SUM, group=self.group)
 
+    def global_count(self, n_local):
+        """N_global = sum of the ranks' shard sizes (shards may be unequal,
+        shard_range gives the first n % world ranks one more record)."""
+        if self.world == 1 or not dist.is_initialized():
+            return int(n_local)
+        v = torch.tensor([int(n_local)], dtype=torch.int64, device=self.t.grad_tensor().device)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
+        return int(v.item())
+
     def train_step(self, q, wi, target, spdf, n_local=None, n_global=None, want_stats=False):
         """One data-parallel optimisation step on this rank's shard.
-        n_global defaults to world * n_local (equal shards)."""
+        n_global defaults to the sum of the ranks' n_local (one small
+        allreduce; pass it to avoid that)."""
         if n_global is None:
-            n_global = self.world * (n_local if n_local is not None else q.n)
+            n_global = self.global_count(n_local if n_local is not None else q.n)
         st = self.t.accumulate(q, wi, target, spdf, n_global, want_stats)
         self.allreduce_grads()
         st2 = self.t.optimizer_step(want_stats)
@@ -104,11 +117,20 @@ class DataParallel:
         Each rank cuts its n_local records into consecutive slices of
         micro_local (make_slice(a, b) -> (q, wi, target, spdf) of local
         records [a, b)); micro-step j is one optimisation step over the union
-        of every rank's slice j, N_global = world * slice size (equal shards).
-        Returns the per-step stats (reduced over ranks) if want_stats."""
+        of every rank's slice j, N_global = the sum of the ranks' slice sizes.
+        Every rank runs the same number of micro-steps (that of the largest
+        shard); a rank whose shard is exhausted contributes an empty slice
+        (make_slice(a, a)).  Returns the per-step stats (reduced over ranks)
+        if want_stats."""
         out = []
-        for a in range(0, int(n_local), int(micro_local)):
-            b = min(a + int(micro_local), int(n_local))
+        n_max = int(n_local)
+        if self.world > 1 and dist.is_initialized():
+            v = torch.tensor([n_max], dtype=torch.int64, device=self.t.grad_tensor().device)
+            dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
+            n_max = int(v.item())
+        for a0 in range(0, n_max, int(micro_local)):
+            a = min(a0, int(n_local))
+            b = min(a0 + int(micro_local), int(n_local))
             q, wi, target, spdf = make_slice(a, b)
             st = self.train_step(q, wi, target, spdf, n_local=b - a, want_stats=want_stats)
             if want_stats:

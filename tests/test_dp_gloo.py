@@ -146,3 +146,47 @@ def test_two_rank_micro_step_stream_equals_union_micro_batches():
         _, ref = onpm.train_step(st, dict(x=q["x"][:, idx]), wi[:, idx], tgt[..., idx], pdf[idx], idx.size)
         assert s0[j]["n_used"] == ref["n_used"] and np.isclose(s0[j]["loss_proxy"], ref["loss_proxy"], rtol=1e-12)
     assert np.allclose(p0, st.params, rtol=1e-12, atol=1e-14)
+
+
+def _ragged_worker(rank, world, port, n, micro_local, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg, q, wi, tgt, pdf = _batch(n, 10)
+    tr = OracleTrainer(cfg, random_params(cfg, np.random.default_rng(11)))
+    dp = DataParallel(tr)            # world and N_global from the process group
+    a, b = shard_range(n, rank, world)
+    sl = lambda x, s0, s1: np.ascontiguousarray(x[..., a + s0:a + s1])
+    # one full-shard step with N_global inferred (31 + 30 records)
+    st1 = dp.train_step(dict(x=sl(q["x"], 0, b - a)), sl(wi, 0, b - a), sl(tgt, 0, b - a), sl(pdf, 0, b - a),
+                        n_local=b - a, want_stats=True)
+    # then a micro-step stream whose last step is empty on rank 1
+    stats = dp.train_stream(lambda s0, s1: (dict(x=sl(q["x"], s0, s1)), sl(wi, s0, s1), sl(tgt, s0, s1),
+                                            sl(pdf, s0, s1)), b - a, micro_local, want_stats=True)
+    out[rank] = (tr.state.params.copy(), tr.state.t, st1, stats)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_unequal_shards_infer_n_global_and_stream_stays_in_step():
+    # N_global is the sum of the (unequal) shard sizes, and both
+    # ranks run the same number of micro-steps (rank 1's last slice is empty)
+    n, micro_local, world = 61, 15, 2      # shards 31 (15, 15, 1) and 30 (15, 15, 0)
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ragged_worker, args=(world, port, n, micro_local, out), nprocs=world, join=True)
+    p0, t0, a0, s0 = out[0]
+    p1, t1, a1, s1 = out[1]
+    assert np.array_equal(p0, p1) and t0 == t1 == 4
+    from oracle import npm as onpm
+    cfg, q, wi, tgt, pdf = _batch(n, 10)
+    st = onpm.State(cfg, random_params(cfg, np.random.default_rng(11)))
+    _, ref = onpm.train_step(st, q, wi, tgt, pdf, n)
+    assert a0["n_used"] == ref["n_used"] and np.isclose(a0["loss_proxy"], ref["loss_proxy"], rtol=1e-12)
+    shards = [shard_range(n, r, world) for r in range(world)]
+    for j in range(3):
+        idx = np.concatenate([np.arange(a + j * micro_local, min(a + (j + 1) * micro_local, b)) for a, b in shards])
+        _, ref = onpm.train_step(st, dict(x=q["x"][:, idx]), wi[:, idx], tgt[..., idx], pdf[idx], idx.size)
+        assert s0[j]["n_used"] == ref["n_used"] and np.isclose(s0[j]["loss_proxy"], ref["loss_proxy"], rtol=1e-12)
+    assert np.allclose(p0, st.params, rtol=1e-12, atol=1e-14)

@@ -1,0 +1,112 @@
+"""A11 on the CUDA path with more than one rank (VERDICT r1 "missing" #1,
+ADVICE r1): two processes on cuda:0, each holding its own C-ABI model
+(npm.Model), joined by a gloo process group.  DataParallel (dp.py) shards a
+c2-shaped record batch contiguously (ragged: n odd), every rank runs Eq. 9 ->
+backprop -> scatter into its library GRADS buffer with 1/N_global, and the one
+exchange step -- all_reduce(SUM) of the zero-copy GRADS view (BASELINE
+north_star) -- runs over gloo on the CUDA tensor.
+
+Checks: after the exchange the gradient equals the float64 oracle's gradient
+of the UNION batch (rel-L2 2e-3, whole vector and per block); after two full
+optimisation steps the two replicas' parameters and EMA are bitwise
+identical.  (NCCL refuses two ranks on one device, and only 1-GPU boxes are
+available, so the native-communicator path is covered at world size 1 in
+test_gpu_pipeline.py; the reduction it performs is the same SUM.)"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+N = 20001
+NAME = "c2"
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _inputs():
+    from workloads import synth
+    from workloads.configs import CONFIGS
+    from tests.helpers import oracle_config
+    ocfg = oracle_config(NAME)
+    p = synth.random_params(ocfg.layer_dims, ocfg.n_grid, ocfg.n_lobes, seed=61)
+    b = synth.training_batch(N, seed=62, rgb=True, nan_rate=1e-3)
+    b2 = synth.training_batch(N, seed=63)
+    return CONFIGS[NAME]["model"], ocfg, p, b, b2
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2504_04315_b200 import npm
+    from paper_2504_04315_b200.dp import DataParallel, shard_range
+    model_cfg, ocfg, p, b, b2 = _inputs()
+    m = npm.Model(0, **model_cfg)
+    m.set(npm.BUF_PARAMS, p)
+    m.set(npm.BUF_EMA, p)
+    dp = DataParallel(m)
+    assert dp.world == world and dp.reduce
+    a, e = shard_range(N, rank, world)
+
+    def shard(bb):
+        dev = lambda x: torch.from_numpy(np.ascontiguousarray(x[..., a:e])).cuda()
+        return m.query(np.ascontiguousarray(bb["x"][:, a:e])), dev(bb["wi"]), dev(bb["target"]), dev(bb["pdf"])
+
+    # step 1 by hand, to read the exchanged gradient before Adam zeroes it
+    q, wi, tgt, pdf = shard(b)
+    st = dp.t.accumulate(q, wi, tgt, pdf, dp.global_count(e - a), True)
+    dp.allreduce_grads()
+    g = m.get(npm.BUF_GRADS).cpu().numpy()
+    dp.t.optimizer_step(False)
+    # step 2 through the driver
+    q2, wi2, tgt2, pdf2 = shard(b2)
+    dp.train_step(q2, wi2, tgt2, pdf2, n_local=e - a)
+    torch.cuda.synchronize()
+    out[rank] = (g, m.get(npm.BUF_PARAMS).cpu().numpy(), m.get(npm.BUF_EMA).cpu().numpy(), st["n_used"])
+    dist.barrier()
+    m.close()
+    dist.destroy_process_group()
+
+
+def test_two_rank_cuda_allreduce_matches_union_batch_and_replicas_identical():
+    from oracle import npm as onpm
+    from tests.helpers import rel_l2
+    from tests.test_gpu_parity import grad_blocks
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    g0, p0, e0, u0 = out[0]
+    g1, p1, e1, u1 = out[1]
+    # every rank holds the same reduced bytes ...
+    assert np.array_equal(g0, g1)
+    # ... the oracle's union-batch gradient (C-A13: each rank scaled by 1/N_global)
+    _, ocfg, p, b, _ = _inputs()
+    og, ost = onpm.gradient(ocfg, p.astype(np.float64), dict(x=b["x"]), b["wi"].astype(np.float64),
+                            b["target"].astype(np.float64), b["pdf"].astype(np.float64), N)
+    g = g0.astype(np.float64)
+    assert rel_l2(g, og) <= 2e-3
+    for kind, a, e in grad_blocks(ocfg):
+        if np.linalg.norm(og[a:e]) > 0:
+            assert rel_l2(g[a:e], og[a:e]) <= 2e-3, (kind, a, e)
+    assert u0 + u1 == ost["n_used"]
+    # replicas bitwise identical after two optimisation steps
+    assert np.array_equal(p0, p1) and np.array_equal(e0, e1)
+    assert not np.array_equal(p0, p)      # and they did move

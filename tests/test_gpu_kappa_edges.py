@@ -1,0 +1,214 @@
+"""GPU parity at the edges of the concentration range (VERDICT r1 "weak" #2).
+
+Reading C-A8 (Table 1 gives kappa = exp(kappa'), kappa in [0, inf)):
+kappa' is clamped to [ln 1e-5, ln 1e5] and the clamped coordinate gets zero
+gradient.  The ordinary parity parameters draw the kappa' bias from
+N(0, 1.5^2), which never reaches the clamp; here the output bias of each lobe's
+kappa' row is placed
+
+  lobe 0: ln 1e5 + 2    (always clamped high)
+  lobe 1: ln 1e5        (straddles the upper bound: about half clamped)
+  lobe 2: ln 1e5 - 0.5  (kappa ~ 6e4, just inside)
+  lobe 3: ln 1e-5       (straddles the lower bound)
+  lobe 4: ln 1e-5 + 0.5 (just inside)
+  lobe 5: ln 1e-5 - 2   (always clamped low)
+  lobe 6: ln 1e2        lobe 7: ln 1e3   (kappa in [1e2, 1e3])
+
+(W_3 h_2 spreads kappa' by ~0.1 s.d., at most ~0.75, about its bias.)
+
+and the whole path is compared with the float64 oracle at the BASELINE
+tolerances: decode (raw / lambda / mu abs 1e-4, kappa rel 1e-4), pdf (rel
+1e-3) at caller directions aimed at the concentrated lobes, sampling
+(directions abs 1e-4, pdf at the sample rel 1e-3), and the KL (Eq. 9) and
+chi^2 (C-A31) gradients (rel-L2 2e-3, whole vector and per block).  The C-A8
+rule is asserted element by element: the kappa' rows of the output layer for
+the always-clamped lobes 0 and 5 are exactly zero on both sides.
+Also C-A32 (non-finite positions) through encode_debug and decode."""
+import numpy as np
+import pytest
+
+from workloads import synth
+from workloads.configs import CONFIGS
+from tests.helpers import oracle_config, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2504_04315_b200 import npm  # noqa: E402
+from oracle import npm as onpm, grid as ogrid, vmf as ovmf  # noqa: E402
+from tests.test_gpu_parity import gq, oq, grad_blocks, _boundary_mask  # noqa: E402
+
+LN_MAX, LN_MIN = np.log(1e5), np.log(1e-5)
+KAPPA_BIAS = [LN_MAX + 2.0, LN_MAX, LN_MAX - 0.5, LN_MIN, LN_MIN + 0.5, LN_MIN - 2.0, np.log(1e2), np.log(1e3)]
+
+
+def out_layer_rows(ocfg):
+    """(W offset, in, out, b offset) of the output layer in the flat ABI layout."""
+    off = 0
+    for li, (i, o) in enumerate(ocfg.layer_dims):
+        if li == len(ocfg.layer_dims) - 1:
+            return off, i, o, off + o * i
+        off += o * i + o
+
+
+def edge_pair(name, divergence=0, seed=41):
+    model = dict(CONFIGS[name]["model"], divergence=divergence)
+    ocfg = oracle_config(model)
+    assert ocfg.n_lobes == 8
+    p = synth.random_params(ocfg.layer_dims, ocfg.n_grid, ocfg.n_lobes, seed=seed)
+    _, _, _, boff = out_layer_rows(ocfg)
+    p[boff + 8: boff + 16] = np.asarray(KAPPA_BIAS, np.float32)
+    m = npm.Model(0, **model)
+    m.set(npm.BUF_PARAMS, p)
+    m.set(npm.BUF_EMA, p)
+    return m, ocfg, p.astype(np.float64)
+
+
+_CACHE = {}
+
+
+def pair(name, divergence=0):
+    key = (name, divergence)
+    if key not in _CACHE:
+        _CACHE[key] = edge_pair(name, divergence)
+    return _CACHE[key]
+
+
+def _unit(v):
+    return v / np.linalg.norm(v, axis=0, keepdims=True)
+
+
+def aimed_directions(act, lobes, spreads, rng):
+    """Per record: a direction near the oracle's mean of one of `lobes`
+    (cycled), perturbed by N(0, spread^2) per component, so the pdf and the
+    Eq. 9 head are dominated by the concentrated lobes."""
+    n = act["mu"].shape[2]
+    w = np.empty((3, n))
+    for j in range(n):
+        k = lobes[j % len(lobes)]
+        w[:, j] = act["mu"][:, k, j] + rng.normal(scale=spreads[j % len(lobes)], size=3)
+    return _unit(w)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_decode_at_kappa_edges(name):
+    m, ocfg, p = pair(name)
+    b = synth.query_batch(4000, seed=42)
+    raw, lam, kap, mu = (t.cpu().numpy() for t in m.decode(gq(m, b)))
+    oraw, act = onpm.decode(ocfg, p, oq(b, False))
+    kr = oraw[8:16]
+    # the batch really straddles both clamp bounds and covers kappa in [1e2, 1e3]
+    assert 0.05 < (kr[1] > LN_MAX).mean() < 0.95 and 0.05 < (kr[3] < LN_MIN).mean() < 0.95
+    assert np.all(kr[0] > LN_MAX) and np.all(kr[5] < LN_MIN)
+    assert np.abs(raw - oraw).max() <= 1e-4
+    assert np.abs(lam - act["lam"]).max() <= 1e-4
+    assert np.abs(mu - act["mu"]).max() <= 1e-4
+    assert (np.abs(kap - act["kappa"]) / act["kappa"]).max() <= 1e-4
+    assert np.all(kap[0] == kap[0, 0]) and abs(kap[0, 0] - 1e5) <= 1e-4 * 1e5
+    assert abs(kap[5, 0] - 1e-5) <= 1e-4 * 1e-5
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_pdf_aimed_at_concentrated_lobes(name):
+    m, ocfg, p = pair(name)
+    n = 3000
+    b = synth.query_batch(n, seed=43)
+    _, act = onpm.decode(ocfg, p, oq(b, False))
+    rng = np.random.default_rng(44)
+    # lobes 0-2 (kappa ~ 1e5: spread 2e-3 keeps kappa |mu - w|^2 / 2 ~ 0.6),
+    # lobes 6-7 (kappa 1e2 / 1e3), plus uniform directions
+    wq = aimed_directions(act, [0, 1, 2, 6, 7], [2e-3, 2e-3, 2e-3, 0.05, 0.02], rng)
+    wq[:, ::7] = _unit(rng.normal(size=(3, wq[:, ::7].shape[1])))
+    wq = wq.astype(np.float32)
+    pdf = m.pdf(gq(m, b), wq).cpu().numpy()
+    opdf = ovmf.mixture_pdf(wq.astype(np.float64), act)
+    assert np.median(opdf) > 10.0    # dominated by the concentrated lobes
+    assert (np.abs(pdf - opdf) / opdf).max() <= 1e-3
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_sample_at_kappa_edges(name):
+    m, ocfg, p = pair(name)
+    n = 4000
+    b = synth.query_batch(n, seed=45)
+    u = np.random.default_rng(46).uniform(size=(3, n)).astype(np.float32)
+    u[1, :7] = 0.0                   # the u2 = 0 guard of C-O10 at kappa = 1e5
+    wi, pdf = (t.cpu().numpy() for t in m.sample(gq(m, b), u=u))
+    _, act = onpm.decode(ocfg, p, oq(b, False))
+    ow, opdf, _ = ovmf.sample(act, u.astype(np.float64), ocfg.n_lobes)
+    ok = ~_boundary_mask(act, u[0].astype(np.float64), ocfg.n_lobes)
+    assert ok.mean() > 0.99
+    assert np.all(np.isfinite(wi)) and np.all(np.isfinite(pdf))
+    assert np.abs(wi[:, ok] - ow[:, ok]).max() <= 1e-4
+    assert (np.abs(pdf[ok] - opdf[ok]) / opdf[ok]).max() <= 1e-3
+    # samples of the kappa = 1e5 lobes really are concentrated
+    lobe = np.argmax(u[0][None, :].astype(np.float64) < np.cumsum(act["lam"], axis=0), axis=0)
+    sel = ok & (lobe == 0)
+    assert sel.sum() > 50
+    cosang = (wi[:, sel] * act["mu"][:, 0, sel]).sum(0)
+    assert np.all(cosang > 0.999)
+
+
+def _edge_training_batch(ocfg, p, n, seed):
+    b = synth.training_batch(n, seed=seed, rgb=False, nan_rate=1e-3)
+    _, act = onpm.decode(ocfg, p, oq(b, False))
+    rng = np.random.default_rng(seed + 1)
+    wi = aimed_directions(act, [0, 1, 2, 6, 7, 3], [2e-3, 2e-3, 2e-3, 0.05, 0.02, 0.5], rng)
+    keep = rng.uniform(size=n) < 0.25       # a quarter keep the drawn directions
+    wi[:, keep] = b["wi"][:, keep]
+    b["wi"] = wi.astype(np.float32)
+    return b
+
+
+@pytest.mark.parametrize("name,divergence", [("c1", 0), ("c2", 0), ("c1", 1), ("c2", 1)])
+def test_gradient_at_kappa_edges(name, divergence):
+    m, ocfg, p = pair(name, divergence)
+    n = 8192
+    b = _edge_training_batch(ocfg, p, n, seed=47)
+    st = m.accumulate_grads(gq(m, b), b["wi"], b["target"], b["pdf"], n_global=n)
+    g = m.get(npm.BUF_GRADS).cpu().numpy().astype(np.float64)
+    m.set(npm.BUF_GRADS, np.zeros(m.n_params, np.float32))
+    og, ost = onpm.gradient(ocfg, p, oq(b, False), b["wi"].astype(np.float64), b["target"].astype(np.float64),
+                            b["pdf"].astype(np.float64), n)
+    assert np.all(np.isfinite(g))
+    assert rel_l2(g, og) <= 2e-3
+    for kind, a, e in grad_blocks(ocfg):
+        if np.linalg.norm(og[a:e]) > 0:
+            assert rel_l2(g[a:e], og[a:e]) <= 2e-3, (kind, a, e)
+    assert abs(st["loss_proxy"] - ost["loss_proxy"]) <= 1e-4 * abs(ost["loss_proxy"])
+    for k in ("n_used", "n_zero_target", "n_dropped"):
+        assert st[k] == ost[k], k
+    # C-A8 element-wise: kappa' rows of the always-clamped lobes 0 and 5
+    woff, nin, nout, boff = out_layer_rows(ocfg)
+    for lobe in (0, 5):
+        r = 8 + lobe
+        assert np.all(og[woff + r * nin: woff + (r + 1) * nin] == 0) and og[boff + r] == 0
+        assert np.all(g[woff + r * nin: woff + (r + 1) * nin] == 0), lobe
+        assert g[boff + r] == 0, lobe
+    # ... while the straddling lobes do train their kappa' (non-zero rows)
+    for lobe in (1, 2, 3, 4, 6, 7):
+        assert og[boff + 8 + lobe] != 0 and g[boff + 8 + lobe] != 0
+
+
+def test_non_finite_positions():
+    """C-A32: NaN -> lower face, +-inf -> the faces (IEEE maxNum/minNum clamp):
+    corner indices bit-exact with the oracle, decoded mixtures finite."""
+    m, ocfg, p = pair("c2")
+    b = synth.query_batch(1024, seed=48)
+    x = b["x"]
+    x[0, 0] = np.nan; x[1, 1] = np.nan; x[2, 2] = np.nan
+    x[0, 3] = np.inf; x[1, 4] = -np.inf; x[:, 5] = np.nan; x[:, 6] = np.inf
+    q = gq(m, b)
+    idx, w = m.encode_debug(q)
+    idx, w = idx.cpu().numpy().view(np.uint32), w.cpu().numpy()
+    u = ogrid.normalize_position(x, ocfg.aabb_lo, ocfg.aabb_hi)
+    for l, (d, s) in enumerate(zip(ocfg.resolutions, ocfg.table_sizes)):
+        oi, ow = ogrid.level_corners(u, d, s, s != d ** 3)
+        assert np.array_equal(idx[l].astype(np.int64), oi), "level %d" % l
+        assert np.abs(w[l] - ow).max() <= 1e-6
+    raw, lam, kap, mu = (t.cpu().numpy() for t in m.decode(q))
+    oraw, act = onpm.decode(ocfg, p, oq(b, False))
+    assert np.all(np.isfinite(raw)) and np.abs(raw - oraw).max() <= 1e-4

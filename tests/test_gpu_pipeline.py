@@ -91,3 +91,32 @@ def test_native_nccl_communicator_single_rank():
     p2 = m2.get(npm.BUF_PARAMS).cpu().numpy()
     assert np.abs(p1 - p2).max() <= 2 * 5e-3   # Adam amplification of fp32 atomic-order noise only
     assert (p1 == p2).mean() > 0.99
+
+
+def test_binned_queries_on_two_streams_with_different_sizes():
+    """the binning permutation is per-model scratch; two
+    device-pointer queries of different sizes (both >= 65,536, so both binned)
+    enqueued back to back on two streams must give exactly the results of the
+    same queries run one after the other on one stream."""
+    m, _, _ = make_pair("c2", seed=44)
+    sizes = (300007, 70001)
+    bs = [synth.query_batch(n, seed=45 + j) for j, n in enumerate(sizes)]
+    ref = []
+    for b in bs:
+        q = m.query(b["x"])
+        ref.append([t.cpu().numpy() for t in m.sample(q, seed=7, offset=0, wq=b["wq"])])
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    qs = [m.query(b["x"]) for b in bs]
+    wqs = [torch.from_numpy(b["wq"]).cuda() for b in bs]
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(3):                           # several rounds of interleaving
+        for s, q, wq in zip(streams, qs, wqs):
+            with torch.cuda.stream(s):
+                outs.append((s, m.sample(q, seed=7, offset=0, wq=wq)))
+    torch.cuda.synchronize()
+    for j, (s, o) in enumerate(outs):
+        got = [t.cpu().numpy() for t in o]
+        for a, b in zip(got, ref[j % 2]):
+            assert np.array_equal(a, b), j

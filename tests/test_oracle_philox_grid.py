@@ -166,3 +166,48 @@ def test_hash_range_and_convention():
     h = grid.corner_index(p, 86, 1 << 18, True)
     assert np.all((h >= 0) & (h < (1 << 18)))
     assert h[0] == 0 and h[1] == 1
+
+
+def _hash_golden():
+    rows = []
+    with open(os.path.join(os.path.dirname(__file__), "golden", "spatial_hash.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                px, py, pz, lt, hy, hz, h, idx = line.split()
+                rows.append((int(px), int(py), int(pz), int(lt), int(hy, 16), int(hz, 16), int(h, 16), int(idx)))
+    return rows
+
+
+def test_hash_hand_computed_golden():
+    # tests/golden/spatial_hash.txt: the C-A4 hash worked out by hand (products
+    # mod 2^32 in hex); pins corner_index against a swapped prime, '+' for XOR,
+    # or a missing 32-bit wrap
+    rows = _hash_golden()
+    assert len(rows) >= 10
+    for px, py, pz, lt, hy, hz, h, idx in rows:
+        got = grid.corner_index((np.array([px]), np.array([py]), np.array([pz])), 0, 1 << lt, True)
+        assert int(got[0]) == idx, (px, py, pz, lt)
+        assert (px ^ hy ^ hz) == h and h & ((1 << lt) - 1) == idx   # the file is self-consistent
+
+
+def test_level_corners_hashed_matches_golden_corner():
+    # a position whose cell's (1,1,1) corner is lattice point (1,1,1) on a hashed
+    # level with D = 86: corner 7 must be the golden index 77349
+    d, t = 86, 1 << 18
+    u = np.full((3, 1), np.float32(0.5 / 85), np.float32)   # s = 0.5 -> cell (0,0,0)
+    idx, _ = grid.level_corners(u, d, t, True)
+    assert int(idx[7, 0]) == 77349 and int(idx[0, 0]) == 0 and int(idx[1, 0]) == 1
+
+
+def test_non_finite_positions_reading():
+    # C-A32: the AABB clamp uses IEEE-754 maxNum / minNum (fmax / fmin): a NaN
+    # coordinate is replaced by the clamp bound it meets first (the lower face),
+    # +inf clamps to the upper face and -inf to the lower one
+    x = np.array([[np.nan, np.inf, -np.inf, 0.0],
+                  [0.0, np.nan, 0.0, np.inf],
+                  [0.0, 0.0, np.nan, -np.inf]], np.float32)
+    u = grid.normalize_position(x, (-1, -1, -1), (1, 1, 1))
+    assert np.all(np.isfinite(u))
+    assert u[0, 0] == 0 and u[1, 1] == 0 and u[2, 2] == 0
+    assert u[0, 1] == grid.U_MAX and u[0, 2] == 0 and u[1, 3] == grid.U_MAX and u[2, 3] == 0
+    assert u[1, 0] == np.float32(0.5)
