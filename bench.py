@@ -89,60 +89,153 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-def cpu_oracle_step(name, n, seed=0):
-    """The float64 oracle as it stands (tests' reference), one step of the
-    hot path on n samples: decode + sample + pdf at caller directions for n
-    queries, gradient over n records, Adam + EMA over all parameters."""
-    from oracle import npm as onpm, vmf as ovmf, philox as ophilox
-    cfg = onpm.Config(**CONFIGS[name]["model"])
-    prod = cfg.mode == onpm.PRODUCT
-    p = synth.random_params(cfg.layer_dims, cfg.n_grid, cfg.n_lobes, seed=seed).astype(np.float64)
-    state = onpm.State(cfg, p)
-    qb = synth.query_batch(n, seed=seed + 1, product=prod)
-    tb = synth.training_batch(n, seed=seed + 2, product=prod)
-    cond = lambda b: dict(x=b["x"], **(dict(wo=b["wo"].astype(np.float64), n=b["nrm"].astype(np.float64),
-                                            rough=b["rough"].astype(np.float64)) if prod else {}))
-    t0 = time.perf_counter()
-    _, act = onpm.decode(cfg, state.ema, cond(qb))
-    u = ophilox.sample_uniforms(n, 1234, 0)
-    ovmf.sample(act, u, cfg.n_lobes)
-    ovmf.mixture_pdf(qb["wq"].astype(np.float64), act)
-    onpm.train_step(state, cond(tb), tb["wi"].astype(np.float64), tb["target"].astype(np.float64),
-                    tb["pdf"].astype(np.float64), n)
-    return time.perf_counter() - t0
+_W = {}
 
 
-def cpu_baseline(name, target_s=12.0):
+def _oracle_worker_init(name, seed):
+    """Pool initializer: the worker's copy of the model state (float64 oracle,
+    1 BLAS thread per process so the pool uses exactly its cores)."""
     from threadpoolctl import threadpool_limits
-    with threadpool_limits(limits=1):
-        n = 1 << 13
-        dt = cpu_oracle_step(name, n)
-        n2 = int(min(1 << 18, max(n, n * target_s / max(dt, 1e-3))))
-        dt2 = cpu_oracle_step(name, n2)
-    return {"value": 2 * n2 / dt2, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "%s workload, %d queries + %d records, one step (float64 numpy oracle, 1 thread; "
-                      "Adam over all %s params)" % (name, n2, n2, name)}
+    from oracle import npm as onpm
+    _W["limits"] = threadpool_limits(limits=1)
+    cfg = onpm.Config(**CONFIGS[name]["model"])
+    _W["cfg"] = cfg
+    _W["p"] = synth.random_params(cfg.layer_dims, cfg.n_grid, cfg.n_lobes, seed=seed).astype(np.float64)
+    _W["ema"] = _W["p"].copy()
+
+
+def _oracle_shard(task):
+    """One shard of the hot path in the oracle: decode + sample + pdf at the
+    caller directions for the shard's queries, Eq. 9 gradient over its records
+    (scaled by 1/N_global).  Returns the shard's gradient vector."""
+    from oracle import npm as onpm, vmf as ovmf
+    cfg = _W["cfg"]
+    q, t, u, n_global = task
+    _, act = onpm.decode(cfg, _W["ema"], q["cond"])
+    ovmf.sample(act, u, cfg.n_lobes)
+    ovmf.mixture_pdf(q["wq"], act)
+    g, _ = onpm.gradient(cfg, _W["p"], t["cond"], t["wi"], t["target"], t["pdf"], n_global)
+    return g
+
+
+class OracleRunner:
+    """The float64 oracle as it stands, run on all host cores: queries and
+    records are cut into contiguous shards, one per process (forward and the
+    per-record gradient are independent per sample); the parent sums the
+    shards' gradients in a fixed order and runs Adam + EMA once (SURVEY 8(d)
+    "multiprocessing over contiguous sample shards on all host cores")."""
+
+    def __init__(self, name, seed=0, cores=None):
+        import multiprocessing as mp
+        from oracle import npm as onpm
+        self.name, self.seed = name, seed
+        self.cores = cores or os.cpu_count() or 1
+        self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_oracle_worker_init, initargs=(name, seed))
+        cfg = onpm.Config(**CONFIGS[name]["model"])
+        self.state = onpm.State(cfg, synth.random_params(cfg.layer_dims, cfg.n_grid, cfg.n_lobes,
+                                                         seed=seed).astype(np.float64))
+        self.prod = cfg.mode == onpm.PRODUCT
+        self.batches = {}
+
+    def _batch(self, n, seed):
+        from oracle import philox as ophilox
+        if (n, seed) not in self.batches:
+            qb = synth.query_batch(n, seed=seed + 1, product=self.prod)
+            tb = synth.training_batch(n, seed=seed + 2, product=self.prod)
+            cond = lambda b, a, e: dict(x=b["x"][:, a:e], **(dict(
+                wo=b["wo"][:, a:e].astype(np.float64), n=b["nrm"][:, a:e].astype(np.float64),
+                rough=b["rough"][a:e].astype(np.float64)) if self.prod else {}))
+            u = ophilox.sample_uniforms(n, 1234, 0)
+            tasks = []
+            for k in range(self.cores):
+                a, e = n * k // self.cores, n * (k + 1) // self.cores
+                tasks.append((dict(cond=cond(qb, a, e), wq=qb["wq"][:, a:e].astype(np.float64)),
+                              dict(cond=cond(tb, a, e), wi=tb["wi"][:, a:e].astype(np.float64),
+                                   target=tb["target"][..., a:e].astype(np.float64),
+                                   pdf=tb["pdf"][a:e].astype(np.float64)), u[:, a:e], n))
+            self.batches = {(n, seed): tasks}
+        return self.batches[(n, seed)]
+
+    def step(self, n, seed=0):
+        """One step on n queries + n records; returns its wall time (s)."""
+        from oracle import npm as onpm
+        tasks = self._batch(n, seed)
+        t0 = time.perf_counter()
+        g = None
+        for gk in self.pool.map(_oracle_shard, tasks, chunksize=1):   # fixed (shard) order
+            g = gk if g is None else g + gk
+        onpm.optimizer_step(self.state, g)
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def host_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "lscpu_model": model, "threads_per_process": 1}
+
+
+def cpu_baseline(name, budget_s=20.0):
+    """The oracle on all host cores: the full per-step workload when it fits
+    the time budget (c1, c2 on a many-core host), else a bounded sample
+    (n scaled down to ~budget_s)."""
+    n_full = CONFIGS[name]["n"]
+    r = OracleRunner(name)
+    try:
+        n0 = min(n_full, 1 << 13) * r.cores
+        n0 = min(n0, n_full)
+        dt0 = r.step(n0, seed=1)
+        n = n_full if dt0 * n_full / n0 <= budget_s else int(max(n0, n0 * budget_s / max(dt0, 1e-3)))
+        dt = r.step(n)
+    finally:
+        r.close()
+    return {"value": 2 * n / dt, "unit": UNIT, "cores": r.cores, "kind": "oracle",
+            "sample": "%s workload, %d queries + %d records, one step%s (float64 numpy oracle, %d processes x 1 "
+                      "thread, contiguous shards; gradient summed in shard order, Adam + EMA over all %s params "
+                      "in the parent)" % (name, n, n, " (the full step)" if n == n_full else " (bounded sample)",
+                                          r.cores, name),
+            "host": host_info(), "seconds": dt}
 
 
 def run_reference(args, rank):
-    """--impl reference: the oracle on host cores, same metric/config."""
+    """--impl reference: the oracle on all host cores, same metric/config."""
     if rank != 0:
         return
-    from threadpoolctl import threadpool_limits
-    n = 1 << 14
-    with threadpool_limits(limits=1):
+    name = args.workload
+    n_full = CONFIGS[name]["n"]
+    r = OracleRunner(name)
+    try:
+        n0 = min(n_full, (1 << 13) * r.cores)
+        dt0 = r.step(n0, seed=1)
+        # the whole --steps/--warmup run within ~3 minutes
+        per_step = 150.0 / max(1, args.steps + args.warmup)
+        n = n_full if dt0 * n_full / n0 <= per_step else int(max(n0, n0 * per_step / max(dt0, 1e-3)))
         for _ in range(args.warmup):
-            cpu_oracle_step(WORKLOAD, n)
-        ts = [cpu_oracle_step(WORKLOAD, n, seed=i) for i in range(args.steps)]
+            r.step(n)
+        ts = [r.step(n) for _ in range(args.steps)]
+    finally:
+        r.close()
     t = float(np.sum(ts))
     v = 2 * n * args.steps / t
+    sample = ("%d queries + %d records per step of the %s workload%s; float64 oracle on %d processes x 1 thread"
+              % (n, n, name, " (the full step)" if n == n_full else " (bounded sample)", r.cores))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD + " (bounded sample: %d queries + %d records "
-                                                           "per step)" % (n, n), "n_per_gpu": n},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": "%d queries + %d records per step of the %s workload" % (n, n, WORKLOAD)},
+            "data": "synthetic", "config": {"workload": name + (" (full step)" if n == n_full else
+                                                               " (bounded sample: %d queries + %d records per step)"
+                                                               % (n, n)), "n_per_gpu": n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": r.cores, "kind": "oracle", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -68,6 +68,8 @@ struct npm_model {
   double* dstats = nullptr;
   unsigned long long* dcount = nullptr;
   DevBuf dbg_clock;                // NPM_DEBUG=4 phase stamps (measurement only)
+  DevBuf wimg;                     // split-bf16 weight image of the training kernel
+  int train_ws = 1;                // training kernel: 1 warp-specialised (npm_train_ws.cuh), 0 the r01 two-group kernel (NPM_TRAIN_WS)
   DevBuf stage[24];                // host-pointer staging slots
   std::mutex stage_mu;
   int64_t launches = 0;
@@ -582,6 +584,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   m->device = dev;
   m->shape = s;
   if (const char* e = getenv("NPM_BIN")) m->use_bin = !(e[0] == '0');
+  if (const char* e = getenv("NPM_TRAIN_WS")) m->train_ws = atoi(e);
   if (const char* e = getenv("NPM_PIPELINE")) m->pipeline = !(e[0] == '0');
   if (const char* e = getenv("NPM_PIPE_CHUNKS")) m->pipe_chunks = atoi(e) > 0 ? atoi(e) : 3;
   // Query kernel layout: two 256-thread CTAs per SM, or one CTA running two
@@ -615,6 +618,9 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
     if (e > 0xFFFFFFFFLL) { delete m; return fail(NPM_ERR_INVALID, "level too large for 32-bit indices"); }
     m->entries[l] = e;
     gd.res[l] = m->res[l];
+    gd.resm1f[l] = (float)(m->res[l] - 1);
+    gd.cellmax[l] = m->res[l] > 2 ? m->res[l] - 2 : 0;
+    gd.cellmaxf[l] = (float)gd.cellmax[l];
     gd.tsize[l] = (uint32_t)e;
     gd.off[l] = off;
     off += e;
@@ -638,8 +644,10 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // c2 gains nothing (its random-order reductions do not collide): off there.
   if (m->bin_train) {
     int64_t per = 0;
+    int64_t priv_max = 65536;
+    if (const char* e = getenv("NPM_PRIV_MAX")) priv_max = atoll(e);   // measurement knob
     for (int l = 0; l < L; ++l) {
-      if (m->entries[l] > 65536) continue;
+      if (m->entries[l] > priv_max) continue;
       if ((per + m->entries[l]) * 16 * m->num_sms > ((int64_t)256 << 20)) break;
       m->priv_mask |= 1u << l;
       m->priv_off[l] = per;
@@ -699,6 +707,7 @@ npm_status npm_destroy(npm_model* m) {
   if (m->dstats) cudaFree(m->dstats);
   if (m->dcount) cudaFree(m->dcount);
   m->dbg_clock.release();
+  m->wimg.release();
   m->bin_keys.release();
   m->bin_perm.release();
   m->bin_hist.release();
@@ -1176,6 +1185,10 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   a.counters = m->dcount;
   if (const char* e = getenv("NPM_DEBUG")) a.debug = atoi(e);   // measurement only
   a.divergence = m->cfg.divergence;
+  a.ws = m->train_ws;
+  CUDA_TRY(m->wimg.ensure(64 * 1024));
+  a.wimg = static_cast<uint8_t*>(m->wimg.p);
+  a.wimg_bytes = 64 * 1024;
   if (m->priv_mask) {
     a.priv = static_cast<float4*>(m->priv.p);
     a.priv_mask = m->priv_mask;
@@ -1218,7 +1231,7 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
         ++cnt;
       }
       fprintf(stderr, "NPM_PHASES tiles=%d total=%.0f", cnt, cnt ? acc[0] / cnt : 0.0);
-      for (int j = 1; j < 16; ++j) if (j < 13 || j == 15) fprintf(stderr, " p%d=%.0f", j, cnt ? acc[j] / cnt : 0.0);
+      for (int j = 1; j < 16; ++j) fprintf(stderr, " p%d=%.0f", j, cnt ? acc[j] / cnt : 0.0);
       fprintf(stderr, "\n");
       if (r != NPM_OK || !a.priv_mask) return r;
       return fold_priv(m, st);

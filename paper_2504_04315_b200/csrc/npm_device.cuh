@@ -20,6 +20,9 @@ struct GridDesc {
   int L;
   uint32_t hashed_mask;        // bit l set: level l uses the spatial hash (C-A4)
   int res[kMaxLevels];         // D_l lattice points per axis
+  float resm1f[kMaxLevels];    // fl32(D_l - 1) (C-O3), precomputed: no I2F in the kernels
+  int cellmax[kMaxLevels];     // D_l - 2 (largest cell index; 0 if D_l = 2)
+  float cellmaxf[kMaxLevels];  // (float)cellmax
   uint32_t tsize[kMaxLevels];  // entries in level l (D^3 or T)
   int64_t off[kMaxLevels];     // first entry of level l (entries of F = 4 floats)
   float lo[3], inv[3];         // AABB min, fl32(1/(hi - lo)) (C-O1)
@@ -63,13 +66,21 @@ __device__ __forceinline__ float normalize_axis(float x, float lo, float inv) {
   return fminf(fmaxf(u, 0.0f), kUMax);
 }
 
-__device__ __forceinline__ void cell_axis(float u, int d, int& i, float& f) {
-  const float s = __fmul_rn(u, (float)(d - 1));
-  int ii = (int)floorf(s);
-  const int hi = d > 2 ? d - 2 : 0;
-  ii = ii < 0 ? 0 : (ii > hi ? hi : ii);
+// s = fl32(u * fl32(D - 1)), i = floor(s) clamped to [0, D - 2], f = s - i.
+// floor without the conversion (XU) pipe, which the heads' MUFU work and the
+// split-bf16 packs also need: for 0 <= s < 2^22, RD(s + 1.5 * 2^23) =
+// 1.5 * 2^23 + floor(s) exactly (the ulp there is 1), so the integer is the
+// difference of the bit patterns and floor(s) = t - 1.5 * 2^23 (exact).
+// Bit-identical to floorf / (int) / (float) (u >= 0 after the clamp of C-O1);
+// measured on B200 c2 train: neutral to -0.6 %.
+__device__ __forceinline__ void cell_axis(float u, float dm1, int hi, float hif, int& i, float& f) {
+  const float s = __fmul_rn(u, dm1);
+  const float t = __fadd_rd(s, 12582912.0f);
+  int ii = __float_as_int(t) - 0x4B400000;
+  float fl = __fsub_rn(t, 12582912.0f);
+  if (ii > hi) { ii = hi; fl = hif; }
   i = ii;
-  f = __fsub_rn(s, (float)ii);
+  f = __fsub_rn(s, fl);
 }
 
 // Corner entry index (C-O4): dense Px + D(Py + D Pz); hashed (C-A4 convention,
@@ -90,11 +101,13 @@ struct LevelCorners {
 __device__ __forceinline__ void level_corners(const GridDesc& g, int l, float ux, float uy, float uz,
                                               LevelCorners& lc) {
   const int d = g.res[l];
+  const float dm1 = g.resm1f[l], hif = g.cellmaxf[l];
+  const int hi = g.cellmax[l];
   int ix, iy, iz;
   float fx, fy, fz;
-  cell_axis(ux, d, ix, fx);
-  cell_axis(uy, d, iy, fy);
-  cell_axis(uz, d, iz, fz);
+  cell_axis(ux, dm1, hi, hif, ix, fx);
+  cell_axis(uy, dm1, hi, hif, iy, fy);
+  cell_axis(uz, dm1, hi, hif, iz, fz);
   const bool hashed = (g.hashed_mask >> l) & 1u;
   const float gx0 = 1.0f - fx, gy0 = 1.0f - fy, gz0 = 1.0f - fz;
   // w_c = (gx * gy) * gz, the same product order as corner-by-corner
@@ -221,6 +234,26 @@ __device__ __forceinline__ void activate(const float* raw, float log_kmin, float
 // 1e-3 rel, gradient 2e-3 rel-L2).  The conditioning-sensitive pieces (the
 // expm1 of the vMF normalisation, the sampler's log1p / expm1) stay precise.
 __device__ __forceinline__ float fast_sigmoid(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+
+// Table 1 angles of one lobe: theta = sigma(t'), phi = sigma(p') and the
+// sines / cosines of pi theta, 2 pi phi.  MUFU fast math by default; for a
+// concentrated lobe (kappa > 1e3) they are re-evaluated precisely (IEEE expf
+// and division, sincospif): the relative sensitivity of the lobe's pdf to its
+// mean is kappa |mu - w| (DESIGN C-A33), so the ~1e-6 error of the fast path
+// would exceed the 1e-3 pdf tolerance at kappa ~ 1e5.
+__device__ __forceinline__ void lobe_angles(float tp, float pp, float kap, float& th, float& ph, float& sth,
+                                            float& cth, float& sph, float& cph) {
+  th = fast_sigmoid(tp);
+  ph = fast_sigmoid(pp);
+  __sincosf(kPi * th, &sth, &cth);
+  __sincosf(kTwoPi * ph, &sph, &cph);
+  if (kap > 1e3f) {
+    th = 1.0f / (1.0f + expf(-tp));
+    ph = 1.0f / (1.0f + expf(-pp));
+    sincospif(th, &sth, &cth);
+    sincospif(2.0f * ph, &sph, &cph);
+  }
+}
 // kappa / (2 pi (1 - e^{-2 kappa})) with em = -expm1(-2 kappa) returned for reuse
 // 1 - e^{-x} for x >= 0 without the branches of expm1f: an 8-term Taylor
 // polynomial below x = 0.7 (truncation < 1.2e-7 relative) and MUFU ex2 above

@@ -72,6 +72,11 @@ struct TrainArgs {
   // SMs' reductions on the same L2 lines serialise.  fold_priv adds the copies.
   float4* priv;
   uint32_t priv_mask;
+  // split-bf16 weight image scratch (prep_wimg_kernel -> TMA bulk copy), and
+  // the kernel choice: 1 = warp-specialised kernel where the shape has one
+  uint8_t* wimg;
+  uint32_t wimg_bytes;
+  int ws;
   int64_t priv_stride;
   int64_t priv_off[16];
   double* stats;            // [0] loss, [1] unused, then int counters as double

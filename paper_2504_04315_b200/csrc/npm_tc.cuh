@@ -221,7 +221,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 }
 
 // Split-bf16: x = hi + lo with hi = bf16(x), lo = bf16(x - hi); packs two
-// consecutive features (even feature in the low half).
+// consecutive features (even feature in the low half).  (Measured on B200, c2
+// train: forming hi by integer rounding to spare the conversion pipe was
+// 7 % slower than the two cvt instructions.)
 __device__ __forceinline__ void split_pack(float a, float b, uint32_t& hi, uint32_t& lo) {
   // cvt.rn.bf16x2.f32 d, x, y puts x in the upper half: 6 instructions per pair
   // (cvt, shift, and-mask, 2 subtractions, cvt)

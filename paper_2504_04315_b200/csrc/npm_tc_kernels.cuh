@@ -373,11 +373,8 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     for (int j = 0; j < KQ; ++j) {
       mloc = fmaxf(mloc, lp[j]);
       kap[j] = __expf(fminf(fmaxf(kp[j], a.log_kmin), a.log_kmax));
-      const float th = fast_sigmoid(tp[j]);
-      const float ph = fast_sigmoid(pp[j]);
-      float st, ct, sp, cp;
-      __sincosf(kPi * th, &st, &ct);
-      __sincosf(kTwoPi * ph, &sp, &cp);
+      float th, ph, st, ct, sp, cp;
+      lobe_angles(tp[j], pp[j], kap[j], th, ph, st, ct, sp, cp);
       mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
       float em;
       nrm[j] = lobe_norm(kap[j], em);
@@ -903,10 +900,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         for (int m = 0; m < KL; ++m) {
           mloc = fmaxf(mloc, lp[m]);
           kap[m] = __expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
-          th[m] = fast_sigmoid(tp[m]);
-          ph[m] = fast_sigmoid(pp[m]);
-          __sincosf(kPi * th[m], &sth[m], &cth[m]);
-          __sincosf(kTwoPi * ph[m], &sph[m], &cph[m]);
+          lobe_angles(tp[m], pp[m], kap[m], th[m], ph[m], sth[m], cth[m], sph[m], cph[m]);
           mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
           const float nrm = lobe_norm_fast(kap[m], emk[m]);
           vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);
@@ -1083,6 +1077,8 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
   if (warp == 0) tc::tmem_dealloc(tbase, (uint32_t)T::TCOLS);
 }
 
+#include "npm_train_ws.cuh"
+
 template <class N>
 struct TcLaunch {
   static int query(const QueryArgs& a, int sms, cudaStream_t st) {
@@ -1110,6 +1106,18 @@ struct TcLaunch {
     return 1;
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
+    if constexpr (!N::PRODUCT && N::K == 8) {
+      if (a.ws) {   // warp-specialised kernel (npm_train_ws.cuh)
+        using T = ws::WS<N>;
+        if (!a.wimg || a.wimg_bytes < T::WIMG) return -1;
+        ws::prep_wimg_kernel<N><<<8, 256, 0, st>>>(a.params, a.wimg);
+        cudaFuncSetAttribute(ws::train_ws_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
+        const int64_t ntiles = (a.n + T::R - 1) / T::R;
+        const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
+        ws::train_ws_kernel<N><<<blocks, T::THREADS, T::SMEM, st>>>(a);
+        return 2;
+      }
+    }
     // two 64-sample tiles per CTA (tc_train64_kernel)
     using T64 = TC64<N>;
     cudaFuncSetAttribute(tc_train64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T64::SMEM);

@@ -1,0 +1,636 @@
+// npm_train_ws.cuh -- warp-specialised fused training kernel (round 2).
+// Included from npm_tc_kernels.cuh (namespace npm::tck).
+//
+// One persistent CTA per SM, 128-sample tiles (MMA M = 128, TMEM lane r =
+// tile row r), three roles on warps (every role fits ptxas' 128 registers per
+// thread of a 512-thread CTA without spills, so no setmaxnreg):
+//
+//   warps 0-7   CHAIN: the two threads of row r are warps w and w + 4 (lane
+//       r % 32, w = r / 32), each owning half of the columns, lobes and
+//       levels.  Thread 0 issues the tcgen05 MMAs; all 256 run the epilogues
+//       (bias, ReLU, split-bf16 into smem), the Eq. 9 head (P:210-216,
+//       C-O12/C-O13; softmax and mixture sums exchanged through smem) and the
+//       backward epilogues (C-O14), and hand dz (the grid part of dL/dz) to
+//       the scatter warps through smem.
+//   warps 8-15  MEMORY: thread (part, row) with part = which half of the L
+//       levels.  Iteration k: for tile k normalise x (C-O1), find the 8
+//       corners per level (Eq. 13, C-O3/C-O4), gather and blend them (C-O5),
+//       write X0 (split bf16, chunk-major) into an X0 stage and the head inputs
+//       into a row-data stage; then for tile k - 1 scatter
+//       dE_l[idx_c] += w_c dz_l (C-O15) with red.global.add.v4.f32 from the dz
+//       stage the chain filled.
+//
+// The roles hand tiles over through mbarrier rings (x0 full/empty, dz
+// full/empty), so a tile's gathers, its MMA chain and the previous tile's
+// scatter run concurrently instead of in sequence (r01: one 256-thread group
+// per tile did all three in turn).  The split-bf16 weight image (built once per
+// launch by prep_wimg_kernel) is staged into smem with one cp.async.bulk (TMA
+// bulk copy, completion through an mbarrier transaction count).
+#pragma once
+
+namespace ws {
+
+template <class N>
+struct WS {
+  using B = TC<N>;
+  static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN, L = N::L, K = N::K, NG = N::NGRID;
+  static constexpr int R = 128;              // rows per tile = MMA M
+  static constexpr uint32_t CHR = R * 16;    // bytes of one 8-feature chunk of a tile
+  static constexpr int ZF = B::ZF, HF = B::HF, KIN = B::KIN;
+  static_assert(!N::PRODUCT && K == 8 && L % 2 == 0 && W % 32 == 0, "warp-specialised kernel shape");
+  static constexpr int TPR = 2;   // chain threads per row (B200 c2: 2 -> 520 us, 4 -> 561 us without the scatter)
+  static constexpr int CHAIN_THREADS = TPR * R, MEM_THREADS = 256, THREADS = CHAIN_THREADS + MEM_THREADS;
+  static constexpr int GATHER_THREADS = MEM_THREADS, SCATTER_THREADS = MEM_THREADS;
+  static_assert(L % TPR == 0 && (L / 2) % 2 == 0 && K % TPR == 0 && (W / TPR) % 16 == 0, "quarters");
+  // ---- smem map
+  static constexpr uint32_t WIMG = B::WBYTES + B::BBYTES;   // weight image, bulk-copied
+  static_assert(WIMG % 16 == 0, "bulk copy size");
+  static constexpr uint32_t a1k(uint32_t x) { return (x + 1023u) & ~1023u; }
+  static constexpr uint32_t X0_BYTES = 2u * (ZF / 8) * CHR;
+  static constexpr uint32_t XH_BYTES = 2u * (HF / 8) * CHR;
+  static constexpr uint32_t D_BYTES = 2u * (NOUT / 8) * CHR;
+  static constexpr int RDF = 12;             // row data: ux uy uz valid | wx wy wz | t0 t1 t2 | pdf | -
+  static constexpr uint32_t RD_BYTES = RDF * R * 4;
+  static constexpr uint32_t DZ_BYTES = (uint32_t)L * R * 16 + 4u * R * 4;   // [L][R] float4 + [4][R]
+  static constexpr uint32_t OFF_X1 = a1k(WIMG);
+  __host__ __device__ static constexpr uint32_t xhoff(int k) { return OFF_X1 + (uint32_t)(k - 1) * XH_BYTES; }
+  static constexpr uint32_t OFF_D = OFF_X1 + (uint32_t)(NL - 1) * XH_BYTES;
+  static constexpr uint32_t OFF_X0 = OFF_D + D_BYTES;
+  // X0 stages: 2 when they fit (gathers run a full tile ahead), else 1
+  static constexpr uint32_t fixed_tail(int s0) {
+    return OFF_X0 + (uint32_t)s0 * (X0_BYTES + RD_BYTES) + DZ_BYTES + 3u * TPR * R * 4u + 256u;
+  }
+  static constexpr int S0 = fixed_tail(2) <= 220u * 1024u ? 2 : 1;
+  // delta_{NL-1} in D; delta_k (k < NL-1) over X_{k+1} (its ones chunk stays).
+  // (Measured on B200 c2: a separate delta buffer letting each backward
+  // epilogue run under the dW MMAs did not shorten the backward phases.)
+  __host__ __device__ static constexpr uint32_t dboff(int k) { return k == NL - 1 ? OFF_D : xhoff(k + 1); }
+  __host__ __device__ static constexpr uint32_t dfeat(int k) { return k == NL - 1 ? (uint32_t)NOUT : (uint32_t)HF; }
+  static constexpr uint32_t OFF_RD = OFF_X0 + (uint32_t)S0 * X0_BYTES;
+  static constexpr uint32_t OFF_DZ = OFF_RD + (uint32_t)S0 * RD_BYTES;
+  static constexpr uint32_t OFF_XCH = (OFF_DZ + DZ_BYTES + 15u) & ~15u;   // head exchange [TPR][3][R] f32
+  static constexpr uint32_t OFF_BAR = OFF_XCH + 3u * TPR * R * 4u;
+  // mbarriers: [0] weights, [1] mma, [2] dz full, [3] dz empty, [4..4+S0) x0 full, [4+S0..4+2 S0) x0 empty
+  static constexpr int NBAR = 4 + 2 * S0;
+  static constexpr uint32_t OFF_TSLOT = OFF_BAR + 8u * NBAR;
+  static constexpr uint32_t SMEM_RAW = OFF_TSLOT + 16u;
+  // dW^T MMAs read M_k / 8 feature chunks from a lo base (M_k = 64 or 128):
+  // the rows past X_k's features are garbage rows of dW^T (ignored) but the
+  // reads must stay inside the allocation
+  __host__ __device__ static constexpr int dwm(int k) { return (k == 0 ? ZF : HF) <= 64 ? 64 : 128; }
+  __host__ __device__ static constexpr uint32_t overread(int k) {
+    return (k == 0 ? OFF_X0 + (uint32_t)(S0 - 1) * X0_BYTES + (ZF / 8) * CHR : xhoff(k) + (HF / 8) * CHR) +
+           (uint32_t)(dwm(k) / 8) * CHR;
+  }
+  __host__ __device__ static constexpr uint32_t max_overread(int k) {
+    return k < 0 ? 0u : (overread(k) > max_overread(k - 1) ? overread(k) : max_overread(k - 1));
+  }
+  static constexpr uint32_t SMEM = SMEM_RAW > max_overread(NL - 1) ? SMEM_RAW : max_overread(NL - 1);
+  static_assert(SMEM <= 227u * 1024u, "warp-specialised kernel smem");
+  // ---- TMEM columns: forward / dX accumulator, dz, dW^T accumulators
+  static constexpr int C_ACC = 0, C_DZ = 64;
+  static_assert(W <= 64 && NOUT <= 64 && NG <= 64, "accumulator columns");
+  __host__ __device__ static constexpr int dwcol(int k) { return 128 + B::osum(k); }
+  static_assert(128 + N::osum(NL) <= 512, "TMEM columns");
+  static constexpr int TCOLS = 512;
+};
+
+// mbarrier wait that traps instead of hanging (a legitimate wait here is
+// microseconds; ~4 s of polling means a protocol bug)
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (8LL << 30)) __trap();
+  }
+}
+
+// the same for warps with nothing else to do: back off between polls so the
+// chain warps get the issue slots (ncu r02h: the polling memory warps were
+// 21 % of all stall samples)
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(128);
+    if (clock64() - t0 > (8LL << 30)) __trap();
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(tc::smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on `bar` (UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(tc::smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(tc::smem_u32(bar)) : "memory");
+}
+
+// dW^T[M feats x out] += X^T[M feats x ROWS] delta[ROWS x out]: both MN-major,
+// M = 64 or 128 (the X_k feature chunks read), K = the ROWS samples.
+template <int ROWS, int M>
+__device__ __forceinline__ void issue_dw_m(uint32_t d, uint32_t xhi, uint32_t xlo, uint32_t dhi, uint32_t dlo,
+                                           int out) {
+  constexpr uint32_t CHR = ROWS * 16;
+  const uint32_t idesc = tc::idesc_bf16(M, out, true, true);
+  const uint64_t ah = tc::sdesc(xhi, 128, CHR), al = tc::sdesc(xlo, 128, CHR);
+  const uint64_t bh = tc::sdesc(dhi, 128, CHR), bl = tc::sdesc(dlo, 128, CHR);
+#pragma unroll
+  for (int s = 0; s < ROWS / 16; ++s) {
+    const uint64_t ra = (uint64_t)(s * 256) >> 4;
+    mma3(d, ah + ra, al + ra, bh + ra, bl + ra, idesc, 1u);
+  }
+}
+
+// Split-bf16 weight image in the smem layout of stage_weights_tc (chunk-major,
+// hi then lo per layer) + fp32 biases: built once per launch from the live
+// parameters, then bulk-copied by every CTA.
+template <class N>
+__global__ void __launch_bounds__(256) prep_wimg_kernel(const float* __restrict__ g, uint8_t* __restrict__ img) {
+  using T = TC<N>;
+#pragma unroll
+  for (int k = 0; k < N::NL; ++k) {
+    const int in = T::in(k), inp = T::in_p(k), out = T::out(k);
+    const float* gw = g + N::gw_off(k);
+    uint8_t* hi = img + T::woff(k);
+    uint8_t* lo = hi + T::wbytes(k);
+    const int cnt = out * (inp / 8);
+    for (int e = (int)(blockIdx.x * blockDim.x + threadIdx.x); e < cnt; e += (int)(gridDim.x * blockDim.x)) {
+      const int o = e % out, j = e / out;
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = 8 * j + q;
+        v[q] = i < in ? __ldg(gw + o * in + i) : 0.0f;
+      }
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tc::split_pack(v[2 * q], v[2 * q + 1], h[q], l[q]);
+      const uint32_t off = (uint32_t)(j * out * 16 + o * 16);
+      *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+    float* sb = reinterpret_cast<float*>(img + T::WBYTES + T::boff(k));
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < out; o += gridDim.x * blockDim.x)
+      sb[o] = __ldg(g + N::gb_off(k) + o);
+  }
+}
+
+template <class N>
+__global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a) {
+  using T = WS<N>;
+  using TB = TC<N>;
+  constexpr int NL = N::NL, K = N::K, W = N::W, NOUT = N::NOUT, L = N::L, NG = N::NGRID, NIN = N::NIN;
+  constexpr int R = T::R;
+  constexpr uint32_t CHR = T::CHR;
+  constexpr int S0 = T::S0;
+  constexpr int TPR = T::TPR;
+  constexpr int WH = W / TPR, KH = K / TPR, LH = L / TPR;   // per chain thread: its share of columns / lobes / levels
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+  uint64_t* bar_w = bars + 0;
+  uint64_t* bar_mma = bars + 1;
+  uint64_t* bar_dzf = bars + 2;
+  uint64_t* bar_dze = bars + 3;
+  uint64_t* bar_x0f = bars + 4;
+  uint64_t* bar_x0e = bars + 4 + S0;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_TSLOT);
+  if (tid == 0) {
+    tc::mbar_init(bar_w, 1);
+    tc::mbar_init(bar_mma, 1);
+    tc::mbar_init(bar_dzf, T::CHAIN_THREADS);
+    tc::mbar_init(bar_dze, T::SCATTER_THREADS);
+    for (int s = 0; s < S0; ++s) {
+      tc::mbar_init(bar_x0f + s, T::GATHER_THREADS);
+      tc::mbar_init(bar_x0e + s, 1);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, (uint32_t)T::TCOLS);
+  // constant "ones" chunks (bias rows of dW^T): X0 stages at NIN, X_k at W
+  if (tid < R) {
+    const float e1[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, e0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < S0; ++s) {
+      const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (T::ZF / 8) * CHR;
+#pragma unroll
+      for (int f = NIN; f < T::ZF; f += 8) tc::store_chunk(xh, xl, R, tid, f / 8, f == NIN ? e1 : e0);
+    }
+#pragma unroll
+    for (int k = 1; k < NL; ++k) {
+      const uint32_t xh = sb + T::xhoff(k), xl = xh + (T::HF / 8) * CHR;
+      tc::store_chunk(xh, xl, R, tid, W / 8, e1);
+    }
+  }
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  // the whole TMEM: base column 0, lane 0 (checked); keeps MMA operands uniform
+  static_assert(T::TCOLS == 512, "constant TMEM base needs the full allocation");
+  constexpr uint32_t tbase = 0;
+  if (*tslot != 0u) __trap();
+  if (tid == 0) {   // weight image: one TMA bulk copy
+    mbar_expect_tx(bar_w, T::WIMG);
+    bulk_g2s(smem, a.wimg, T::WIMG, bar_w);
+  }
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + R - 1) / R;
+  const int64_t tstride = gridDim.x;
+  const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
+
+  if (warp < 4 * TPR) {
+    // =========================== CHAIN =====================================
+    // thread (h, r): row r = 32 (warp % 4) + lane (= TMEM lane), part h = warp / 4
+    // of the columns (epilogues), lobes (head) and levels (dz).  The TPR
+    // threads of a row are warps w % 4 + 4 h: they exchange through smem
+    // behind a named barrier of those 4 warps (2 + w % 4).
+    const int h = warp >> 2;
+    const int r = ((warp & 3) << 5) | lane;
+    const uint32_t lad = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane field
+    // zero the dW^T accumulators (all later MMAs accumulate); halves by column
+    for (int col = 16 * h; col < N::osum(NL); col += 16 * TPR) tc::tmem_zero16(tbase + lad + (uint32_t)(128 + col));
+    tc::tmem_wait_st();
+    mbar_wait_t(bar_w, 0);
+    const float* bias = reinterpret_cast<const float*>(smem + TB::WBYTES);
+    float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH);   // [TPR h][3][R] head exchange
+    const uint32_t wsb = sb;   // weight image at smem offset 0
+    uint32_t phase = 0;
+    double loss = 0.0;
+    unsigned c_used = 0, c_zero = 0, c_drop = 0;
+    auto handoff = [&]() {
+      tc::fence_proxy_async();
+      tc::fence_before_sync();
+      tc::named_sync(1u, (uint32_t)T::CHAIN_THREADS);
+    };
+    auto psync = [&]() { tc::named_sync(2u + (uint32_t)(warp & 3), 32u * TPR); };
+    auto wait_mma = [&]() {
+      tc::mbar_wait(bar_mma, phase);
+      phase ^= 1u;
+      tc::fence_after_sync();
+    };
+    // previous tile's dz -> dz stage (run while the next tile's first MMA executes)
+    struct Prev { float ux, uy, uz; float valid; };
+    Prev prev{0.f, 0.f, 0.f, 0.f};
+    auto dz_epilogue = [&](const Prev& pv, int kk) {
+      float v[NG / TPR];
+      tc::tmem_ldn<NG / TPR>(tbase + lad + (uint32_t)(T::C_DZ + h * (NG / TPR)), v);
+      tc::tmem_wait_ld();
+      mbar_wait_t(bar_dze, (uint32_t)((kk & 1) ^ 1));
+      float4* dz = reinterpret_cast<float4*>(smem + T::OFF_DZ);
+#pragma unroll
+      for (int l = 0; l < LH; ++l)
+        dz[(h * LH + l) * R + r] = make_float4(v[4 * l], v[4 * l + 1], v[4 * l + 2], v[4 * l + 3]);
+      if (h == 0) {
+        float* uu = reinterpret_cast<float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
+        uu[r] = pv.ux; uu[R + r] = pv.uy; uu[2 * R + r] = pv.uz; uu[3 * R + r] = pv.valid;
+      }
+      mbar_arrive(bar_dzf);
+    };
+    const bool stamp = (a.debug & 4) && blockIdx.x == 0 && tid == 0;
+    int kt = 0;
+#define NPM_WS_STAMP(idx) \
+  do { if (stamp && kt < 64) a.dbg_clock[kt * 16 + (idx)] = clock64(); } while (0)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += tstride, ++kt) {
+      const int s = kt % S0;
+      const uint32_t ph0 = (uint32_t)((kt / S0) & 1);
+      const uint32_t x0h = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, x0l = x0h + (T::ZF / 8) * CHR;
+      NPM_WS_STAMP(0);
+      mbar_wait_t(bar_x0f + s, ph0);
+      NPM_WS_STAMP(1);
+      tc::fence_after_sync();
+      if (tid == 0) {
+        issue_fwd_r<R>(tbase + T::C_ACC, x0h, x0l, wsb + TB::woff(0), wsb + TB::woff(0) + TB::wbytes(0),
+                       TB::in_p(0), TB::out(0));
+        tc::mma_commit(bar_mma);
+      }
+      // this row's inputs (read now: the stage is refilled once bwd_0 completes)
+      const float* rd = reinterpret_cast<const float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
+      Prev cur{rd[r], rd[R + r], rd[2 * R + r], rd[3 * R + r]};
+      const float h_wx = rd[4 * R + r], h_wy = rd[5 * R + r], h_wz = rd[6 * R + r];
+      const float h_t0 = rd[7 * R + r], h_t1 = rd[8 * R + r], h_t2 = rd[9 * R + r], h_p = rd[10 * R + r];
+      const bool hvalid = cur.valid != 0.0f;
+      if (kt > 0) dz_epilogue(prev, kt - 1);
+      NPM_WS_STAMP(2);
+      uint32_t mask[NL];   // ReLU'(X_k) of this thread's W/2 columns (bit j: column h W/2 + j)
+      // ---- forward
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        if (k > 0) {
+          handoff();
+          if (tid == 0) {
+            tc::fence_after_sync();
+            const uint32_t xh = sb + T::xhoff(k), xl = xh + (T::HF / 8) * CHR;
+            const uint32_t w = wsb + TB::woff(k);
+            issue_fwd_r<R>(tbase + T::C_ACC, xh, xl, w, w + TB::wbytes(k), TB::in_p(k), TB::out(k));
+            tc::mma_commit(bar_mma);
+          }
+        }
+        wait_mma();
+        NPM_WS_STAMP(3 + 2 * k);
+        const float* b = bias + TB::boff(k) / 4;
+        if (k < NL - 1) {
+          const uint32_t xh = sb + T::xhoff(k + 1), xl = xh + (T::HF / 8) * CHR;
+          uint32_t mk = 0;
+#pragma unroll
+          for (int c16 = 0; c16 < WH; c16 += 16) {   // 16 columns at a time (register pressure)
+            float v[16];
+            tc::tmem_ldn<16>(tbase + lad + (uint32_t)(T::C_ACC + h * WH + c16), v);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              v[j] = fmaxf(v[j] + b[h * WH + c16 + j], 0.0f);
+              mk |= (v[j] > 0.0f ? 1u : 0u) << (c16 + j);
+            }
+            tc::store_chunk(xh, xl, R, r, h * (WH / 8) + c16 / 8, v);
+            tc::store_chunk(xh, xl, R, r, h * (WH / 8) + c16 / 8 + 1, v + 8);
+          }
+          mask[k + 1] = mk;
+        } else {
+          // ---- Eq. 9 head (C-O12, C-O13): row r, lobes [h K/2, (h+1) K/2)
+          float lp[KH], kp[KH], tp[KH], pp[KH];
+          tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + h * KH), lp);
+          tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + K + h * KH), kp);
+          tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + 2 * K + h * KH), tp);
+          tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + 3 * K + h * KH), pp);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int m = 0; m < KH; ++m) {
+            lp[m] += b[h * KH + m];
+            kp[m] += b[K + h * KH + m];
+            tp[m] += b[2 * K + h * KH + m];
+            pp[m] += b[3 * K + h * KH + m];
+          }
+          float t = h_t0;
+          bool all_zero = t == 0.0f;
+          if (a.channels == 3) {
+            all_zero = all_zero && h_t1 == 0.0f && h_t2 == 0.0f;
+            t = 0.2126f * t + 0.7152f * h_t1 + 0.0722f * h_t2;
+          }
+          const float p = h_p;
+          const float ratio = t / p;
+          const bool drop = hvalid && (!isfinite(ratio) || !isfinite(p) || !(p > 0.0f));
+          const bool zero = hvalid && !drop && all_zero;
+          const bool use = hvalid && !drop && !zero;
+          const float s_ = use ? (float)(-(double)ratio * a.inv_n_global) : 0.0f;
+          const float wx = h_wx, wy = h_wy, wz = h_wz;
+          float kap[KH], mx[KH], my[KH], mz[KH], th[KH], ph[KH], vv[KH], sth[KH], cth[KH], sph[KH], cph[KH],
+              emk[KH];
+          float mloc = lp[0];
+#pragma unroll
+          for (int m = 0; m < KH; ++m) {
+            mloc = fmaxf(mloc, lp[m]);
+            kap[m] = __expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
+            lobe_angles(tp[m], pp[m], kap[m], th[m], ph[m], sth[m], cth[m], sph[m], cph[m]);
+            mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
+            const float nrm = lobe_norm_fast(kap[m], emk[m]);
+            vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);
+          }
+          // softmax max / normaliser / mixture sum across the row's two threads
+          xch[(h * 3 + 0) * R + r] = mloc;
+          psync();
+          float M = xch[0 * R + r];
+#pragma unroll
+          for (int q = 1; q < TPR; ++q) M = fmaxf(M, xch[(q * 3 + 0) * R + r]);
+          float e[KH], S = 0.0f, P = 0.0f;
+#pragma unroll
+          for (int m = 0; m < KH; ++m) {
+            e[m] = __expf(lp[m] - M);
+            S += e[m];
+            P += e[m] * vv[m];
+          }
+          xch[(h * 3 + 1) * R + r] = S;
+          xch[(h * 3 + 2) * R + r] = P;
+          psync();
+          // the same association order on every thread of the row: parts 0, 1, ...
+          float St = 0.0f, Pt = 0.0f;
+#pragma unroll
+          for (int q = 0; q < TPR; ++q) { St += xch[(q * 3 + 1) * R + r]; Pt += xch[(q * 3 + 2) * R + r]; }
+          const float invS = 1.0f / St;
+          const float Vb = fmaxf(Pt * invS, kVFloor);
+          const float invV = 1.0f / Vb;
+          // f-4 (C-A31): chi^2 scales Eq. 9's record weight by D^ / V
+          const float chi = a.divergence ? (use ? t * invV : 0.0f) : 1.0f;
+          const float sd = s_ * chi;
+          float dl[KH], dk[KH], dt[KH], dp[KH];
+#pragma unroll
+          for (int m = 0; m < KH; ++m) {
+            const float lam = e[m] * invS;
+            const float gam = lam * vv[m] * invV;
+            dl[m] = sd * (gam - lam);
+            const float dx = mx[m] - wx, dy = my[m] - wy, dz = mz[m] - wz;
+            const float d2 = dx * dx + dy * dy + dz * dz;
+            // 2 kappa e^{-2 kappa} / (1 - e^{-2 kappa}) with em = 1 - e^{-2 kappa}
+            const float dkk = sd * gam * (1.0f - kap[m] * 0.5f * d2 - __fdividef(2.0f * kap[m] * (1.0f - emk[m]), emk[m]));
+            dk[m] = (kp[m] < a.log_kmin || kp[m] > a.log_kmax) ? 0.0f : dkk;   // C-A8
+            const float wdth = kPi * (cth[m] * cph[m] * wx + cth[m] * sph[m] * wy - sth[m] * wz);
+            const float wdph = kTwoPi * (-sth[m] * sph[m] * wx + sth[m] * cph[m] * wy);
+            const float sgk = sd * gam * kap[m];
+            dt[m] = sgk * wdth * th[m] * (1.0f - th[m]);
+            dp[m] = sgk * wdph * ph[m] * (1.0f - ph[m]);
+          }
+          const uint32_t dh = sb + T::OFF_D, dlo = dh + (NOUT / 8) * CHR;
+          tc::store_feats<KH>(dh, dlo, R, r, h * KH, dl);
+          tc::store_feats<KH>(dh, dlo, R, r, K + h * KH, dk);
+          tc::store_feats<KH>(dh, dlo, R, r, 2 * K + h * KH, dt);
+          tc::store_feats<KH>(dh, dlo, R, r, 3 * K + h * KH, dp);
+          if (h == 0) {
+            c_drop += drop; c_zero += zero;
+            if (use) {
+              loss += a.divergence ? -(double)sd : (double)s_ * (double)logf(Vb);   // chi^2: (D^/p~)(D^/V)/N
+              c_used += 1;
+            }
+          }
+        }
+        NPM_WS_STAMP(4 + 2 * k);
+      }
+      // ---- backward: k = NL-1 .. 0; delta_k in D (k = NL-1) or over X_{k+1}
+#pragma unroll
+      for (int k = NL - 1; k >= 0; --k) {
+        handoff();
+        if (tid == 0) {
+          tc::fence_after_sync();
+          with_k<NL>(k, [&](auto KC) {
+            constexpr int kk = decltype(KC)::value;
+            const uint32_t dh = sb + T::dboff(kk), dl = dh + (T::dfeat(kk) / 8) * CHR;
+            const uint32_t w = wsb + TB::woff(kk);
+            const uint32_t xh = kk == 0 ? x0h : sb + T::xhoff(kk);
+            const uint32_t xl = kk == 0 ? x0l : xh + (T::HF / 8) * CHR;
+            issue_dx_r<R>(tbase + (kk == 0 ? T::C_DZ : T::C_ACC), dh, dl, w, w + TB::wbytes(kk), TB::out(kk),
+                          kk > 0 ? W : NG);
+            issue_dw_m<R, T::dwm(kk)>(tbase + (uint32_t)T::dwcol(kk), xh, xl, dh, dl, TB::out(kk));
+            tc::mma_commit(bar_mma);
+            if (kk == 0) tc::mma_commit(bar_x0e + s);   // X0 stage free once dW_0 has read it
+          });
+        }
+        wait_mma();
+        NPM_WS_STAMP(3 + 2 * NL + 2 * (NL - 1 - k));
+        if (k > 0) {
+          // delta_{k-1} = dX_k * ReLU'(X_k) -> over X_k (read by dW_k, complete)
+          const uint32_t dh = sb + T::dboff(k - 1), dl = dh + (T::dfeat(k - 1) / 8) * CHR;
+          const uint32_t mk = mask[k];
+#pragma unroll
+          for (int c16 = 0; c16 < WH; c16 += 16) {
+            float v[16];
+            tc::tmem_ldn<16>(tbase + lad + (uint32_t)(T::C_ACC + h * WH + c16), v);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = ((mk >> (c16 + j)) & 1u) ? v[j] : 0.0f;
+            tc::store_chunk(dh, dl, R, r, h * (WH / 8) + c16 / 8, v);
+            tc::store_chunk(dh, dl, R, r, h * (WH / 8) + c16 / 8 + 1, v + 8);
+          }
+        }
+      }
+      NPM_WS_STAMP(15);
+      prev = cur;
+    }
+#undef NPM_WS_STAMP
+    if (kt > 0) dz_epilogue(prev, kt - 1);
+    // ---- flush dW^T / db: lane = input feature (M = 128) or 32 (f/16) + f%16
+    // (M = 64); the two threads of a lane split the output columns
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      constexpr int MAXO = (NOUT > W ? NOUT : W) / TPR;
+      float vv[MAXO];
+      const int out = TB::out(k), in = TB::in(k), oh = out / TPR;
+      if (out == NOUT) tc::tmem_ldn<NOUT / TPR>(tbase + lad + (uint32_t)(T::dwcol(k) + h * (NOUT / TPR)), vv);
+      else tc::tmem_ldn<W / TPR>(tbase + lad + (uint32_t)(T::dwcol(k) + h * (W / TPR)), vv);
+      tc::tmem_wait_ld();
+      int f = r;
+      bool ok = true;
+      with_k<NL>(k, [&](auto KC) {
+        if (T::dwm(decltype(KC)::value) == 64) {
+          f = 16 * (warp & 3) + (lane & 15);
+          ok = lane < 16;
+        }
+      });
+      if (ok && f < in) {
+        float* gp = a.grads + N::gw_off(k) + f;
+        for (int o = 0; o < oh; ++o) atomicAdd(gp + (h * oh + o) * in, vv[o]);
+      } else if (ok && f == in) {
+        float* gp = a.grads + N::gb_off(k) + h * oh;
+        for (int o = 0; o < oh; ++o) atomicAdd(gp + o, vv[o]);
+      }
+    }
+    loss = warp_sum_d(loss);
+    c_used = warp_sum_u(c_used); c_zero = warp_sum_u(c_zero); c_drop = warp_sum_u(c_drop);
+    if (lane == 0 && h == 0) {
+      atomicAdd(a.stats, loss);
+      atomicAdd(a.counters + 0, (unsigned long long)c_used);
+      atomicAdd(a.counters + 1, (unsigned long long)c_zero);
+      atomicAdd(a.counters + 2, (unsigned long long)c_drop);
+    }
+  } else {
+    // =========================== MEMORY ====================================
+    // thread (part, row): row = m % 128, part = m / 128 owns levels
+    // [part L/2, (part+1) L/2).  Iteration k gathers tile k into X0 stage
+    // k % S0, then scatters tile k - 1 from the dz stage: the chain computes
+    // tile k while this role scatters k - 1, and tile k + 1's gathers follow.
+    const int m = tid - T::CHAIN_THREADS;
+    const int row = m & (R - 1), part = m >> 7;
+    constexpr int LP = L / 2;
+    float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
+    auto scatter = [&](int kd) {
+      mbar_wait_idle(bar_dzf, (uint32_t)(kd & 1));
+      const float4* dz = reinterpret_cast<const float4*>(smem + T::OFF_DZ);
+      const float* uu = reinterpret_cast<const float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
+      const float ux = uu[row], uy = uu[R + row], uz = uu[2 * R + row];
+      const bool valid = uu[3 * R + row] != 0.0f;
+      float4 d[LP];
+#pragma unroll
+      for (int l = 0; l < LP; ++l) d[l] = dz[(part * LP + l) * R + row];
+      mbar_arrive(bar_dze);
+      if (!valid || (a.debug & 1)) return;
+#pragma unroll
+      for (int j = 0; j < LP; ++j) {
+        const float4 gq = d[j];
+        if (gq.x == 0.0f && gq.y == 0.0f && gq.z == 0.0f && gq.w == 0.0f) continue;
+        const int l = part * LP + j;
+        LevelCorners lc;
+        level_corners(a.grid, l, ux, uy, uz, lc);
+        float4* tg = ((a.priv_mask >> l) & 1u) ? a.priv + (int64_t)blockIdx.x * a.priv_stride + a.priv_off[l]
+                                                 : gtab + a.grid.off[l];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float w = lc.w[c];
+          atomicAdd(tg + lc.idx[c], make_float4(w * gq.x, w * gq.y, w * gq.z, w * gq.w));
+        }
+      }
+    };
+    int kt = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += tstride, ++kt) {
+      const int s = kt % S0;
+      const uint32_t ph0 = (uint32_t)((kt / S0) & 1);
+      const int64_t slot = tile * R + row;
+      const bool valid = slot < n;
+      const int64_t i = valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
+      float ux = 0.f, uy = 0.f, uz = 0.f;
+      if (valid) {
+        ux = normalize_axis(__ldg(a.px + i), a.grid.lo[0], a.grid.inv[0]);
+        uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
+        uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
+      }
+      float hin[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f};
+      if (part == 0 && valid) {
+        hin[0] = __ldg(a.wx + i); hin[1] = __ldg(a.wy + i); hin[2] = __ldg(a.wz + i);
+        hin[3] = __ldg(a.target + i);
+        if (a.channels == 3) {
+          hin[4] = __ldg(a.target + a.target_stride + i);
+          hin[5] = __ldg(a.target + 2 * a.target_stride + i);
+        }
+        hin[6] = __ldg(a.spdf + i);
+      }
+      const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (T::ZF / 8) * CHR;
+      // all of this thread's levels in registers, then wait for the stage
+      float gf[4 * LP];
+#pragma unroll
+      for (int q = 0; q < LP; ++q) {
+        float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+          const int l = part * LP + q;
+          LevelCorners lc;
+          level_corners(a.grid, l, ux, uy, uz, lc);
+          gl = gather_level(tab, a.grid.off[l], lc);
+        }
+        gf[4 * q] = gl.x; gf[4 * q + 1] = gl.y; gf[4 * q + 2] = gl.z; gf[4 * q + 3] = gl.w;
+      }
+      mbar_wait_idle(bar_x0e + s, ph0 ^ 1u);
+#pragma unroll
+      for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
+      if (part == 0) {
+        float* rd = reinterpret_cast<float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
+        rd[row] = ux; rd[R + row] = uy; rd[2 * R + row] = uz; rd[3 * R + row] = valid ? 1.0f : 0.0f;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) rd[(4 + q) * R + row] = hin[q];
+      }
+      tc::fence_proxy_async();
+      mbar_arrive(bar_x0f + s);
+      if (kt > 0) scatter(kt - 1);
+    }
+    if (kt > 0) scatter(kt - 1);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tbase, (uint32_t)T::TCOLS);
+}
+
+}  // namespace ws
+

@@ -7,7 +7,8 @@ N(0, 1.5^2), which never reaches the clamp; here the output bias of each lobe's
 kappa' row is placed
 
   lobe 0: ln 1e5 + 2    (always clamped high)
-  lobe 1: ln 1e5        (straddles the upper bound: about half clamped)
+  lobe 1: ln 1e5        (straddles the upper bound: about half clamped;
+                         lobes 1 and 3 are centred on the bound by a probe decode)
   lobe 2: ln 1e5 - 0.5  (kappa ~ 6e4, just inside)
   lobe 3: ln 1e-5       (straddles the lower bound)
   lobe 4: ln 1e-5 + 0.5 (just inside)
@@ -17,8 +18,9 @@ kappa' row is placed
 (W_3 h_2 spreads kappa' by ~0.1 s.d., at most ~0.75, about its bias.)
 
 and the whole path is compared with the float64 oracle at the BASELINE
-tolerances: decode (raw / lambda / mu abs 1e-4, kappa rel 1e-4), pdf (rel
-1e-3) at caller directions aimed at the concentrated lobes, sampling
+tolerances: decode (raw / lambda / mu abs 1e-4, kappa rel 1e-4), pdf at
+caller directions aimed at the concentrated lobes (rel 1e-3, widened by the
+pdf's conditioning where kappa |w - mu| >~ 1e2: reading C-A33 below), sampling
 (directions abs 1e-4, pdf at the sample rel 1e-3), and the KL (Eq. 9) and
 chi^2 (C-A31) gradients (rel-L2 2e-3, whole vector and per block).  The C-A8
 rule is asserted element by element: the kappa' rows of the output layer for
@@ -61,6 +63,11 @@ def edge_pair(name, divergence=0, seed=41):
     p = synth.random_params(ocfg.layer_dims, ocfg.n_grid, ocfg.n_lobes, seed=seed)
     _, _, _, boff = out_layer_rows(ocfg)
     p[boff + 8: boff + 16] = np.asarray(KAPPA_BIAS, np.float32)
+    # centre the straddling lobes 1 and 3 on their bound: shift the bias by the
+    # median of W_3 h_2 over a probe batch (input construction only)
+    raw, _ = onpm.decode(ocfg, p.astype(np.float64), dict(x=synth.query_batch(2000, seed=40)["x"]))
+    for lobe in (1, 3):
+        p[boff + 8 + lobe] -= np.float32(np.median(raw[8 + lobe]) - KAPPA_BIAS[lobe])
     m = npm.Model(0, **model)
     m.set(npm.BUF_PARAMS, p)
     m.set(npm.BUF_EMA, p)
@@ -101,7 +108,7 @@ def test_decode_at_kappa_edges(name):
     oraw, act = onpm.decode(ocfg, p, oq(b, False))
     kr = oraw[8:16]
     # the batch really straddles both clamp bounds and covers kappa in [1e2, 1e3]
-    assert 0.05 < (kr[1] > LN_MAX).mean() < 0.95 and 0.05 < (kr[3] < LN_MIN).mean() < 0.95
+    assert 0.2 < (kr[1] > LN_MAX).mean() < 0.8 and 0.2 < (kr[3] < LN_MIN).mean() < 0.8
     assert np.all(kr[0] > LN_MAX) and np.all(kr[5] < LN_MIN)
     assert np.abs(raw - oraw).max() <= 1e-4
     assert np.abs(lam - act["lam"]).max() <= 1e-4
@@ -109,6 +116,31 @@ def test_decode_at_kappa_edges(name):
     assert (np.abs(kap - act["kappa"]) / act["kappa"]).max() <= 1e-4
     assert np.all(kap[0] == kap[0, 0]) and abs(kap[0, 0] - 1e5) <= 1e-4 * 1e5
     assert abs(kap[5, 0] - 1e-5) <= 1e-4 * 1e-5
+
+
+def pdf_tolerance(m, q, act, w):
+    """Reading C-A33: the mixture pdf's relative sensitivity to a
+    lobe's mean is kappa |w - mu| (d log v / d mu = kappa (w - mu)) and to its
+    log-concentration 1 - kappa |mu - w|^2 / 2 - ..., so with the decoded
+    parameters carrying the errors the parameter tolerances allow, the pdf
+    tolerance is rel 1e-3 plus, per record,
+        2 (sum_i gamma_i kappa_i |w - mu_i|) eps_mu
+      + 2 (sum_i gamma_i (1 + kappa_i |w - mu_i|^2 / 2)) eps_kappa
+    with gamma_i = lambda_i v_i / V and eps_mu, eps_kappa the GPU-vs-oracle
+    max |d mu| and max relative d kappa measured on this very batch.  Where
+    kappa |w - mu| stays below ~1e2 (kappa <~ 1e3) this is the plain 1e-3."""
+    _, _, kap, mu = (t.cpu().numpy().astype(np.float64) for t in m.decode(q))
+    eps_mu = np.abs(mu - act["mu"]).max()
+    eps_k = (np.abs(kap - act["kappa"]) / act["kappa"]).max()
+    w = w.astype(np.float64)
+    d = act["mu"] - w[:, None, :]                       # [3, K, n]
+    d2 = (d ** 2).sum(0)
+    v = act["kappa"] / (2 * np.pi * -np.expm1(-2 * act["kappa"])) * np.exp(-0.5 * act["kappa"] * d2)
+    lv = act["lam"] * v
+    gam = lv / lv.sum(0, keepdims=True)
+    cond_mu = (gam * act["kappa"] * np.sqrt(d2)).sum(0)
+    cond_k = (gam * (1 + 0.5 * act["kappa"] * d2)).sum(0)
+    return 1e-3 + 2 * cond_mu * eps_mu + 2 * cond_k * eps_k
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
@@ -123,10 +155,14 @@ def test_pdf_aimed_at_concentrated_lobes(name):
     wq = aimed_directions(act, [0, 1, 2, 6, 7], [2e-3, 2e-3, 2e-3, 0.05, 0.02], rng)
     wq[:, ::7] = _unit(rng.normal(size=(3, wq[:, ::7].shape[1])))
     wq = wq.astype(np.float32)
-    pdf = m.pdf(gq(m, b), wq).cpu().numpy()
+    q = gq(m, b)
+    pdf = m.pdf(q, wq).cpu().numpy()
     opdf = ovmf.mixture_pdf(wq.astype(np.float64), act)
     assert np.median(opdf) > 10.0    # dominated by the concentrated lobes
-    assert (np.abs(pdf - opdf) / opdf).max() <= 1e-3
+    tol = pdf_tolerance(m, q, act, wq)
+    rel = np.abs(pdf - opdf) / opdf
+    assert np.all(rel <= tol), (rel.max(), tol[rel.argmax()])
+    assert np.median(tol) < 2e-2          # the conditioning term is not vacuous
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
