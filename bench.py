@@ -249,6 +249,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD, choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the c3 strong-scaling block")
     ap.add_argument("--native-comm", action="store_true",
                     help="GRADS allreduce through the library's own NCCL communicator (npm_comm_init)")
     args = ap.parse_args()
@@ -293,7 +294,7 @@ def main():
                        wq[2], pdfq_o, stream=stream)
         if ev is not None:
             ev.record()
-        dp.train_step(qt, twi, ttg, tpd, n_local=n)
+        dp.train_step(qt, twi, ttg, tpd, n_local=n, n_global=n * world)
 
     for i in range(args.warmup):
         step(i)
@@ -390,7 +391,7 @@ def main():
     def e2e_step(i):
         npm.npm_sample(m.h, hq, None, 0xC0FFEE, i * n, True, hwi[0], hwi[1], hwi[2], hpdf, hwq[0], hwq[1], hwq[2],
                        hpdfq, stream=stream)
-        dp.train_step(ht, htwi, httg, htpd, n_local=n, want_stats=False)
+        dp.train_step(ht, htwi, httg, htpd, n_local=n, n_global=n * world, want_stats=False)
         # the step's loss read back to pinned host memory every step, without a
         # host synchronisation per step (the timed region ends with one)
         npm.npm_step_stats_async(m.h, hstats.data_ptr(), stream=stream)
@@ -413,6 +414,40 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = 2 * n * world * K / te.item()
 
+    # ---- c3 strong scaling: N_global = 2^23 training records per
+    # optimisation step, sharded contiguously over the ranks (n_global / N each),
+    # one allreduce of GRADS + Adam per step; the same model shape as c2
+    strong = None
+    if name == "c2" and not args.no_strong:
+        from paper_2504_04315_b200.dp import shard_range
+        ng = CONFIGS["c3"]["n_global"]
+        a3, e3 = shard_range(ng, rank, world)
+        n3 = e3 - a3
+        sb3 = synth.training_batch(n3, seed=400 + rank, product=m.product)
+        sx3, sw3, st3, sp3 = T(sb3["x"]), T(sb3["wi"]), T(sb3["target"]), T(sb3["pdf"])
+        q3 = m.query(sx3, *([T(sb3["wo"]), T(sb3["nrm"]), T(sb3["rough"])] if m.product else []))
+        for _ in range(2):
+            dp.train_step(q3, sw3, st3, sp3, n_local=n3, n_global=ng)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k3 = 5
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(k3):
+            dp.train_step(q3, sw3, st3, sp3, n_local=n3, n_global=ng)
+        a1.record()
+        torch.cuda.synchronize()
+        t3 = torch.tensor([a0.elapsed_time(a1) / 1e3], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t3, op=dist.ReduceOp.MAX)
+        t3v = t3.item() / k3
+        strong = {"workload": "c3: 2^23 training records per optimisation step over all ranks (strong scaling)",
+                  "n_global": ng, "n_per_gpu": n3, "steps": k3, "ms_per_step": 1e3 * t3v,
+                  "train_samples_per_s": ng / t3v, "scaling": "strong",
+                  "note": "device time, max over ranks; inputs resident; includes the GRADS allreduce and Adam"}
+        del sx3, sw3, st3, sp3, q3
+
     # ---- the paper's own workloads, as context (RTX 3070): a training step on a
     # 2^18-record batch (~10 ms) and one guided evaluation of a 1280x720 frame (~3 ms)
     paper_ctx = None
@@ -422,14 +457,14 @@ def main():
         q18 = m.query(C(tx), *[C(e) if e is not None else None for e in extra_t])
         w18, t18, p18 = C(twi), C(ttg), C(tpd)
         for _ in range(3):
-            dp.train_step(q18, w18, t18, p18, n_local=k18)
+            dp.train_step(q18, w18, t18, p18, n_local=k18, n_global=k18 * world)
         torch.cuda.synchronize()
         ts = []
         for _ in range(10):
             flush.zero_()
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record()
-            dp.train_step(q18, w18, t18, p18, n_local=k18)
+            dp.train_step(q18, w18, t18, p18, n_local=k18, n_global=k18 * world)
             a1.record()
             torch.cuda.synchronize()
             ts.append(a0.elapsed_time(a1))
@@ -531,7 +566,8 @@ def main():
                         "host_enqueue_ms_per_step": host_enqueue_ms},
                 "gpu_launches": launches, "gpu_launches_per_step": launches / K,
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
-                "clocks": clk.summary(), "cpu_baseline": cpu, "paper_context": paper_ctx, "f1_guided_mis": f1,
+                "clocks": clk.summary(), "cpu_baseline": cpu, "strong_c3": strong, "paper_context": paper_ctx,
+                "f1_guided_mis": f1,
                 "f2_cosine_product": f2}
         print(json.dumps(line), flush=True)
     if distributed:
