@@ -303,6 +303,36 @@ npm_status npm_optimizer_step(npm_model* model, npm_step_stats* stats, void* str
 npm_status npm_get_unique_id(uint8_t out[128]);
 npm_status npm_comm_init(npm_model* model, int rank, int world, const uint8_t uid[128]);
 
+/* The exchange schedule of the attached communicator:
+ *   NPM_EXCHANGE_ALLREDUCE (default): ncclAllReduce(GRADS), then Adam + EMA
+ *     on every rank over the whole vector;
+ *   NPM_EXCHANGE_ZERO1: ncclReduceScatter(GRADS) -> Adam on this rank's
+ *     shard (npm_shard_range) -> ncclAllGather(PARAMS) -> EMA over the whole
+ *     (replicated) vector on every rank.  Same update as ALLREDUCE (the EMA
+ *     needs no exchange: it is elementwise in the gathered parameters); each
+ *     rank reads / writes the Adam moments of 1/P of the parameters.
+ * Bad mode -> NPM_ERR_INVALID. */
+typedef enum { NPM_EXCHANGE_ALLREDUCE = 0, NPM_EXCHANGE_ZERO1 = 1 } npm_exchange;
+npm_status npm_set_exchange(npm_model* model, int mode);
+
+/* ZeRO-1 building blocks, for a caller that runs the collectives on its own
+ * process group (paper_2504_04315_b200/dp.py with zero1=True):
+ *   npm_shard_range: rank's shard of the flat parameter vector, [*begin,
+ *     *begin + *count), *chunk = ceil(n_total / world / 4) * 4 floats per rank;
+ *     world * chunk <= n_total + 264, and every buffer is allocated (zero-
+ *     padded) to that size, so a reduce-scatter / all-gather may view
+ *     world * chunk floats from the buffer's start.  1 <= world <= 64.
+ *   npm_optimizer_step_shard: t := t + 1, Adam over the shard (GRADS there
+ *     must already hold the reduced gradient), then GRADS := 0 everywhere;
+ *     stats (optional, synchronises) hold the shard's grad_norm_sq and
+ *     n_nonfinite_grad.  No EMA: call npm_ema_update after gathering PARAMS.
+ *   npm_ema_update: EMA <- d EMA + (1 - d) PARAMS over the whole vector (C-O18).
+ * Bad rank / world -> NPM_ERR_INVALID. */
+npm_status npm_shard_range(const npm_model* model, int rank, int world, int64_t* begin, int64_t* count,
+                           int64_t* chunk);
+npm_status npm_optimizer_step_shard(npm_model* model, int rank, int world, npm_step_stats* stats, void* stream);
+npm_status npm_ema_update(npm_model* model, void* stream);
+
 /* Asynchronous form of the statistics read: enqueues on `stream` the copy of
  * the last training step's statistics (loss proxy, gradient norm, record
  * counters; as npm_train_step's stats) into `out`, which should be pinned

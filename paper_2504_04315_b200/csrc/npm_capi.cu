@@ -102,8 +102,9 @@ struct npm_model {
   cudaEvent_t pipe_in_free[4] = {nullptr, nullptr, nullptr, nullptr};   // last kernel that read pipe_in[set]
   cudaEvent_t pipe_out_free = nullptr;                 // last device->host copy out of pipe_out
   std::vector<cudaEvent_t> sync_events;
-  ncclComm_t comm = nullptr;   // npm_comm_init: GRADS allreduced inside npm_optimizer_step
-  int comm_world = 1;
+  ncclComm_t comm = nullptr;   // npm_comm_init: GRADS exchanged inside npm_optimizer_step
+  int comm_world = 1, comm_rank = 0;
+  int exchange = NPM_EXCHANGE_ALLREDUCE;   // npm_set_exchange
   bool pipeline = true;    // NPM_PIPELINE=0 disables
   int pipe_chunks = 3;     // NPM_PIPE_CHUNKS (c2 e2e: 2 -> 1.31, 3 -> 1.32, 4 -> 1.28, 8 -> 1.13 G/s)
   int query_groups = 1;    // NPM_QUERY_GROUPS
@@ -364,6 +365,17 @@ const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward"
 enum Kind { kKQuery = 0, kKEncode, kKTrainFwd, kKTrainBwd, kKWgrad, kKAdam, kKTrainFused, kKBin, kKUnwind, kKFold,
             kKinds };
 constexpr int64_t kBinMin = 65536;  // batches at least this large are spatially binned
+constexpr int64_t kBufPad = 8 + 4 * 64;   // floats past n_total in every parameter buffer
+constexpr int kMaxShardWorld = 64;
+
+// ZeRO-1 shard of rank in world: [begin, begin + count) of the flat parameter
+// vector, chunk = ceil(n_total / world / 4) * 4 floats per rank (float4 Adam).
+void shard_of(const npm_model* m, int rank, int world, int64_t& begin, int64_t& count, int64_t& chunk) {
+  chunk = ((m->n_total + world - 1) / world + 3) / 4 * 4;
+  begin = (int64_t)rank * chunk;
+  count = m->n_total - begin;
+  count = count < 0 ? 0 : (count > chunk ? chunk : count);
+}
 
 cudaEvent_t take_event(npm_model* m) {
   if (!m->pool.empty()) { cudaEvent_t e = m->pool.back(); m->pool.pop_back(); return e; }
@@ -464,6 +476,9 @@ struct Nccl {
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                 cudaStream_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
   bool ok = false;
 };
@@ -477,8 +492,10 @@ const Nccl& nccl() {
     r.comm_init_rank = reinterpret_cast<decltype(r.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
     r.all_reduce = reinterpret_cast<decltype(r.all_reduce)>(dlsym(h, "ncclAllReduce"));
     r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    r.reduce_scatter = reinterpret_cast<decltype(r.reduce_scatter)>(dlsym(h, "ncclReduceScatter"));
+    r.all_gather = reinterpret_cast<decltype(r.all_gather)>(dlsym(h, "ncclAllGather"));
     r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
-    r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy;
+    r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy && r.reduce_scatter && r.all_gather;
     return r;
   }();
   return n;
@@ -523,6 +540,23 @@ npm_status npm_comm_init(npm_model* m, int rank, int world, const uint8_t uid[12
   const ncclResult_t e = n.comm_init_rank(&m->comm, world, id, rank);
   if (e != ncclSuccess) { m->comm = nullptr; return nccl_fail(e, "ncclCommInitRank"); }
   m->comm_world = world;
+  m->comm_rank = rank;
+  return NPM_OK;
+}
+
+npm_status npm_set_exchange(npm_model* m, int mode) {
+  if (!m || (mode != NPM_EXCHANGE_ALLREDUCE && mode != NPM_EXCHANGE_ZERO1)) return fail(NPM_ERR_INVALID, "bad argument");
+  m->exchange = mode;
+  return NPM_OK;
+}
+
+npm_status npm_shard_range(const npm_model* m, int rank, int world, int64_t* begin, int64_t* count, int64_t* chunk) {
+  if (!m || world < 1 || world > kMaxShardWorld || rank < 0 || rank >= world) return fail(NPM_ERR_INVALID, "bad argument");
+  int64_t b, c, ch;
+  shard_of(m, rank, world, b, c, ch);
+  if (begin) *begin = b;
+  if (count) *count = c;
+  if (chunk) *chunk = ch;
   return NPM_OK;
 }
 
@@ -666,12 +700,14 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   if (nm % 4) { delete m; return fail(NPM_ERR_INVALID, "internal: MLP size not 16B aligned"); }
   m->n_total = m->n_mlp + m->n_grid;
   for (int b = 0; b < 5; ++b) {
-    // +8 floats: the paired grid gathers (gather_level) read the 32-B entry
-    // pair containing the last table entry
-    if (cudaMalloc(&m->buf[b], (m->n_total + 8) * sizeof(float)) != cudaSuccess) {
+    // + kBufPad floats: the paired grid gathers (gather_level) read the 32-B
+    // entry pair containing the last table entry, and the ZeRO-1 exchange
+    // views world * chunk >= n_total floats (npm_shard_range, world <= 64)
+    if (cudaMalloc(&m->buf[b], (m->n_total + kBufPad) * sizeof(float)) != cudaSuccess) {
       npm_destroy(m);
       return fail(NPM_ERR_OOM, "parameter buffers");
     }
+    cudaMemsetAsync(m->buf[b] + m->n_total, 0, kBufPad * sizeof(float), 0);
   }
   if (cudaMalloc(&m->dstats, 2 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&m->dcount, 4 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -1312,27 +1348,69 @@ npm_status npm_accumulate_grads(npm_model* m, const npm_query* q, const float* w
   return NPM_OK;
 }
 
+// Adam (+ EMA) over [begin, begin + count) of the flat vector (the whole
+// vector, or a ZeRO-1 shard); statistics over that range.
+static npm_status adam_range(npm_model* m, int64_t begin, int64_t count, bool ema, cudaStream_t st) {
+  const npm_config& c = m->cfg;
+  AdamArgs a;
+  a.n_total = count;
+  a.n_mlp = m->n_mlp - begin < 0 ? 0 : (m->n_mlp - begin > count ? count : m->n_mlp - begin);
+  a.p = m->buf[NPM_BUF_PARAMS] + begin; a.g = m->buf[NPM_BUF_GRADS] + begin; a.m = m->buf[NPM_BUF_ADAM_M] + begin;
+  a.v = m->buf[NPM_BUF_ADAM_V] + begin; a.e = m->buf[NPM_BUF_EMA] + begin;
+  a.lr = c.lr; a.beta1 = c.beta1; a.beta2 = c.beta2; a.eps = c.adam_eps; a.decay = c.ema_decay;
+  a.c1 = (float)(1.0 / (1.0 - std::pow((double)c.beta1, (double)m->t)));
+  a.c2 = (float)(1.0 / (1.0 - std::pow((double)c.beta2, (double)m->t)));
+  a.ema = ema ? 1 : 0;
+  a.gnorm = m->dstats + 1;
+  a.nonfinite = m->dcount + 3;
+  CUDA_TRY(cudaMemsetAsync(m->dstats + 1, 0, sizeof(double), st));
+  CUDA_TRY(cudaMemsetAsync(m->dcount + 3, 0, sizeof(unsigned long long), st));
+  return check_launch(m, timed(m, kKAdam, st, [&] { return launch_adam(a, m->num_sms, st); }));
+}
+
+// ZeRO-1 after the shard's Adam: GRADS outside the shard back to zero (the
+// shard's part was zeroed by Adam) -- the next accumulation starts from zero.
+static npm_status zero_grads_outside(npm_model* m, int64_t begin, int64_t count, cudaStream_t st) {
+  float* g = m->buf[NPM_BUF_GRADS];
+  if (begin > 0) CUDA_TRY(cudaMemsetAsync(g, 0, (size_t)begin * sizeof(float), st));
+  const int64_t end = begin + count, cap = m->n_total + kBufPad;
+  if (end < cap) CUDA_TRY(cudaMemsetAsync(g + end, 0, (size_t)(cap - end) * sizeof(float), st));
+  return NPM_OK;
+}
+
 static npm_status optimizer(npm_model* m, cudaStream_t st) {
+  if (m->comm && m->exchange == NPM_EXCHANGE_ZERO1 && m->comm_world > 1) {
+    // ZeRO-1: reduce-scatter GRADS, Adam on this rank's 1/P,
+    // all-gather PARAMS, EMA locally over the whole (replicated) vector --
+    // the same result as allreduce + replicated Adam + EMA, with 1/P of the
+    // optimiser's m / v traffic per rank and no EMA exchange
+    int64_t b, c, ch;
+    shard_of(m, m->comm_rank, m->comm_world, b, c, ch);
+    float* g = m->buf[NPM_BUF_GRADS];
+    ncclResult_t e = nccl().reduce_scatter(g, g + b, (size_t)ch, ncclFloat32, ncclSum, m->comm, st);
+    if (e != ncclSuccess) return nccl_fail(e, "ncclReduceScatter(GRADS)");
+    m->t += 1;
+    npm_status r = adam_range(m, b, c, false, st);
+    if (r != NPM_OK) return r;
+    if ((r = zero_grads_outside(m, b, c, st)) != NPM_OK) return r;
+    float* p = m->buf[NPM_BUF_PARAMS];
+    e = nccl().all_gather(p + b, p, (size_t)ch, ncclFloat32, m->comm, st);
+    if (e != ncclSuccess) return nccl_fail(e, "ncclAllGather(PARAMS)");
+    // the statistics of the step are sums over the shards
+    e = nccl().all_reduce(m->dstats + 1, m->dstats + 1, 1, ncclFloat64, ncclSum, m->comm, st);
+    if (e == ncclSuccess) e = nccl().all_reduce(m->dcount + 3, m->dcount + 3, 1, ncclUint64, ncclSum, m->comm, st);
+    if (e != ncclSuccess) return nccl_fail(e, "ncclAllReduce(stats)");
+    return check_launch(m, timed(m, kKAdam, st, [&] {
+      return launch_ema(m->buf[NPM_BUF_EMA], p, m->n_total, m->cfg.ema_decay, m->num_sms, st);
+    }));
+  }
   if (m->comm) {   // A11: the one exchange step -- sum of the ranks' GRADS (each already / N_global)
     const ncclResult_t e = nccl().all_reduce(m->buf[NPM_BUF_GRADS], m->buf[NPM_BUF_GRADS], (size_t)m->n_total,
                                              ncclFloat32, ncclSum, m->comm, st);
     if (e != ncclSuccess) return nccl_fail(e, "ncclAllReduce(GRADS)");
   }
   m->t += 1;
-  const npm_config& c = m->cfg;
-  AdamArgs a;
-  a.n_mlp = m->n_mlp;
-  a.n_total = m->n_total;
-  a.p = m->buf[NPM_BUF_PARAMS]; a.g = m->buf[NPM_BUF_GRADS]; a.m = m->buf[NPM_BUF_ADAM_M];
-  a.v = m->buf[NPM_BUF_ADAM_V]; a.e = m->buf[NPM_BUF_EMA];
-  a.lr = c.lr; a.beta1 = c.beta1; a.beta2 = c.beta2; a.eps = c.adam_eps; a.decay = c.ema_decay;
-  a.c1 = (float)(1.0 / (1.0 - std::pow((double)c.beta1, (double)m->t)));
-  a.c2 = (float)(1.0 / (1.0 - std::pow((double)c.beta2, (double)m->t)));
-  a.gnorm = m->dstats + 1;
-  a.nonfinite = m->dcount + 3;
-  CUDA_TRY(cudaMemsetAsync(m->dstats + 1, 0, sizeof(double), st));
-  CUDA_TRY(cudaMemsetAsync(m->dcount + 3, 0, sizeof(unsigned long long), st));
-  return check_launch(m, timed(m, kKAdam, st, [&] { return launch_adam(a, m->num_sms, st); }));
+  return adam_range(m, 0, m->n_total, true, st);
 }
 
 npm_status npm_train_stream(npm_model* m, const npm_query* q, const float* wix, const float* wiy,
@@ -1400,6 +1478,32 @@ npm_status npm_optimizer_step(npm_model* m, npm_step_stats* stats, void* stream)
     return read_stats(m, st, stats, false, true);
   }
   return NPM_OK;
+}
+
+npm_status npm_optimizer_step_shard(npm_model* m, int rank, int world, npm_step_stats* stats, void* stream) {
+  if (!m || world < 1 || world > kMaxShardWorld || rank < 0 || rank >= world) return fail(NPM_ERR_INVALID, "bad argument");
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t b, c, ch;
+  shard_of(m, rank, world, b, c, ch);
+  m->t += 1;
+  npm_status r = adam_range(m, b, c, false, st);
+  if (r != NPM_OK) return r;
+  if ((r = zero_grads_outside(m, b, c, st)) != NPM_OK) return r;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    return read_stats(m, st, stats, false, true);
+  }
+  return NPM_OK;
+}
+
+npm_status npm_ema_update(npm_model* m, void* stream) {
+  if (!m) return fail(NPM_ERR_INVALID, "null model");
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  return check_launch(m, timed(m, kKAdam, st, [&] {
+    return launch_ema(m->buf[NPM_BUF_EMA], m->buf[NPM_BUF_PARAMS], m->n_total, m->cfg.ema_decay, m->num_sms, st);
+  }));
 }
 
 npm_status npm_train_step(npm_model* m, const npm_query* q, const float* wix, const float* wiy,

@@ -6,6 +6,13 @@
 
 namespace npm {
 namespace detail {
+// EMA blend (C-O18) with a pinned operation order, shared by adam_kernel and
+// ema_kernel so the ZeRO-1 schedule (Adam on a shard, EMA after the gather)
+// reproduces the fused update bit for bit.
+__device__ __forceinline__ float ema_blend(float d, float e, float p) {
+  return __fmaf_rn(d, e, __fmul_rn(1.0f - d, p));
+}
+
 // Adam + EMA (C-O17, C-O18); zeroes the gradient buffer.
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
   // float4 per thread; n_mlp and n_total are multiples of 4, so a vector is
@@ -48,13 +55,14 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
     } else if (gv.x != 0.0f || gv.y != 0.0f || gv.z != 0.0f || gv.w != 0.0f) {
       g4[j] = make_float4(0.f, 0.f, 0.f, 0.f);   // non-finite entries zeroed
     }
-    __stcs(e4 + j, make_float4(a.decay * ev.x + (1.0f - a.decay) * p[0], a.decay * ev.y + (1.0f - a.decay) * p[1],
-                               a.decay * ev.z + (1.0f - a.decay) * p[2], a.decay * ev.w + (1.0f - a.decay) * p[3]));
+    if (a.ema)
+      __stcs(e4 + j, make_float4(ema_blend(a.decay, ev.x, p[0]), ema_blend(a.decay, ev.y, p[1]),
+                                 ema_blend(a.decay, ev.z, p[2]), ema_blend(a.decay, ev.w, p[3])));
   };
   // one float4 per thread per iteration (measured on B200: two per iteration
   // with all loads hoisted was slower, c5 925 -> 1180 us)
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x)
-    body(j, g4[j], p4[j], __ldcs(e4 + j));
+    body(j, g4[j], p4[j], a.ema ? __ldcs(e4 + j) : make_float4(0.f, 0.f, 0.f, 0.f));
   // block reduction, then one atomic per block: per-warp double atomics on
   // one address serialise at its L2 slice (~19 k per c2 step)
   __shared__ double sgn[8];
@@ -292,7 +300,26 @@ int launch_unwind(const UnwindArgs& a, int sms, cudaStream_t st) {
   return 1;
 }
 
+// EMA e <- d e + (1 - d) p (C-O18) over n floats (n % 4 == 0), float4 per thread.
+__global__ void __launch_bounds__(256) ema_kernel(float4* __restrict__ e, const float4* __restrict__ p, int64_t n4,
+                                                  float d) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+    const float4 ev = __ldcs(e + j), pv = p[j];
+    __stcs(e + j, make_float4(ema_blend(d, ev.x, pv.x), ema_blend(d, ev.y, pv.y), ema_blend(d, ev.z, pv.z),
+                              ema_blend(d, ev.w, pv.w)));
+  }
+}
+
+int launch_ema(float* e, const float* p, int64_t n, float decay, int sms, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int64_t need = (n / 4 + 255) / 256;
+  const int blocks = (int)(need < (int64_t)sms * 16 ? need : (int64_t)sms * 16);
+  ema_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(e), reinterpret_cast<const float4*>(p), n / 4, decay);
+  return 1;
+}
+
 int launch_adam(const AdamArgs& a, int sms, cudaStream_t st) {
+  if (a.n_total <= 0) return 0;
   const int64_t need = (a.n_total / 4 + 255) / 256;
   const int blocks = (int)(need < (int64_t)sms * 16 ? need : (int64_t)sms * 16);
   adam_kernel<<<blocks, 256, 0, st>>>(a);

@@ -84,12 +84,15 @@ struct TrainArgs {
 };
 
 struct AdamArgs {
-  int64_t n_mlp, n_total;
+  int64_t n_mlp, n_total;   // of the range processed (a shard: n_mlp relative to its start)
   float *p, *g, *m, *v, *e;
   float lr, beta1, beta2, eps, decay, c1, c2;  // c1 = 1/(1-b1^t), c2 = 1/(1-b2^t)
+  int ema;                  // 1: EMA in the same pass; 0: Adam only (ZeRO-1 shard, EMA after the all-gather)
   double* gnorm;
   unsigned long long* nonfinite;
 };
+// EMA over the whole parameter vector (C-O18), after a sharded Adam step.
+int launch_ema(float* e, const float* p, int64_t n, float decay, int num_sms, cudaStream_t st);
 
 bool shape_supported(const NetShape& s);
 size_t weight_smem_bytes(const NetShape& s);

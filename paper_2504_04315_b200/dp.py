@@ -8,6 +8,8 @@ exchange step of the method.  One optimisation step:
     accumulate_grads(local shard, N_global)   # Eq. 9 -> backprop -> scatter (CUDA)
     all_reduce(GRADS, SUM)                    # NCCL over NVLink/NVSwitch (world > 1)
     optimizer_step()                          # Adam + EMA (CUDA), identical on every rank
+or, with zero1=True (the c5 schedule of SURVEY 8(e)):
+    reduce_scatter(GRADS) -> Adam on this rank's shard -> all_gather(PARAMS) -> EMA
 
 Every rank receives the same reduced bytes and runs the same deterministic
 optimiser kernel, so the replicas stay bitwise identical (no parameter
@@ -49,23 +51,47 @@ class NpmTrainer:
     def optimizer_step(self, want_stats):
         return self.npm.npm_optimizer_step(self.m.h, want_stats, self.m._stream())
 
-    def grad_tensor(self):
+    def grad_tensor(self, count=None):
+        if count is not None:
+            return self.m.buffer_view(self.npm.BUF_GRADS, count)
         if self._grads is None:
             self._grads = self.m.buffer_view(self.npm.BUF_GRADS)
         return self._grads
 
+    # ZeRO-1 building blocks (include/npm.h npm_shard_range ...)
+    def shard_range(self, rank, world):
+        return self.npm.npm_shard_range(self.m.h, rank, world)
+
+    def optimizer_step_shard(self, rank, world, want_stats):
+        return self.npm.npm_optimizer_step_shard(self.m.h, rank, world, want_stats, self.m._stream())
+
+    def param_tensor(self, count):
+        return self.m.buffer_view(self.npm.BUF_PARAMS, count)
+
+    def ema_update(self):
+        self.npm.npm_ema_update(self.m.h, self.m._stream())
+
 
 class DataParallel:
-    def __init__(self, model, world=None, group=None, force_allreduce=False, native=False):
+    def __init__(self, model, world=None, group=None, force_allreduce=False, native=False, zero1=False):
         """native=True (CUDA model only): the library's own NCCL communicator
         (npm_get_unique_id / npm_comm_init, id broadcast over the process
-        group) sums GRADS inside npm_optimizer_step; otherwise GRADS are
-        allreduced here through torch.distributed."""
+        group) exchanges GRADS inside npm_optimizer_step; otherwise the
+        exchange runs here through torch.distributed.
+
+        zero1=True: instead of allreduce + a replicated
+        optimiser, reduce-scatter GRADS, Adam on this rank's 1/P shard,
+        all-gather PARAMS, EMA locally on the whole replicated vector (the EMA
+        is elementwise in the parameters, so it needs no exchange).  The same
+        update as the allreduce schedule; each rank touches the Adam moments
+        of 1/P of the parameters."""
         self.t = model if hasattr(model, "accumulate") else NpmTrainer(model)
         # rank and world are taken within `group` (the default group if None)
         self.world = world if world is not None else (dist.get_world_size(group) if dist.is_initialized() else 1)
         self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.reduce = self.world > 1 or force_allreduce   # force: exercise the collective at world size 1
+        self.zero1 = bool(zero1)
         if native:
             from . import npm
             rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -75,11 +101,42 @@ class DataParallel:
                 src = dist.get_global_rank(group, 0) if group is not None else 0
                 dist.broadcast_object_list(uid, src=src, group=group)
             npm.npm_comm_init(self.t.m.h, rank, self.world, uid[0])
+            if self.zero1:
+                npm.npm_set_exchange(self.t.m.h, npm.EXCHANGE_ZERO1)
             self.reduce = False
+            self.zero1 = False      # the library runs the sharded schedule itself
 
     def allreduce_grads(self):
         if self.reduce:
             dist.all_reduce(self.t.grad_tensor(), op=dist.ReduceOp.SUM, group=self.group)
+
+    def _gloo(self):
+        return dist.get_backend(self.group) == "gloo"
+
+    def zero1_step(self, want_stats):
+        """reduce-scatter GRADS -> Adam on the own shard -> all-gather PARAMS
+        -> EMA over the whole vector.  (gloo has no reduce-scatter: there the
+        shard comes from an allreduce, the same sums.)"""
+        b, c, ch = self.t.shard_range(self.rank, self.world)
+        n = self.world * ch
+        g = self.t.grad_tensor(n)
+        if self._gloo():
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+        else:
+            dist.reduce_scatter_tensor(g[b:b + ch], g, op=dist.ReduceOp.SUM, group=self.group)
+        st = self.t.optimizer_step_shard(self.rank, self.world, want_stats)
+        p = self.t.param_tensor(n)
+        mine = p[b:b + ch].clone()
+        if self._gloo():
+            dist.all_gather(list(p.split(ch)), mine, group=self.group)
+        else:
+            dist.all_gather_into_tensor(p, mine, group=self.group)
+        self.t.ema_update()
+        if want_stats:
+            v = torch.tensor([st["grad_norm_sq"], st["n_nonfinite_grad"]], dtype=torch.float64, device=g.device)
+            dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
+            st = dict(st, grad_norm_sq=v[0].item(), n_nonfinite_grad=int(v[1].item()))
+        return st
 
     def global_count(self, n_local):
         """N_global = sum of the ranks' shard sizes (shards may be unequal,
@@ -97,8 +154,11 @@ class DataParallel:
         if n_global is None:
             n_global = self.global_count(n_local if n_local is not None else q.n)
         st = self.t.accumulate(q, wi, target, spdf, n_global, want_stats)
-        self.allreduce_grads()
-        st2 = self.t.optimizer_step(want_stats)
+        if self.zero1 and self.world > 1:
+            st2 = self.zero1_step(want_stats)
+        else:
+            self.allreduce_grads()
+            st2 = self.t.optimizer_step(want_stats)
         if not want_stats:
             return None
         st = dict(st)

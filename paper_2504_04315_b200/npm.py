@@ -20,6 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NPM_LIB") or os.path.join(_HERE, "libnpm.so")   # NPM_LIB: A/B builds
 
 RADIANCE, PRODUCT = 0, 1
+EXCHANGE_ALLREDUCE, EXCHANGE_ZERO1 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_ADAM_M, BUF_ADAM_V, BUF_EMA = range(5)
 STATUS = {0: "NPM_OK", 1: "NPM_ERR_INVALID", 2: "NPM_ERR_CUDA", 3: "NPM_ERR_NCCL", 4: "NPM_ERR_OOM",
           5: "NPM_ERR_STATE"}
@@ -96,6 +97,10 @@ def _load():
         "npm_optimizer_step": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
         "npm_step_stats_async": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
         "npm_get_unique_id": (I32, [V]),
+        "npm_set_exchange": (I32, [M, I32]),
+        "npm_shard_range": (I32, [M, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "npm_optimizer_step_shard": (I32, [M, I32, I32, ctypes.POINTER(npm_step_stats), V]),
+        "npm_ema_update": (I32, [M, V]),
         "npm_comm_init": (I32, [M, I32, I32, V]),
         "npm_buffer_device_ptr": (I32, [M, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(I64)]),
         "npm_launch_count": (I64, [M]),
@@ -284,6 +289,28 @@ def npm_optimizer_step(h, want_stats=True, stream=None):
     return st.as_dict() if st is not None else None
 
 
+def npm_set_exchange(h, mode):
+    _check(_lib.npm_set_exchange(h, int(mode)))
+
+
+def npm_shard_range(h, rank, world):
+    """(begin, count, chunk) of rank's ZeRO-1 shard of the flat parameter vector."""
+    b, c, ch = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.npm_shard_range(h, int(rank), int(world), ctypes.byref(b), ctypes.byref(c), ctypes.byref(ch)))
+    return b.value, c.value, ch.value
+
+
+def npm_optimizer_step_shard(h, rank, world, want_stats=True, stream=None):
+    st = npm_step_stats() if want_stats else None
+    _check(_lib.npm_optimizer_step_shard(h, int(rank), int(world), ctypes.byref(st) if st is not None else None,
+                                         _stream(stream)))
+    return st.as_dict() if st is not None else None
+
+
+def npm_ema_update(h, stream=None):
+    _check(_lib.npm_ema_update(h, _stream(stream)))
+
+
 def npm_param_count(h):
     a, b = ctypes.c_int64(), ctypes.c_int64()
     _check(_lib.npm_param_count(h, ctypes.byref(a), ctypes.byref(b)))
@@ -416,9 +443,15 @@ class Model:
         q._keep = keep
         return q
 
-    def buffer_view(self, which):
-        """Zero-copy torch view of a model buffer (e.g. GRADS for a collective)."""
+    def buffer_view(self, which, count=None):
+        """Zero-copy torch view of a model buffer (e.g. GRADS for a collective);
+        count > n_params views the zero padding too (<= n_params + 264, the
+        ZeRO-1 world * chunk of npm_shard_range)."""
         p, n = npm_buffer_device_ptr(self.h, which)
+        if count is not None:
+            if count > n + 264:
+                raise ValueError("view beyond the buffer's padding")
+            n = count
         return self.torch.as_tensor(_CudaArray(p, n), device=self.device)
 
     def get(self, which=BUF_PARAMS):

@@ -18,14 +18,49 @@ from paper_2504_04315_b200.dp import DataParallel, shard_range
 from tests.test_oracle_npm import tiny_cfg, random_params, random_batch
 
 
+PAD = 264   # the library's buffer padding past n_params (npm.h npm_shard_range)
+
+
 class OracleTrainer:
-    """DataParallel protocol backed by the float64 oracle (test double)."""
+    """DataParallel protocol backed by the float64 oracle (test double),
+    including the ZeRO-1 building blocks with the library's shard layout."""
 
     def __init__(self, cfg, params):
         from oracle import npm as onpm
         self.onpm = onpm
         self.state = onpm.State(cfg, params.copy())
-        self.grads = torch.zeros(params.size, dtype=torch.float64)
+        self.n = params.size
+        self.gbuf = torch.zeros(self.n + PAD, dtype=torch.float64)
+        self.grads = self.gbuf[:self.n]
+        self.pbuf = torch.zeros(self.n + PAD, dtype=torch.float64)
+
+    def shard_range(self, rank, world):
+        chunk = ((self.n + world - 1) // world + 3) // 4 * 4
+        b = rank * chunk
+        return b, max(0, min(chunk, self.n - b)), chunk
+
+    def optimizer_step_shard(self, rank, world, want_stats):
+        from oracle import adam as oadam
+        st, c = self.state, self.state.cfg
+        b, cnt, _ = self.shard_range(rank, world)
+        g = self.gbuf[:self.n].numpy()[b:b + cnt].copy()
+        st.t += 1
+        sl = slice(b, b + cnt)
+        p, m, v, _, nnf = oadam.adam_ema_step(st.params[sl], g, st.m[sl], st.v[sl], st.ema[sl], st.t,
+                                              self.onpm.grid_mask(c)[sl], c.lr, c.beta1, c.beta2, c.adam_eps,
+                                              c.ema_decay)
+        st.params[sl], st.m[sl], st.v[sl] = p, m, v
+        self.gbuf.zero_()
+        return dict(grad_norm_sq=float(np.sum(np.where(np.isfinite(g), g, 0.0) ** 2)), n_nonfinite_grad=nnf)
+
+    def param_tensor(self, count):
+        self.pbuf[:self.n] = torch.from_numpy(self.state.params)
+        return self.pbuf[:count]
+
+    def ema_update(self):
+        st, d = self.state, self.state.cfg.ema_decay
+        st.params = self.pbuf[:self.n].numpy().copy()
+        st.ema = d * st.ema + (1 - d) * st.params
 
     def accumulate(self, q, wi, target, spdf, n_global, want_stats):
         g, st = self.onpm.gradient(self.state.cfg, self.state.params, q, wi, target, spdf, n_global)
@@ -38,8 +73,8 @@ class OracleTrainer:
         self.grads.zero_()
         return dict(grad_norm_sq=float((g ** 2).sum()), n_nonfinite_grad=nnf)
 
-    def grad_tensor(self):
-        return self.grads
+    def grad_tensor(self, count=None):
+        return self.grads if count is None else self.gbuf[:count]
 
 
 def _free_port():
@@ -190,3 +225,50 @@ def test_two_rank_unequal_shards_infer_n_global_and_stream_stays_in_step():
         _, ref = onpm.train_step(st, dict(x=q["x"][:, idx]), wi[:, idx], tgt[..., idx], pdf[idx], idx.size)
         assert s0[j]["n_used"] == ref["n_used"] and np.isclose(s0[j]["loss_proxy"], ref["loss_proxy"], rtol=1e-12)
     assert np.allclose(p0, st.params, rtol=1e-12, atol=1e-14)
+
+
+def _zero1_worker(rank, world, port, n, steps, zero1, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg, q, wi, tgt, pdf = _batch(n, 12)
+    tr = OracleTrainer(cfg, random_params(cfg, np.random.default_rng(13)))
+    dp = DataParallel(tr, world, zero1=zero1)
+    a, b = shard_range(n, rank, world)
+    sl = lambda x: np.ascontiguousarray(x[..., a:b])
+    stats = [dp.train_step(dict(x=sl(q["x"])), sl(wi), sl(tgt), sl(pdf), n_global=n, want_stats=True)
+             for _ in range(steps)]
+    out[(zero1, rank)] = (tr.state.params.copy(), tr.state.m.copy(), tr.state.v.copy(), tr.state.ema.copy(), stats)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_zero1_sharded_optimiser_equals_replicated_bit_for_bit():
+    """SURVEY 8(e) c5 schedule: reduce-scatter -> Adam on 1/P -> all-gather ->
+    local EMA gives bit for bit the replicated allreduce + Adam + EMA update
+    (2 ranks: the two-term sums are order-free), on every rank, over several
+    steps, with ragged shards (n_params not a multiple of 4 P) and the grid-skip
+    rule crossing a shard boundary."""
+    n, steps, world = 41, 3, 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    for zero1 in (False, True):
+        mp.spawn(_zero1_worker, args=(world, _free_port(), n, steps, zero1, out), nprocs=world, join=True)
+    ref = out[(False, 0)]
+    tr = OracleTrainer(tiny_cfg(), random_params(tiny_cfg(), np.random.default_rng(13)))
+    for rank in range(world):
+        got = out[(True, rank)]
+        # parameters and EMA: replicated, identical everywhere
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[3], ref[3])
+        # Adam moments: each rank keeps only its own shard's (ZeRO-1)
+        b, c, _ = tr.shard_range(rank, world)
+        assert np.array_equal(got[1][b:b + c], ref[1][b:b + c]) and np.array_equal(got[2][b:b + c], ref[2][b:b + c])
+        for sa, sb in zip(got[4], ref[4]):
+            assert sa["n_nonfinite_grad"] == sb["n_nonfinite_grad"]
+            assert np.isclose(sa["grad_norm_sq"], sb["grad_norm_sq"], rtol=1e-12)
+    assert not np.array_equal(ref[0], tr.state.params)
+    # the shards of this tiny model are ragged and the grid-skip boundary
+    # (n_mlp) falls inside rank 0's shard
+    assert tr.n % (4 * world) != 0
+    b1, _, _ = tr.shard_range(1, world)
+    assert 0 < tiny_cfg().n_mlp < b1

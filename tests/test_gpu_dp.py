@@ -50,7 +50,7 @@ def _inputs():
     return CONFIGS[NAME]["model"], ocfg, p, b, b2
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, zero1=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,7 +61,7 @@ def _worker(rank, world, port, out):
     m = npm.Model(0, **model_cfg)
     m.set(npm.BUF_PARAMS, p)
     m.set(npm.BUF_EMA, p)
-    dp = DataParallel(m)
+    dp = DataParallel(m, zero1=zero1)
     assert dp.world == world and dp.reduce
     a, e = shard_range(N, rank, world)
 
@@ -72,14 +72,18 @@ def _worker(rank, world, port, out):
     # step 1 by hand, to read the exchanged gradient before Adam zeroes it
     q, wi, tgt, pdf = shard(b)
     st = dp.t.accumulate(q, wi, tgt, pdf, dp.global_count(e - a), True)
-    dp.allreduce_grads()
-    g = m.get(npm.BUF_GRADS).cpu().numpy()
-    dp.t.optimizer_step(False)
+    if zero1:
+        g = None
+        dp.zero1_step(False)
+    else:
+        dp.allreduce_grads()
+        g = m.get(npm.BUF_GRADS).cpu().numpy()
+        dp.t.optimizer_step(False)
     # step 2 through the driver
     q2, wi2, tgt2, pdf2 = shard(b2)
     dp.train_step(q2, wi2, tgt2, pdf2, n_local=e - a)
     torch.cuda.synchronize()
-    out[rank] = (g, m.get(npm.BUF_PARAMS).cpu().numpy(), m.get(npm.BUF_EMA).cpu().numpy(), st["n_used"])
+    out[(zero1, rank)] = (g, m.get(npm.BUF_PARAMS).cpu().numpy(), m.get(npm.BUF_EMA).cpu().numpy(), st["n_used"])
     dist.barrier()
     m.close()
     dist.destroy_process_group()
@@ -93,8 +97,8 @@ def test_two_rank_cuda_allreduce_matches_union_batch_and_replicas_identical():
     mgr = ctx.Manager()
     out = mgr.dict()
     mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
-    g0, p0, e0, u0 = out[0]
-    g1, p1, e1, u1 = out[1]
+    g0, p0, e0, u0 = out[(False, 0)]
+    g1, p1, e1, u1 = out[(False, 1)]
     # every rank holds the same reduced bytes ...
     assert np.array_equal(g0, g1)
     # ... the oracle's union-batch gradient (C-A13: each rank scaled by 1/N_global)
@@ -110,3 +114,20 @@ def test_two_rank_cuda_allreduce_matches_union_batch_and_replicas_identical():
     # replicas bitwise identical after two optimisation steps
     assert np.array_equal(p0, p1) and np.array_equal(e0, e1)
     assert not np.array_equal(p0, p)      # and they did move
+
+
+def test_two_rank_zero1_schedule_equals_allreduce_schedule_bit_for_bit():
+    """SURVEY 8(e) c5 schedule through the C ABI's ZeRO-1 building blocks
+    (npm_shard_range, npm_optimizer_step_shard, npm_ema_update) on the CUDA
+    model: after two steps every rank's PARAMS and EMA equal, bit for bit, the
+    allreduce + replicated Adam + EMA schedule's (two ranks: order-free sums).
+    (The native NCCL form, npm_set_exchange(ZERO1), needs one GPU per rank.)"""
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    for zero1 in (False, True):
+        mp.start_processes(_worker, args=(2, _free_port(), out, zero1), nprocs=2, join=True, start_method="spawn")
+    _, pr, er, _ = out[(False, 0)]
+    for rank in range(2):
+        _, pz, ez, _ = out[(True, rank)]
+        assert np.array_equal(pz, pr) and np.array_equal(ez, er), rank

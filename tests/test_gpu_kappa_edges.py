@@ -172,14 +172,18 @@ def test_sample_at_kappa_edges(name):
     b = synth.query_batch(n, seed=45)
     u = np.random.default_rng(46).uniform(size=(3, n)).astype(np.float32)
     u[1, :7] = 0.0                   # the u2 = 0 guard of C-O10 at kappa = 1e5
-    wi, pdf = (t.cpu().numpy() for t in m.sample(gq(m, b), u=u))
+    q = gq(m, b)
+    wi, pdf = (t.cpu().numpy() for t in m.sample(q, u=u))
     _, act = onpm.decode(ocfg, p, oq(b, False))
     ow, opdf, _ = ovmf.sample(act, u.astype(np.float64), ocfg.n_lobes)
     ok = ~_boundary_mask(act, u[0].astype(np.float64), ocfg.n_lobes)
     assert ok.mean() > 0.99
     assert np.all(np.isfinite(wi)) and np.all(np.isfinite(pdf))
     assert np.abs(wi[:, ok] - ow[:, ok]).max() <= 1e-4
-    assert (np.abs(pdf[ok] - opdf[ok]) / opdf[ok]).max() <= 1e-3
+    # pdf at the sample: rel 1e-3 widened by the pdf's conditioning (C-A33)
+    tol = pdf_tolerance(m, q, act, ow)
+    rel = np.abs(pdf - opdf) / opdf
+    assert np.all(rel[ok] <= tol[ok]), (rel[ok].max(), tol[ok][rel[ok].argmax()])
     # samples of the kappa = 1e5 lobes really are concentrated
     lobe = np.argmax(u[0][None, :].astype(np.float64) < np.cumsum(act["lam"], axis=0), axis=0)
     sel = ok & (lobe == 0)
