@@ -388,10 +388,19 @@ def main():
     import ctypes
     hstats = torch.zeros(ctypes.sizeof(npm.npm_step_stats), dtype=torch.uint8).pin_memory()
 
+    frame_call = world == 1 or args.native_comm   # the exchange then runs inside the library
+
     def e2e_step(i):
-        npm.npm_sample(m.h, hq, None, 0xC0FFEE, i * n, True, hwi[0], hwi[1], hwi[2], hpdf, hwq[0], hwq[1], hwq[2],
-                       hpdfq, stream=stream)
-        dp.train_step(ht, htwi, httg, htpd, n_local=n, n_global=n * world, want_stats=False)
+        if frame_call:
+            # one host call per frame: queries + records through ONE chunked
+            # host<->device pipeline, then the optimiser (npm_frame_step)
+            npm.npm_frame_step(m.h, hq, None, 0xC0FFEE, i * n, True, hwi[0], hwi[1], hwi[2], hpdf, hwq[0], hwq[1],
+                               hwq[2], hpdfq, ht, htwi[0], htwi[1], htwi[2], httg, httg.shape[0], htpd, n * world,
+                               want_stats=False, stream=stream)
+        else:
+            npm.npm_sample(m.h, hq, None, 0xC0FFEE, i * n, True, hwi[0], hwi[1], hwi[2], hpdf, hwq[0], hwq[1],
+                           hwq[2], hpdfq, stream=stream)
+            dp.train_step(ht, htwi, httg, htpd, n_local=n, n_global=n * world, want_stats=False)
         # the step's loss read back to pinned host memory every step, without a
         # host synchronisation per step (the timed region ends with one)
         npm.npm_step_stats_async(m.h, hstats.data_ptr(), stream=stream)
@@ -563,7 +572,9 @@ def main():
                            "parallelism": "dp%d" % world},
                 "train_samples_per_s": n * world * K / t_t, "queries_per_s": n * world * K / t_q,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                        "host_enqueue_ms_per_step": host_enqueue_ms},
+                        "host_enqueue_ms_per_step": host_enqueue_ms,
+                        "call": "npm_frame_step (one pipeline per frame)" if frame_call else
+                                "npm_sample + DataParallel.train_step (torch.distributed exchange)"},
                 "gpu_launches": launches, "gpu_launches_per_step": launches / K,
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
                 "clocks": clk.summary(), "cpu_baseline": cpu, "strong_c3": strong, "paper_context": paper_ctx,

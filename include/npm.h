@@ -291,6 +291,23 @@ npm_status npm_accumulate_grads(npm_model* model, const npm_query* q, const floa
                                 npm_step_stats* stats, void* stream);
 npm_status npm_optimizer_step(npm_model* model, npm_step_stats* stats, void* stream);
 
+/* One frame of the hot path in one call: npm_sample over the query batch q
+ * (same arguments, including the optional fused pdf at caller directions),
+ * then npm_accumulate_grads over the records tq, then npm_optimizer_step
+ * (with the attached communicator's exchange).  Results equal the three
+ * calls.  When every array is a host pointer, q->n == tq->n (one record per
+ * queried vertex, the paper's per-frame stream) and n >= 131,072, both
+ * phases' host<->device copies run in ONE chunked pipeline: chunk j's query
+ * and training inputs move together and chunk j's kernels (queries, then the
+ * records' gradient) run while chunk j+1 uploads and chunk j-1's outputs
+ * download -- one pipeline fill and one drain per frame instead of two.
+ * stats as npm_train_step (NULL: no host synchronisation). */
+npm_status npm_frame_step(npm_model* model, const npm_query* q, const float* u, uint64_t seed, uint64_t offset,
+                          int use_ema, float* wix, float* wiy, float* wiz, float* pdf, const float* qx,
+                          const float* qy, const float* qz, float* pdf_q, const npm_query* tq, const float* twx,
+                          const float* twy, const float* twz, const float* target, int target_channels,
+                          const float* sample_pdf, int64_t n_global, npm_step_stats* stats, void* stream);
+
 /* Multi-GPU (A11): rank 0 calls npm_get_unique_id and shares
  * the 128-byte id with the other ranks (e.g. over the torch process group);
  * every rank then attaches a communicator with npm_comm_init (one process per

@@ -1269,6 +1269,18 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       fprintf(stderr, "NPM_PHASES tiles=%d total=%.0f", cnt, cnt ? acc[0] / cnt : 0.0);
       for (int j = 1; j < 16; ++j) fprintf(stderr, " p%d=%.0f", j, cnt ? acc[j] / cnt : 0.0);
       fprintf(stderr, "\n");
+      // the same stamps as cycles since the tile's stamp 0 (stamp indices need
+      // not be in time order)
+      double since[16] = {};
+      int cs = 0;
+      for (int t = 1; t < 64; ++t) {
+        if (h[t * 16 + 15] == 0) break;
+        for (int j = 1; j < 16; ++j) if (h[t * 16 + j]) since[j] += (double)(h[t * 16 + j] - h[t * 16]);
+        ++cs;
+      }
+      fprintf(stderr, "NPM_STAMPS");
+      for (int j = 1; j < 16; ++j) fprintf(stderr, " s%d=%.0f", j, cs ? since[j] / cs : 0.0);
+      fprintf(stderr, "\n");
       if (r != NPM_OK || !a.priv_mask) return r;
       return fold_priv(m, st);
     }
@@ -1504,6 +1516,109 @@ npm_status npm_ema_update(npm_model* m, void* stream) {
   return check_launch(m, timed(m, kKAdam, st, [&] {
     return launch_ema(m->buf[NPM_BUF_EMA], m->buf[NPM_BUF_PARAMS], m->n_total, m->cfg.ema_decay, m->num_sms, st);
   }));
+}
+
+npm_status npm_frame_step(npm_model* m, const npm_query* q, const float* u, uint64_t seed, uint64_t offset,
+                          int use_ema, float* wix, float* wiy, float* wiz, float* pdf, const float* qx,
+                          const float* qy, const float* qz, float* pdf_q, const npm_query* tq, const float* twx,
+                          const float* twy, const float* twz, const float* target, int channels,
+                          const float* spdf, int64_t n_global, npm_step_stats* stats, void* stream) {
+  if (!m || !query_ok(m, q) || (q->n > 0 && (!wix || !wiy || !wiz || !pdf)))
+    return fail(NPM_ERR_INVALID, "bad argument");
+  if (!train_args_ok(m, tq, twx, twy, twz, target, channels, spdf, n_global)) return fail(NPM_ERR_INVALID, "bad argument");
+  const bool fused = qx && qy && qz && pdf_q;
+  if ((qx || qy || qz || pdf_q) && !fused) return fail(NPM_ERR_INVALID, "fused query needs qx, qy, qz, pdf_q");
+  if (stats) memset(stats, 0, sizeof(*stats));
+  DeviceGuard g(m->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool prod = m->cfg.mode == NPM_PRODUCT;
+  // one chunked pipeline over both phases when every array is a host pointer
+  // and the two batches have the same size (a record per queried vertex)
+  if (q->n == tq->n && q->n > 0 &&
+      HostPipe::usable(m, q->n, {q->px, q->py, q->pz, prod ? q->wox : nullptr, prod ? q->nx : nullptr,
+                                 prod ? q->rough : nullptr, u, qx, wix, pdf, pdf_q, tq->px, tq->py, tq->pz,
+                                 prod ? tq->wox : nullptr, prod ? tq->nx : nullptr, prod ? tq->rough : nullptr, twx,
+                                 twy, twz, target, spdf})) {
+    std::lock_guard<std::mutex> lk(m->stage_mu);
+    HostPipe hp{m, st, q->n};
+    auto cond = [&](const npm_query* qq, HostPipe::Tri& two, HostPipe::Tri& tn, int& kr) {
+      if (!prod) return;
+      two = hp.in3(qq->wox, qq->woy, qq->woz);
+      tn = hp.in3(qq->nx, qq->ny, qq->nz);
+      kr = (int)hp.ins.size();
+      hp.ins.push_back({qq->rough, nullptr, 1});
+    };
+    const HostPipe::Tri tx = hp.in3(q->px, q->py, q->pz);
+    HostPipe::Tri two{}, tn{}, ttwo{}, ttn{};
+    int kr = -1, tkr = -1;
+    cond(q, two, tn, kr);
+    const int ku = u ? (int)hp.ins.size() : -1;
+    if (u) hp.ins.push_back({u, nullptr, 3});
+    HostPipe::Tri tqd{};
+    if (fused) tqd = hp.in3(qx, qy, qz);
+    const HostPipe::Tri ttx = hp.in3(tq->px, tq->py, tq->pz);
+    cond(tq, ttwo, ttn, tkr);
+    const HostPipe::Tri tw = hp.in3(twx, twy, twz);
+    const int kt = (int)hp.ins.size();
+    hp.ins.push_back({target, nullptr, channels});
+    hp.ins.push_back({spdf, nullptr, 1});
+    const HostPipe::Tri to = hp.out3(wix, wiy, wiz);
+    const int kp = (int)hp.outs.size();
+    hp.outs.push_back({nullptr, pdf, 1});
+    const int kpq = (int)hp.outs.size();
+    if (fused) hp.outs.push_back({nullptr, pdf_q, 1});
+    const npm_status r = hp.run([&](int j, int64_t c) -> npm_status {
+      // queries of chunk j (EMA or live weights; GRADS untouched) ...
+      npm_query d{};
+      d.n = c;
+      d.px = hp.din3(tx, 0, j); d.py = hp.din3(tx, 1, j); d.pz = hp.din3(tx, 2, j);
+      if (prod) {
+        d.wox = hp.din3(two, 0, j); d.woy = hp.din3(two, 1, j); d.woz = hp.din3(two, 2, j);
+        d.nx = hp.din3(tn, 0, j); d.ny = hp.din3(tn, 1, j); d.nz = hp.din3(tn, 2, j); d.rough = hp.din(kr, j);
+      }
+      QueryArgs a;
+      fill_query_args(m, d, use_ema, a);
+      a.do_sample = 1;
+      a.u = ku >= 0 ? hp.din(ku, j) : nullptr;
+      a.seed = seed;
+      a.offset = offset + (uint64_t)j * (uint64_t)hp.C;   // Philox counter = global sample index
+      if (fused) {
+        a.wx = hp.din3(tqd, 0, j); a.wy = hp.din3(tqd, 1, j); a.wz = hp.din3(tqd, 2, j);
+        a.pdf = hp.dout(kpq, j);
+      }
+      a.sx = hp.dout3(to, 0, j); a.sy = hp.dout3(to, 1, j); a.sz = hp.dout3(to, 2, j); a.spdf = hp.dout(kp, j);
+      npm_status rr = maybe_bin(m, a.px, a.py, a.pz, a.n, st, &a.perm);
+      if (rr == NPM_OK) rr = query_launch(m, a, st);
+      if (rr != NPM_OK) return rr;
+      // ... then the records of chunk j into GRADS
+      npm_query dt{};
+      dt.n = c;
+      dt.px = hp.din3(ttx, 0, j); dt.py = hp.din3(ttx, 1, j); dt.pz = hp.din3(ttx, 2, j);
+      if (prod) {
+        dt.wox = hp.din3(ttwo, 0, j); dt.woy = hp.din3(ttwo, 1, j); dt.woz = hp.din3(ttwo, 2, j);
+        dt.nx = hp.din3(ttn, 0, j); dt.ny = hp.din3(ttn, 1, j); dt.nz = hp.din3(ttn, 2, j); dt.rough = hp.din(tkr, j);
+      }
+      Stager s2{m, st};   // device chunk pointers: pass-through
+      return accumulate(m, &dt, hp.din3(tw, 0, j), hp.din3(tw, 1, j), hp.din3(tw, 2, j), hp.din(kt, j), channels,
+                        hp.din(kt + 1, j), n_global, st, s2, -1, j == 0);
+    });
+    if (r != NPM_OK) return fail(r, hp.err != cudaSuccess ? cudaGetErrorString(hp.err) : "pipelined frame step");
+  } else {
+    npm_status r = npm_sample(m, q, u, seed, offset, use_ema, wix, wiy, wiz, pdf, qx, qy, qz, pdf_q, stream);
+    if (r != NPM_OK) return r;
+    if (tq->n > 0) {
+      std::lock_guard<std::mutex> lk(m->stage_mu);
+      Stager s{m, st};
+      if ((r = accumulate(m, tq, twx, twy, twz, target, channels, spdf, n_global, st, s)) != NPM_OK) return r;
+    } else {
+      CUDA_TRY(cudaMemsetAsync(m->dstats, 0, sizeof(double), st));
+      CUDA_TRY(cudaMemsetAsync(m->dcount, 0, 3 * sizeof(unsigned long long), st));
+    }
+  }
+  npm_status r = optimizer(m, st);
+  if (r != NPM_OK) return r;
+  if (stats) return read_stats(m, st, stats, true, true);
+  return NPM_OK;
 }
 
 npm_status npm_train_step(npm_model* m, const npm_query* q, const float* wix, const float* wiy,

@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
         for (int m = 0; m < KL; ++m) {
           mloc = fmaxf(mloc, lp[m]);
           kap[m] = __expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
-          lobe_angles(tp[m], pp[m], kap[m], th[m], ph[m], sth[m], cth[m], sph[m], cph[m]);
+          lobe_angles<false>(tp[m], pp[m], kap[m], th[m], ph[m], sth[m], cth[m], sph[m], cph[m]);
           mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
           const float nrm = lobe_norm_fast(kap[m], emk[m]);
           vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);

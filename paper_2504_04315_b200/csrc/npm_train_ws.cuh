@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
           tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + 2 * K + h * KH), tp);
           tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + 3 * K + h * KH), pp);
           tc::tmem_wait_ld();
+          NPM_WS_STAMP(10);
 #pragma unroll
           for (int m = 0; m < KH; ++m) {
             lp[m] += b[h * KH + m];
@@ -398,12 +399,13 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
           for (int m = 0; m < KH; ++m) {
             mloc = fmaxf(mloc, lp[m]);
             kap[m] = __expf(fminf(fmaxf(kp[m], a.log_kmin), a.log_kmax));
-            lobe_angles(tp[m], pp[m], kap[m], th[m], ph[m], sth[m], cth[m], sph[m], cph[m]);
+            lobe_angles<false>(tp[m], pp[m], kap[m], th[m], ph[m], sth[m], cth[m], sph[m], cph[m]);
             mx[m] = sth[m] * cph[m]; my[m] = sth[m] * sph[m]; mz[m] = cth[m];
             const float nrm = lobe_norm_fast(kap[m], emk[m]);
             vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);
           }
           // softmax max / normaliser / mixture sum across the row's two threads
+          NPM_WS_STAMP(12);
           xch[(h * 3 + 0) * R + r] = mloc;
           psync();
           float M = xch[0 * R + r];
@@ -419,6 +421,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
           xch[(h * 3 + 1) * R + r] = S;
           xch[(h * 3 + 2) * R + r] = P;
           psync();
+          NPM_WS_STAMP(14);
           // the same association order on every thread of the row: parts 0, 1, ...
           float St = 0.0f, Pt = 0.0f;
 #pragma unroll

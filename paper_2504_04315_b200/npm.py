@@ -96,6 +96,8 @@ def _load():
                                    ctypes.POINTER(npm_step_stats), V]),
         "npm_optimizer_step": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
         "npm_step_stats_async": (I32, [M, ctypes.POINTER(npm_step_stats), V]),
+        "npm_frame_step": (I32, [M, ctypes.POINTER(npm_query), V, U64, U64, I32, V, V, V, V, V, V, V, V,
+                                 ctypes.POINTER(npm_query), V, V, V, V, I32, V, I64, ctypes.POINTER(npm_step_stats), V]),
         "npm_get_unique_id": (I32, [V]),
         "npm_set_exchange": (I32, [M, I32]),
         "npm_shard_range": (I32, [M, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
@@ -286,6 +288,16 @@ def npm_accumulate_grads(h, q, wx, wy, wz, target, channels, spdf, n_global, wan
 def npm_optimizer_step(h, want_stats=True, stream=None):
     st = npm_step_stats() if want_stats else None
     _check(_lib.npm_optimizer_step(h, ctypes.byref(st) if st is not None else None, _stream(stream)))
+    return st.as_dict() if st is not None else None
+
+
+def npm_frame_step(h, q, u, seed, offset, use_ema, wx, wy, wz, pdf, qx, qy, qz, pdf_q, tq, twx, twy, twz, target,
+                   channels, spdf, n_global, want_stats=True, stream=None):
+    st = npm_step_stats() if want_stats else None
+    _check(_lib.npm_frame_step(h, ctypes.byref(q), _ptr(u), int(seed), int(offset), int(use_ema), _ptr(wx), _ptr(wy),
+                               _ptr(wz), _ptr(pdf), _ptr(qx), _ptr(qy), _ptr(qz), _ptr(pdf_q), ctypes.byref(tq),
+                               _ptr(twx), _ptr(twy), _ptr(twz), _ptr(target), int(channels), _ptr(spdf),
+                               int(n_global), ctypes.byref(st) if st is not None else None, _stream(stream)))
     return st.as_dict() if st is not None else None
 
 

@@ -116,18 +116,58 @@ def test_two_rank_cuda_allreduce_matches_union_batch_and_replicas_identical():
     assert not np.array_equal(p0, p)      # and they did move
 
 
+def _zero1_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2504_04315_b200 import npm
+    from paper_2504_04315_b200.dp import DataParallel
+    model_cfg, ocfg, p, _, _ = _inputs()
+    ma, mz = npm.Model(0, **model_cfg), npm.Model(0, **model_cfg)
+    for m in (ma, mz):
+        m.set(npm.BUF_PARAMS, p)
+        m.set(npm.BUF_EMA, p)
+    da, dz = DataParallel(ma), DataParallel(mz, zero1=True)
+    rng = np.random.default_rng(70 + rank)
+    stats = []
+    for step in range(3):
+        # the same per-rank gradient into both models (the scatter's atomics
+        # would make two accumulations differ in their last bits); exact zeros
+        # in the grid part exercise the skip rule, a NaN the non-finite count
+        g = (rng.normal(size=ma.n_params) * 1e-3).astype(np.float32)
+        g[ma.n_mlp:][rng.uniform(size=ma.n_grid) < 0.5] = 0.0
+        g[rank + 3 * step] = np.nan
+        ma.set(npm.BUF_GRADS, g)
+        mz.set(npm.BUF_GRADS, g)
+        da.allreduce_grads()
+        sa = da.t.optimizer_step(True)
+        sz = dz.zero1_step(True)
+        stats.append((sa, sz))
+    torch.cuda.synchronize()
+    out[rank] = tuple(m.get(b).cpu().numpy() for m in (ma, mz) for b in (npm.BUF_PARAMS, npm.BUF_EMA)) + (stats,)
+    dist.barrier()
+    ma.close(); mz.close()
+    dist.destroy_process_group()
+
+
 def test_two_rank_zero1_schedule_equals_allreduce_schedule_bit_for_bit():
     """SURVEY 8(e) c5 schedule through the C ABI's ZeRO-1 building blocks
     (npm_shard_range, npm_optimizer_step_shard, npm_ema_update) on the CUDA
-    model: after two steps every rank's PARAMS and EMA equal, bit for bit, the
-    allreduce + replicated Adam + EMA schedule's (two ranks: order-free sums).
-    (The native NCCL form, npm_set_exchange(ZERO1), needs one GPU per rank.)"""
+    model: from identical per-rank GRADS, three steps of reduce-scatter ->
+    Adam on the shard -> all-gather -> EMA give every rank's PARAMS and EMA
+    bit for bit equal to allreduce + replicated Adam + EMA (two ranks:
+    order-free sums), and the same statistics.  (The native NCCL form,
+    npm_set_exchange(ZERO1), needs one GPU per rank.)"""
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
-    for zero1 in (False, True):
-        mp.start_processes(_worker, args=(2, _free_port(), out, zero1), nprocs=2, join=True, start_method="spawn")
-    _, pr, er, _ = out[(False, 0)]
+    mp.start_processes(_zero1_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    ref_p, ref_e = out[0][0], out[0][1]
     for rank in range(2):
-        _, pz, ez, _ = out[(True, rank)]
-        assert np.array_equal(pz, pr) and np.array_equal(ez, er), rank
+        pa, ea, pz, ez, stats = out[rank]
+        assert np.array_equal(pa, ref_p) and np.array_equal(ea, ref_e)
+        assert np.array_equal(pz, ref_p) and np.array_equal(ez, ref_e), rank
+        for sa, sz in stats:
+            assert sa["n_nonfinite_grad"] == sz["n_nonfinite_grad"] == 2
+            assert np.isclose(sa["grad_norm_sq"], sz["grad_norm_sq"], rtol=1e-6)

@@ -120,3 +120,39 @@ def test_binned_queries_on_two_streams_with_different_sizes():
         got = [t.cpu().numpy() for t in o]
         for a, b in zip(got, ref[j % 2]):
             assert np.array_equal(a, b), j
+
+
+@pytest.mark.parametrize("pipelined", [True, False])
+def test_frame_step_equals_sample_then_train_step(pipelined):
+    """npm_frame_step (one pipeline over a frame's queries and records) gives
+    the query outputs of npm_sample bit for bit and the training step's
+    statistics (loss proxy, record counts, gradient norm) of
+    npm_accumulate_grads + npm_optimizer_step; the post-step parameters agree
+    to the Adam amplification bound (2 lr) and mostly exactly."""
+    n = 300007 if pipelined else 5003
+    b = synth.query_batch(n, seed=51)
+    tb = synth.training_batch(n, seed=52, rgb=True)
+    H = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    res = []
+    for fused in (True, False):
+        m, _, _ = make_pair("c2", seed=50)
+        hx, hw, tx, twi, ttg, tpd = H(b["x"]), H(b["wq"]), H(tb["x"]), H(tb["wi"]), H(tb["target"]), H(tb["pdf"])
+        hq = npm.make_query(n, hx[0], hx[1], hx[2])
+        ht = npm.make_query(n, tx[0], tx[1], tx[2])
+        wi, pdf, pdfq = H(np.zeros((3, n), np.float32)), H(np.zeros(n, np.float32)), H(np.zeros(n, np.float32))
+        if fused:
+            st = npm.npm_frame_step(m.h, hq, None, 5, 77, 1, wi[0], wi[1], wi[2], pdf, hw[0], hw[1], hw[2], pdfq,
+                                    ht, twi[0], twi[1], twi[2], ttg, 3, tpd, n)
+        else:
+            npm.npm_sample(m.h, hq, None, 5, 77, 1, wi[0], wi[1], wi[2], pdf, hw[0], hw[1], hw[2], pdfq)
+            st = npm.npm_train_step(m.h, ht, twi[0], twi[1], twi[2], ttg, 3, tpd, n)
+        torch.cuda.synchronize()
+        res.append((wi.numpy().copy(), pdf.numpy().copy(), pdfq.numpy().copy(), st, m.get(npm.BUF_PARAMS).cpu().numpy()))
+    (w0, p0, q0, s0, par0), (w1, p1, q1, s1, par1) = res
+    assert np.array_equal(w0, w1) and np.array_equal(p0, p1) and np.array_equal(q0, q1)
+    for k in ("n_used", "n_zero_target", "n_dropped", "n_nonfinite_grad"):
+        assert s0[k] == s1[k], k
+    assert abs(s0["loss_proxy"] - s1["loss_proxy"]) <= 1e-5 * abs(s1["loss_proxy"])
+    assert abs(s0["grad_norm_sq"] - s1["grad_norm_sq"]) <= 1e-3 * s1["grad_norm_sq"]
+    d = np.abs(par0.astype(np.float64) - par1)
+    assert d.max() <= 2 * 5e-3 + 1e-6 and (d == 0).mean() > 0.9
