@@ -96,10 +96,11 @@ struct WS {
 };
 
 // mbarrier wait that traps instead of hanging (a legitimate wait here is
-// microseconds; ~4 s of polling means a protocol bug)
+// microseconds; 2^28 polls means a protocol bug).  An iteration count, not
+// clock64: the clock reads and 64-bit compares of every poll were issue slots
+// taken from the chain warps (ncu r02s: polling was ~26 % of issued instructions).
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
-  const long long t0 = clock64();
-  uint32_t ok = 0;
+  uint32_t ok = 0, it = 0;
   while (true) {
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
@@ -107,25 +108,23 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
         "selp.u32 %0, 1, 0, P;\n\t}\n"
         : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
     if (ok) return;
-    if (clock64() - t0 > (8LL << 30)) __trap();
+    if (++it > (1u << 28)) __trap();
   }
 }
 
-// the same for warps with nothing else to do: back off between polls so the
-// chain warps get the issue slots (ncu r02h: the polling memory warps were
-// 21 % of all stall samples)
+// the same for warps with nothing else to do: try_wait with a suspend-time
+// hint -- the warp sleeps in the instruction until the phase completes (or
+// the hint expires) instead of spinning on issue slots the chain needs
 __device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
-  const long long t0 = clock64();
-  uint32_t ok = 0;
+  uint32_t ok = 0, it = 0;
   while (true) {
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P;\n\t}\n"
-        : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+        : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity), "r"(100000u) : "memory");
     if (ok) return;
-    __nanosleep(128);
-    if (clock64() - t0 > (8LL << 30)) __trap();
+    if (++it > (1u << 24)) __trap();
   }
 }
 
@@ -282,7 +281,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
     };
     auto psync = [&]() { tc::named_sync(2u + (uint32_t)(warp & 3), 32u * TPR); };
     auto wait_mma = [&]() {
-      tc::mbar_wait(bar_mma, phase);
+      tc::mbar_wait(bar_mma, phase);   // (a suspend hint here: +2 % on B200 c2)
       phase ^= 1u;
       tc::fence_after_sync();
     };
