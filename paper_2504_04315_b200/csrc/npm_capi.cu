@@ -618,7 +618,6 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   m->device = dev;
   m->shape = s;
   if (const char* e = getenv("NPM_BIN")) m->use_bin = !(e[0] == '0');
-  if (const char* e = getenv("NPM_TRAIN_WS")) m->train_ws = atoi(e);
   if (const char* e = getenv("NPM_PIPELINE")) m->pipeline = !(e[0] == '0');
   if (const char* e = getenv("NPM_PIPE_CHUNKS")) m->pipe_chunks = atoi(e) > 0 ? atoi(e) : 3;
   // Query kernel layout: two 256-thread CTAs per SM, or one CTA running two
@@ -669,6 +668,13 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // or slower (the binned scatter-adds collide on L2 lines).
   m->bin_train = m->n_grid * 4 > ((int64_t)64 << 20);
   if (const char* e = getenv("NPM_BIN_TRAIN")) m->bin_train = e[0] == '1';
+  // Training kernel per shape (B200 measurements): the warp-
+  // specialised kernel for L2-resident tables (c2 612 vs 632 us; c3 equal);
+  // the r01 two-group kernel for HBM-resident tables, whose binned,
+  // privatised scatter it does not have (c5 4.8 vs 6.3 ms), and for the
+  // product shape (no warp-specialised instantiation).
+  m->train_ws = (m->bin_train || c.mode == NPM_PRODUCT) ? 0 : 1;
+  if (const char* e = getenv("NPM_TRAIN_WS")) m->train_ws = atoi(e);
   // Privatise the scatter of small (coarse) levels when training batches are
   // binned: coherent records then add to the same few coarse entries from
   // every SM and the reductions queue on the same L2 lines.  Each SM

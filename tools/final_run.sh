@@ -1,8 +1,10 @@
+# full verification of HEAD on a fresh box (round 2)
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r01f_pytest_gpu.log 2>&1; echo "pytest_gpu rc=$?" >> gpurun_out/r01f_pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r01f_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r01f_smoke.log
-timeout 600 python bench.py > gpurun_out/r01f_bench_default.json 2> gpurun_out/r01f_bench_default.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r01f_bench_reference.json 2> gpurun_out/r01f_bench_reference.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01f_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/r01f_ncu_launch.log 2>&1
+T=${TAG:-r02v}
+timeout 1500 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/${T}_pytest_gpu.log 2>&1; echo "pytest_gpu rc=$?" >> gpurun_out/${T}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${T}_smoke.log
+timeout 600 python bench.py > gpurun_out/${T}_bench_default.json 2> gpurun_out/${T}_bench_default.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_bench_reference.json 2> gpurun_out/${T}_bench_reference.err
+for w in c3 c4 c5; do timeout 600 python bench.py --workload $w --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err; done
 echo done
