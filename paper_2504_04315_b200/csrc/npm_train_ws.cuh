@@ -70,8 +70,9 @@ struct WS {
   static constexpr uint32_t OFF_DZ = OFF_RD + (uint32_t)S0 * RD_BYTES;
   static constexpr uint32_t OFF_XCH = (OFF_DZ + DZ_BYTES + 15u) & ~15u;   // head exchange [TPR][3][R] f32
   static constexpr uint32_t OFF_BAR = OFF_XCH + 3u * TPR * R * 4u;
-  // mbarriers: [0] weights, [1] mma, [2] dz full, [3] dz empty, [4..4+S0) x0 full, [4+S0..4+2 S0) x0 empty
-  static constexpr int NBAR = 4 + 2 * S0;
+  // mbarriers: [0] weights, [1] mma, [2] dz full, [3] dz empty, [4..4+S0) x0 full, [4+S0..4+2 S0) x0 empty,
+  // [4+2 S0] head start (the scatter of tile k-1 waits for tile k's head)
+  static constexpr int NBAR = 5 + 2 * S0;
   static constexpr uint32_t OFF_TSLOT = OFF_BAR + 8u * NBAR;
   static constexpr uint32_t SMEM_RAW = OFF_TSLOT + 16u;
   // dW^T MMAs read M_k / 8 feature chunks from a lo base (M_k = 64 or 128):
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
   uint64_t* bar_mma = bars + 1;
   uint64_t* bar_dzf = bars + 2;
   uint64_t* bar_dze = bars + 3;
+  uint64_t* bar_hs = bars + 4 + 2 * S0;
   uint64_t* bar_x0f = bars + 4;
   uint64_t* bar_x0e = bars + 4 + S0;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_TSLOT);
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
     tc::mbar_init(bar_mma, 1);
     tc::mbar_init(bar_dzf, T::CHAIN_THREADS);
     tc::mbar_init(bar_dze, T::SCATTER_THREADS);
+    tc::mbar_init(bar_hs, 1);
     for (int s = 0; s < S0; ++s) {
       tc::mbar_init(bar_x0f + s, T::GATHER_THREADS);
       tc::mbar_init(bar_x0e + s, 1);
@@ -285,10 +288,13 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
       phase ^= 1u;
       tc::fence_after_sync();
     };
-    // previous tile's dz -> dz stage (run while the next tile's first MMA executes)
-    struct Prev { float ux, uy, uz; float valid; };
-    Prev prev{0.f, 0.f, 0.f, 0.f};
-    auto dz_epilogue = [&](const Prev& pv, int kk) {
+    // previous tile's dz -> dz stage (run while the next tile's first MMA
+    // executes).  Its row data (position, validity) is read from its row-data
+    // stage here: that stage is refilled only by the gather of tile kk + S0,
+    // which the memory warps start after scattering tile kk, i.e. after the
+    // dz_full this epilogue arrives on.
+    auto dz_epilogue = [&](int kk) {
+      const float* rdp = reinterpret_cast<const float*>(smem + T::OFF_RD + (uint32_t)(kk % S0) * T::RD_BYTES);
       float v[NG / TPR];
       tc::tmem_ldn<NG / TPR>(tbase + lad + (uint32_t)(T::C_DZ + h * (NG / TPR)), v);
       tc::tmem_wait_ld();
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
         dz[(h * LH + l) * R + r] = make_float4(v[4 * l], v[4 * l + 1], v[4 * l + 2], v[4 * l + 3]);
       if (h == 0) {
         float* uu = reinterpret_cast<float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
-        uu[r] = pv.ux; uu[R + r] = pv.uy; uu[2 * R + r] = pv.uz; uu[3 * R + r] = pv.valid;
+        uu[r] = rdp[r]; uu[R + r] = rdp[R + r]; uu[2 * R + r] = rdp[2 * R + r]; uu[3 * R + r] = rdp[3 * R + r];
       }
       mbar_arrive(bar_dzf);
     };
@@ -320,15 +326,12 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
                        TB::in_p(0), TB::out(0));
         tc::mma_commit(bar_mma);
       }
-      // this row's inputs (read now: the stage is refilled once bwd_0 completes)
+      // this row's head inputs are read from the row-data stage at the head
+      // (the stage is refilled only after bwd_0 completes): no registers held
+      // across the forward epilogues (they spilled there)
       const float* rd = reinterpret_cast<const float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
-      Prev cur{rd[r], rd[R + r], rd[2 * R + r], rd[3 * R + r]};
-      const float h_wx = rd[4 * R + r], h_wy = rd[5 * R + r], h_wz = rd[6 * R + r];
-      const float h_t0 = rd[7 * R + r], h_t1 = rd[8 * R + r], h_t2 = rd[9 * R + r], h_p = rd[10 * R + r];
-      const bool hvalid = cur.valid != 0.0f;
-      if (kt > 0) dz_epilogue(prev, kt - 1);
+      if (kt > 0) dz_epilogue(kt - 1);
       NPM_WS_STAMP(2);
-      uint32_t mask[NL];   // ReLU'(X_k) of this thread's W/2 columns (bit j: column h W/2 + j)
       // ---- forward
 #pragma unroll
       for (int k = 0; k < NL; ++k) {
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
         const float* b = bias + TB::boff(k) / 4;
         if (k < NL - 1) {
           const uint32_t xh = sb + T::xhoff(k + 1), xl = xh + (T::HF / 8) * CHR;
-          uint32_t mk = 0;
+
 #pragma unroll
           for (int c16 = 0; c16 < WH; c16 += 16) {   // 16 columns at a time (register pressure)
             float v[16];
@@ -356,13 +359,13 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               v[j] = fmaxf(v[j] + b[h * WH + c16 + j], 0.0f);
-              mk |= (v[j] > 0.0f ? 1u : 0u) << (c16 + j);
+
             }
             tc::store_chunk(xh, xl, R, r, h * (WH / 8) + c16 / 8, v);
             tc::store_chunk(xh, xl, R, r, h * (WH / 8) + c16 / 8 + 1, v + 8);
           }
-          mask[k + 1] = mk;
         } else {
+          if (tid == 0) mbar_arrive(bar_hs);   // the memory warps may scatter now
           // ---- Eq. 9 head (C-O12, C-O13): row r, lobes [h K/2, (h+1) K/2)
           float lp[KH], kp[KH], tp[KH], pp[KH];
           tc::tmem_ldn<KH>(tbase + lad + (uint32_t)(T::C_ACC + h * KH), lp);
@@ -378,13 +381,16 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
             tp[m] += b[2 * K + h * KH + m];
             pp[m] += b[3 * K + h * KH + m];
           }
-          float t = h_t0;
+          const bool hvalid = rd[3 * R + r] != 0.0f;
+          const float h_wx = rd[4 * R + r], h_wy = rd[5 * R + r], h_wz = rd[6 * R + r];
+          float t = rd[7 * R + r];
           bool all_zero = t == 0.0f;
           if (a.channels == 3) {
+            const float h_t1 = rd[8 * R + r], h_t2 = rd[9 * R + r];
             all_zero = all_zero && h_t1 == 0.0f && h_t2 == 0.0f;
             t = 0.2126f * t + 0.7152f * h_t1 + 0.0722f * h_t2;
           }
-          const float p = h_p;
+          const float p = rd[10 * R + r];
           const float ratio = t / p;
           const bool drop = hvalid && (!isfinite(ratio) || !isfinite(p) || !(p > 0.0f));
           const bool zero = hvalid && !drop && all_zero;
@@ -487,24 +493,42 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
         if (k > 0) {
           // delta_{k-1} = dX_k * ReLU'(X_k) -> over X_k (read by dW_k, complete)
           const uint32_t dh = sb + T::dboff(k - 1), dl = dh + (T::dfeat(k - 1) / 8) * CHR;
-          const uint32_t mk = mask[k];
 #pragma unroll
           for (int c16 = 0; c16 < WH; c16 += 16) {
             float v[16];
             tc::tmem_ldn<16>(tbase + lad + (uint32_t)(T::C_ACC + h * WH + c16), v);
+            // ReLU'(X_k) from the stored X_k = hi + lo (>= 0): > 0 iff a half
+            // is non-zero; read before this thread overwrites its own slots.
+            // (Keeping the masks in registers from the forward epilogue made the
+            // chain spill: B200 c2 575 -> 547 us.)
+            uint4 xhi[2], xlo[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t off = (uint32_t)((h * (WH / 8) + c16 / 8 + q) * CHR + r * 16);
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xhi[q].x), "=r"(xhi[q].y), "=r"(xhi[q].z),
+                           "=r"(xhi[q].w) : "r"(sb + T::xhoff(k) + off));
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xlo[q].x), "=r"(xlo[q].y), "=r"(xlo[q].z),
+                           "=r"(xlo[q].w) : "r"(sb + T::xhoff(k) + (T::HF / 8) * CHR + off));
+            }
             tc::tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = ((mk >> (c16 + j)) & 1u) ? v[j] : 0.0f;
+            for (int j = 0; j < 16; ++j) {
+              const uint4& hh = xhi[j / 8];
+              const uint4& ll = xlo[j / 8];
+              const uint32_t wh = (&hh.x)[(j % 8) / 2], wl = (&ll.x)[(j % 8) / 2];
+              const uint32_t sh = (j & 1) ? 16u : 0u;
+              const bool pos = (((wh | wl) >> sh) & 0xFFFFu) != 0u;
+              v[j] = pos ? v[j] : 0.0f;
+            }
             tc::store_chunk(dh, dl, R, r, h * (WH / 8) + c16 / 8, v);
             tc::store_chunk(dh, dl, R, r, h * (WH / 8) + c16 / 8 + 1, v + 8);
           }
         }
       }
       NPM_WS_STAMP(15);
-      prev = cur;
     }
 #undef NPM_WS_STAMP
-    if (kt > 0) dz_epilogue(prev, kt - 1);
+    if (kt > 0) dz_epilogue(kt - 1);
     // ---- flush dW^T / db: lane = input feature (M = 128) or 32 (f/16) + f%16
     // (M = 64); the two threads of a lane split the output columns
 #pragma unroll
@@ -549,8 +573,14 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
     const int row = m & (R - 1), part = m >> 7;
     constexpr int LP = L / 2;
     float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
+    const int kt_end = blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + tstride - 1) / tstride) : 0;
     auto scatter = [&](int kd) {
       mbar_wait_idle(bar_dzf, (uint32_t)(kd & 1));
+      // the scatter's reductions contend with the chain's epilogue smem stores
+      // for the LSU: start them once the chain reaches tile kd + 1's head
+      // (ALU / MUFU work; B200 c2: 610 -> 575 us; starting at the first
+      // backward MMA instead: 606 us); the last tile has no successor head
+      if (kd + 1 < kt_end) mbar_wait_idle(bar_hs, (uint32_t)((kd + 1) & 1));
       const float4* dz = reinterpret_cast<const float4*>(smem + T::OFF_DZ);
       const float* uu = reinterpret_cast<const float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
       const float ux = uu[row], uy = uu[R + row], uz = uu[2 * R + row];
