@@ -1251,13 +1251,13 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       if (r != NPM_OK) return r;
     }
     if (a.debug & 4) {   // measurement only: per-phase clock stamps of CTA 0
-      CUDA_TRY(m->dbg_clock.ensure(64 * 16 * sizeof(long long)));
+      CUDA_TRY(m->dbg_clock.ensure(2 * 64 * 16 * sizeof(long long)));
       long long* dclk = static_cast<long long*>(m->dbg_clock.p);
-      cudaMemsetAsync(dclk, 0, 64 * 16 * sizeof(long long), st);
+      cudaMemsetAsync(dclk, 0, 2 * 64 * 16 * sizeof(long long), st);
       a.dbg_clock = dclk;
       npm_status r = check_launch(m, timed(m, kKTrainFused, st, [&] { return launch_train_tc(sh, a, m->num_sms, st); }));
       if (r == NPM_OK) r = bin_release(m, st, a.perm);
-      long long h[64 * 16];
+      long long h[2 * 64 * 16];
       cudaMemcpyAsync(h, dclk, sizeof(h), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       double acc[16] = {};
@@ -1287,6 +1287,21 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
       fprintf(stderr, "NPM_STAMPS");
       for (int j = 1; j < 16; ++j) fprintf(stderr, " s%d=%.0f", j, cs ? since[j] / cs : 0.0);
       fprintf(stderr, "\n");
+      // warp-specialised kernel: the memory role's stamps of the same tiles
+      // (gather of tile t: m0..m3; scatter of tile t-1: m4..m6), cycles since
+      // the chain's stamp 0 of tile t
+      double ms[16] = {};
+      int cm = 0;
+      for (int t = 2; t < 63; ++t) {
+        if (h[t * 16 + 15] == 0 || h[1024 + t * 16] == 0) break;
+        for (int j = 0; j < 7; ++j) if (h[1024 + t * 16 + j]) ms[j] += (double)(h[1024 + t * 16 + j] - h[t * 16]);
+        ++cm;
+      }
+      if (cm) {
+        fprintf(stderr, "NPM_MEMSTAMPS");
+        for (int j = 0; j < 7; ++j) fprintf(stderr, " m%d=%.0f", j, ms[j] / cm);
+        fprintf(stderr, "\n");
+      }
       if (r != NPM_OK || !a.priv_mask) return r;
       return fold_priv(m, st);
     }

@@ -155,8 +155,23 @@ __device__ __forceinline__ void ld_pair(const float4* p, float4& lo, float4& hi)
 // The 32-byte pair loads bypass L1 allocation (the training gathers hit L1
 // 8.9 % of the time): B200, c2 train 646 -> 630 us, c5 5.34 -> 5.04 ms.  The
 // single second-corner loads keep allocating (no_allocate there: c5 +7 %).
+// PAIRS = false: eight plain 16-byte loads (the warp-specialised training
+// kernel's memory warps: fewer ALU / select instructions next to the chain;
+// B200 c2 -1.4 %).
+template <bool PAIRS = true>
 __device__ __forceinline__ float4 gather_level(const float4* __restrict__ tab, uint32_t off, const LevelCorners& lc) {
   float4 v[8];
+  if constexpr (!PAIRS) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = __ldg(tab + off + lc.idx[c]);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      a0 = fmaf(lc.w[c], v[c].x, a0); a1 = fmaf(lc.w[c], v[c].y, a1);
+      a2 = fmaf(lc.w[c], v[c].z, a2); a3 = fmaf(lc.w[c], v[c].w, a3);
+    }
+    return make_float4(a0, a1, a2, a3);
+  }
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const uint32_t e0 = off + lc.idx[2 * p], e1 = off + lc.idx[2 * p + 1];

@@ -30,6 +30,10 @@
 
 namespace ws {
 
+#ifndef NPM_WS_PAIRS
+#define NPM_WS_PAIRS true
+#endif
+
 template <class N>
 struct WS {
   using B = TC<N>;
@@ -574,13 +578,24 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
     constexpr int LP = L / 2;
     float4* gtab = reinterpret_cast<float4*>(a.grads + N::N_MLP);
     const int kt_end = blockIdx.x < ntiles ? (int)((ntiles - blockIdx.x + tstride - 1) / tstride) : 0;
+    // memory-role clock stamps: measurement builds only (-DNPM_WS_MEMSTAMPS;
+    // the runtime check alone cost the production kernel ~3 %)
+#ifdef NPM_WS_MEMSTAMPS
+    const bool mstamp = (a.debug & 4) && blockIdx.x == 0 && m == 0;
+#define NPM_WS_MSTAMP(kk, idx) \
+  do { if (mstamp && (kk) < 64) a.dbg_clock[64 * 16 + (kk) * 16 + (idx)] = clock64(); } while (0)
+#else
+#define NPM_WS_MSTAMP(kk, idx) do { } while (0)
+#endif
     auto scatter = [&](int kd) {
       mbar_wait_idle(bar_dzf, (uint32_t)(kd & 1));
+      NPM_WS_MSTAMP(kd + 1, 4);
       // the scatter's reductions contend with the chain's epilogue smem stores
       // for the LSU: start them once the chain reaches tile kd + 1's head
       // (ALU / MUFU work; B200 c2: 610 -> 575 us; starting at the first
       // backward MMA instead: 606 us); the last tile has no successor head
       if (kd + 1 < kt_end) mbar_wait_idle(bar_hs, (uint32_t)((kd + 1) & 1));
+      NPM_WS_MSTAMP(kd + 1, 5);
       const float4* dz = reinterpret_cast<const float4*>(smem + T::OFF_DZ);
       const float* uu = reinterpret_cast<const float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
       const float ux = uu[row], uy = uu[R + row], uz = uu[2 * R + row];
@@ -605,11 +620,13 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
           atomicAdd(tg + lc.idx[c], make_float4(w * gq.x, w * gq.y, w * gq.z, w * gq.w));
         }
       }
+      NPM_WS_MSTAMP(kd + 1, 6);
     };
     int kt = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += tstride, ++kt) {
       const int s = kt % S0;
       const uint32_t ph0 = (uint32_t)((kt / S0) & 1);
+      NPM_WS_MSTAMP(kt, 0);
       const int64_t slot = tile * R + row;
       const bool valid = slot < n;
       const int64_t i = valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
@@ -635,15 +652,21 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
 #pragma unroll
       for (int q = 0; q < LP; ++q) {
         float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
+#ifdef NPM_WS_MEMSTAMPS
+        if (valid && !(a.debug & 2)) {   // NPM_DEBUG bit 1: skip the gathers (measurement builds)
+#else
         if (valid) {
+#endif
           const int l = part * LP + q;
           LevelCorners lc;
           level_corners(a.grid, l, ux, uy, uz, lc);
-          gl = gather_level(tab, a.grid.off[l], lc);
+          gl = gather_level<NPM_WS_PAIRS>(tab, a.grid.off[l], lc);
         }
         gf[4 * q] = gl.x; gf[4 * q + 1] = gl.y; gf[4 * q + 2] = gl.z; gf[4 * q + 3] = gl.w;
       }
+      NPM_WS_MSTAMP(kt, 1);
       mbar_wait_idle(bar_x0e + s, ph0 ^ 1u);
+      NPM_WS_MSTAMP(kt, 2);
 #pragma unroll
       for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
       if (part == 0) {
@@ -654,9 +677,11 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
       }
       tc::fence_proxy_async();
       mbar_arrive(bar_x0f + s);
+      NPM_WS_MSTAMP(kt, 3);
       if (kt > 0) scatter(kt - 1);
     }
     if (kt > 0) scatter(kt - 1);
+#undef NPM_WS_MSTAMP
   }
   tc::fence_before_sync();
   __syncthreads();
