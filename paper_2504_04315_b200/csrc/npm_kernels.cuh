@@ -46,6 +46,7 @@ struct QueryArgs {
   int cos_product;
   float kappa_c, log_c_kc;            // kappa_c and log C(kappa_c) (host-computed)
   int query_groups;                   // 1: two 256-thread CTAs per SM; 2: one CTA, two groups (NPM_QUERY_GROUPS)
+  long long* dbg_clock;               // measurement builds (-DNPM_QUERY_STAMPS): [64 tiles][16] stamps of CTA 0
 };
 
 struct TrainArgs {

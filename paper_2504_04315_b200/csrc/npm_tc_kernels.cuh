@@ -251,7 +251,15 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
   RowIn nx_row;
   const int64_t tile0 = (int64_t)blockIdx.x * GROUPS + g, tstep = (int64_t)gridDim.x * GROUPS;
   if (tile0 < ntiles) load_row(tile0, nx_row);
-  for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
+  int qt = 0;
+#ifdef NPM_QUERY_STAMPS
+  const bool qstamp = a.dbg_clock && blockIdx.x == 0 && threadIdx.x == 0 && MODE == 0;
+#define QSTAMP(idx) do { if (qstamp && qt < 64) a.dbg_clock[qt * 16 + (idx)] = clock64(); } while (0)
+#else
+#define QSTAMP(idx) do { } while (0)
+#endif
+  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++qt) {
+    QSTAMP(0);
     const RowIn row = nx_row;
     const bool valid = row.valid;
     const int64_t i = row.i;
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     for (int k = 0; k < NL - 1; ++k) {
       const int src = k & 1, dst = (k + 1) & 1;
       handoff();
+      QSTAMP(1 + 2 * k);
       if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t w = sb + WOFF + T::woff(k);
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
       }
       if (k == 0 && tile + tstep < ntiles) load_row(tile + tstep, nx_row);
       wait_mma(mbar, phase);
+      QSTAMP(2 + 2 * k);
       float h[WQ];
       tc::tmem_ldn<WQ>(tbase + lane_addr + (uint32_t)(q * WQ), h);
       tc::tmem_wait_ld();
@@ -343,6 +353,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
         tc::mma_commit(mbar);
       }
       wait_mma(mbar, phase);
+      QSTAMP(6);
     }
     // ---- Table 1 on this quarter's lobes
     float lp[KQ], kp[KQ], tp[KQ], pp[KQ];
@@ -405,6 +416,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     }
     RS(0, q) = mloc;
     psync();
+    QSTAMP(7);
     float M = RS(0, 0);
 #pragma unroll
     for (int qq = 1; qq < TPR; ++qq) M = fmaxf(M, RS(0, qq));
@@ -421,6 +433,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
     RS(1, q) = S;
     RS(2, q) = P;
     psync();
+    QSTAMP(8);
     float B[TPR + 1];
     B[0] = 0.0f;
 #pragma unroll
@@ -468,12 +481,14 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
         red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
       }
       psync();
+    QSTAMP(9);
       const float wx = red[(3 * TPR) * R + r], wy = red[(3 * TPR) * R + R + r], wz = red[(3 * TPR) * R + 2 * R + r];
       float P2 = 0.0f;
 #pragma unroll
       for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
       RS(4, q) = P2;
       psync();
+    QSTAMP(10);
       if (q == 0 && valid) {
         float Pt = 0.0f;
 #pragma unroll
@@ -499,6 +514,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
       }
     }
   }
+#undef QSTAMP
   teardown_cta(tbase - (uint32_t)(g * T::TCOLS_QUERY), GROUPS * T::TCOLS_QUERY);
 }
 
