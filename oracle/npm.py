@@ -46,6 +46,7 @@ class Config:
     kappa_min: float = 1e-5
     kappa_max: float = 1e5
     divergence: int = KL
+    learn_alpha: int = 0   # f-4' (C-A34): the BSDF selection-probability head
 
     @property
     def resolutions(self):
@@ -75,6 +76,15 @@ class Config:
     def n_grid(self):
         return sum(self.table_sizes) * self.n_features
 
+    @property
+    def n_alpha(self):
+        """C-A34: selection head a [W], c, zero-padded to a multiple of 4."""
+        return (self.mlp_width + 1 + 3) // 4 * 4 if self.learn_alpha else 0
+
+    @property
+    def n_total(self):
+        return self.n_mlp + self.n_grid + self.n_alpha
+
 
 def unpack(cfg, flat):
     """Flat parameter vector -> (layers [(W, b)], tables [[size_l, F]])."""
@@ -90,17 +100,25 @@ def unpack(cfg, flat):
     return layers, tables
 
 
-def pack(cfg, layers, tables):
+def pack(cfg, layers, tables, alpha_grad=None):
     parts = []
     for w, b in layers:
         parts += [w.ravel(), b.ravel()]
     parts += [t.ravel() for t in tables]
+    if cfg.n_alpha:
+        parts.append(np.zeros(cfg.n_alpha) if alpha_grad is None else alpha_grad)
     return np.concatenate(parts)
 
 
+def alpha_head(cfg, flat):
+    """C-A34: (a [W], c) of the selection head, stored after the grid."""
+    off = cfg.n_mlp + cfg.n_grid
+    return flat[off:off + cfg.mlp_width], flat[off + cfg.mlp_width]
+
+
 def grid_mask(cfg):
-    m = np.zeros(cfg.n_mlp + cfg.n_grid, bool)
-    m[cfg.n_mlp:] = True
+    m = np.zeros(cfg.n_total, bool)
+    m[cfg.n_mlp:cfg.n_mlp + cfg.n_grid] = True
     return m
 
 
@@ -127,6 +145,43 @@ def decode(cfg, flat, q):
     return raw, vmf.activate(raw, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
 
 
+def selection_probability(cfg, flat, q):
+    """C-A34 ("the BSDF selection probability could also be learned by
+    our network"): alpha(x) = sigmoid(a . h_{L-1} + c), a logistic-linear
+    read-out of the decoder's last hidden layer.  Returns alpha [n]."""
+    layers, _ = unpack(cfg, flat)
+    _, _, inputs = mlp.forward(layers, network_input(cfg, flat, q))
+    a, c = alpha_head(cfg, flat)
+    return 1.0 / (1.0 + np.exp(-(a @ inputs[-1] + c)))
+
+
+def alpha_second_moment_grad(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf, used, n_global):
+    """C-A34: gradient of the MC second moment of the one-sample MIS estimator,
+        M2 = (1/N) sum_n D^_n^2 / (p~_alpha(w_n) p~_s(w_n)),
+        p~_alpha = alpha p_bsdf + (1 - alpha) V     (P:208's combination),
+    with respect to the head (a, c): for the logit z = a . h + c,
+        dM2/dz_n = -(1/N) D^_n^2 (p_bsdf - V) alpha (1 - alpha) / (p~_alpha^2 p~_s)
+    (V and h stop-gradient: the mixture keeps Eq. 9).  Records outside `used`
+    (dropped / zero target, C-O12), or with non-finite p_bsdf < 0 or
+    p~_alpha = 0, contribute 0.  Returns (grad [W + 1], M2 estimate)."""
+    layers, _ = unpack(cfg, flat)
+    raw, _, inputs = mlp.forward(layers, network_input(cfg, flat, q))
+    h = inputs[-1]
+    a, c = alpha_head(cfg, flat)
+    alpha = 1.0 / (1.0 + np.exp(-(a @ h + c)))
+    v = vmf.mixture_pdf(np.asarray(wi, np.float64), vmf.activate(raw, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max))
+    pb = np.asarray(bsdf_pdf, np.float64)
+    ps = np.asarray(sample_pdf, np.float64)
+    pa = alpha * pb + (1.0 - alpha) * v
+    ok = used & np.isfinite(pb) & (pb >= 0) & (pa > 0)
+    tt = np.where(ok, t, 0.0)
+    pa_s = np.where(ok, pa, 1.0)
+    ps_s = np.where(ok, ps, 1.0)
+    gz = np.where(ok, -(tt * tt) * (pb - v) * alpha * (1.0 - alpha) / (pa_s * pa_s * ps_s), 0.0) / n_global
+    m2 = float(np.sum(np.where(ok, tt * tt / (pa_s * ps_s), 0.0)) / n_global)
+    return np.concatenate([h @ gz, [gz.sum()]]), m2
+
+
 def pdf(cfg, flat, q, w):
     """Eq. 4 at caller directions w [3, n]."""
     _, act = decode(cfg, flat, q)
@@ -148,7 +203,7 @@ def scalar_target(target):
     return (LUMA[:, None] * t).sum(axis=0)
 
 
-def gradient(cfg, flat, q, wi, target, sample_pdf, n_global):
+def gradient(cfg, flat, q, wi, target, sample_pdf, n_global, bsdf_pdf=None):
     """Eq. 9 + back propagation: the flat gradient of
     l = sum_n s_n log max(V_n, 1e-30), s_n = -(D^_n/p~_n)/N_global, with respect
     to every parameter, plus step statistics."""
@@ -176,16 +231,31 @@ def gradient(cfg, flat, q, wi, target, sample_pdf, n_global):
                                    dz[:gl], cfg.n_features)
         stats = dict(loss_proxy=float((-s * chi).sum()), n_used=int((~dropped & ~zero).sum()),
                      n_zero_target=int(zero.sum()), n_dropped=int(dropped.sum()))
-        return pack(cfg, mgrads, ggrads), stats
+        return pack(cfg, mgrads, ggrads, _alpha_block(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf,
+                                                      ~dropped & ~zero, n_global, stats)), stats
     draw, logv = vmf.grad_head(raw, wi, s, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
     mgrads, dz = mlp.backward(layers, pres, inputs, draw)
     gl = cfg.n_levels * cfg.n_features
     ggrads = grid.scatter_grad(q['x'], cfg.aabb_lo, cfg.aabb_hi, cfg.resolutions, cfg.table_sizes,
                                dz[:gl], cfg.n_features)
-    g = pack(cfg, mgrads, ggrads)
     stats = dict(loss_proxy=float((s * logv).sum()), n_used=int((~dropped & ~zero).sum()),
                  n_zero_target=int(zero.sum()), n_dropped=int(dropped.sum()))
+    g = pack(cfg, mgrads, ggrads, _alpha_block(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf, ~dropped & ~zero,
+                                               n_global, stats))
     return g, stats
+
+
+def _alpha_block(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf, used, n_global, stats):
+    """The selection head's slice of the gradient (zero-padded to n_alpha)."""
+    if not cfg.learn_alpha:
+        return None
+    if bsdf_pdf is None:
+        raise ValueError("learn_alpha needs the BSDF pdf of every record")
+    ga, m2 = alpha_second_moment_grad(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf, used, n_global)
+    stats["alpha_m2"] = m2
+    out = np.zeros(cfg.n_alpha)
+    out[:ga.size] = ga
+    return out
 
 
 @dataclass
@@ -214,9 +284,10 @@ def optimizer_step(state, g):
     return nnf
 
 
-def train_step(state, q, wi, target, sample_pdf, n_global=None):
+def train_step(state, q, wi, target, sample_pdf, n_global=None, bsdf_pdf=None):
     n = np.asarray(q['x']).shape[1]
-    g, stats = gradient(state.cfg, state.params, q, wi, target, sample_pdf, n if n_global is None else n_global)
+    g, stats = gradient(state.cfg, state.params, q, wi, target, sample_pdf, n if n_global is None else n_global,
+                        bsdf_pdf)
     stats['grad_norm_sq'] = float(np.sum(np.where(np.isfinite(g), g, 0.0) ** 2))
     stats['n_nonfinite_grad'] = optimizer_step(state, g)
     return g, stats
