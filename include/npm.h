@@ -119,17 +119,31 @@ typedef struct {
   uint64_t init_seed;        /* parameter initialisation seed (C-A21) */
   int32_t divergence;        /* training objective: 0 = KL (Eq. 8/9), 1 = Pearson chi^2
                                 (f-4; "other divergence metrics", C-A31) */
+  int32_t learn_alpha;       /* 1: learn the BSDF selection probability (f-4'; "(1) the
+                                BSDF selection probability could also be learned by our
+                                network", reading C-A34): alpha(x) = sigmoid(a . h_{L-1} + c),
+                                a logistic-linear head on the last hidden layer, its W + 1
+                                parameters (zero-initialised: alpha = 1/2, the paper's fixed
+                                choice) stored AFTER the grid, zero-padded to a multiple of 4.
+                                Trained on the second moment of the one-sample MIS estimator
+                                (needs npm_query.bsdf_pdf in training calls); used by
+                                npm_combined_sample in place of its alpha argument.  Radiance
+                                mode only; the model then always uses the warp-specialised
+                                training kernel. */
 } npm_config;
 
 /* One SoA queue of shading points. px/py/pz: world-space x.
  * wox.., nx.., rough: product mode only (w_o unit outgoing direction, n unit
- * normal, roughness in [0,1]); ignored (may be NULL) in radiance mode. */
+ * normal, roughness in [0,1]); ignored (may be NULL) in radiance mode.
+ * bsdf_pdf: training calls of a learn_alpha model only -- the BSDF sampling
+ * pdf p_bsdf(w_i) of each record's direction (C-A34); ignored otherwise. */
 typedef struct {
   int64_t n;
   const float *px, *py, *pz;
   const float *wox, *woy, *woz;
   const float *nx, *ny, *nz;
   const float *rough;
+  const float *bsdf_pdf;
 } npm_query;
 
 /* Training statistics of one step. loss_proxy = sum_n s_n log max(V_n,

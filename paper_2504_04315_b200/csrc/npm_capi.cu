@@ -61,7 +61,7 @@ struct npm_model {
   GridDesc grid{};
   int res[kMaxLevels] = {};
   int64_t entries[kMaxLevels] = {};
-  int64_t n_mlp = 0, n_grid = 0, n_total = 0;
+  int64_t n_mlp = 0, n_grid = 0, n_alpha = 0, n_total = 0;
   float* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // params, grads, m, v, ema
   int64_t t = 0;
   // device statistics: [0] loss, [1] grad norm^2 ; counters [0] used [1] zero [2] dropped [3] nonfinite
@@ -200,6 +200,7 @@ void stage_query(Stager& s, const npm_model* m, const npm_query* q, npm_query& d
   } else {
     d.wox = d.woy = d.woz = d.nx = d.ny = d.nz = d.rough = nullptr;
   }
+  d.bsdf_pdf = m->n_alpha ? s.in(q->bsdf_pdf, n) : nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -237,7 +238,7 @@ struct HostPipe {
   }
 
   static bool usable(const npm_model* m, int64_t n, std::initializer_list<const void*> ptrs) {
-    if (!m->pipeline || n < 2 * kPipeMin) return false;
+    if (!m->pipeline || n < 2 * kPipeMin || m->n_alpha) return false;   // (learn_alpha: staged path)
     for (const void* p : ptrs)
       if (p && Stager::kind(p) == 2) return false;   // a device array: the plain path
     return true;
@@ -358,6 +359,7 @@ void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryA
   a.log_kmin = logf(m->cfg.kappa_min);
   a.log_kmax = logf(m->cfg.kappa_max);
   a.query_groups = m->query_groups;
+  a.alpha_w = m->n_alpha ? a.params + m->n_mlp + m->n_grid : nullptr;
 }
 
 const char* kKindNames[] = {"query", "encode", "train_forward", "train_backward", "weight_grad", "adam",
@@ -597,6 +599,9 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
     return fail(NPM_ERR_INVALID, "need 2 <= D_1 < D_L");
   if (c.log2_hashmap < 0 || c.log2_hashmap > 30) return fail(NPM_ERR_INVALID, "log2_hashmap out of range");
   if (c.divergence != 0 && c.divergence != 1) return fail(NPM_ERR_INVALID, "divergence must be 0 (KL) or 1 (chi^2)");
+  if (c.learn_alpha != 0 && c.learn_alpha != 1) return fail(NPM_ERR_INVALID, "learn_alpha must be 0 or 1");
+  if (c.learn_alpha && (c.mode != NPM_RADIANCE || c.n_lobes != 8))
+    return fail(NPM_ERR_INVALID, "learn_alpha: radiance-mode shapes with K = 8 only");
   for (int a = 0; a < 3; ++a)
     if (!(c.aabb_hi[a] > c.aabb_lo[a]) || !std::isfinite(c.aabb_lo[a]) || !std::isfinite(c.aabb_hi[a]))
       return fail(NPM_ERR_INVALID, "degenerate AABB");
@@ -675,6 +680,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // product shape (no warp-specialised instantiation).
   m->train_ws = (m->bin_train || c.mode == NPM_PRODUCT) ? 0 : 1;
   if (const char* e = getenv("NPM_TRAIN_WS")) m->train_ws = atoi(e);
+  if (c.learn_alpha) m->train_ws = 1;   // the selection head lives in the warp-specialised kernel
   // Privatise the scatter of small (coarse) levels when training batches are
   // binned: coherent records then add to the same few coarse entries from
   // every SM and the reductions queue on the same L2 lines.  Each SM
@@ -704,7 +710,8 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   }
   m->n_mlp = nm;
   if (nm % 4) { delete m; return fail(NPM_ERR_INVALID, "internal: MLP size not 16B aligned"); }
-  m->n_total = m->n_mlp + m->n_grid;
+  m->n_alpha = c.learn_alpha ? ((int64_t)c.mlp_width + 1 + 3) / 4 * 4 : 0;   // C-A34 head after the grid
+  m->n_total = m->n_mlp + m->n_grid + m->n_alpha;
   for (int b = 0; b < 5; ++b) {
     // + kBufPad floats: the paired grid gathers (gather_level) read the 32-B
     // entry pair containing the last table entry, and the ZeRO-1 exchange
@@ -721,8 +728,10 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
     return fail(NPM_ERR_OOM, "stats");
   }
   cudaStream_t st = 0;
-  launch_init_params(m->buf[NPM_BUF_PARAMS], m->n_mlp, m->n_total, s, c.init_seed, st);
+  launch_init_params(m->buf[NPM_BUF_PARAMS], m->n_mlp, m->n_mlp + m->n_grid, s, c.init_seed, st);
   m->launches += 1;
+  if (m->n_alpha)   // the selection head starts at a = 0, c = 0: alpha = 1/2 (the paper's fixed choice)
+    cudaMemsetAsync(m->buf[NPM_BUF_PARAMS] + m->n_mlp + m->n_grid, 0, m->n_alpha * sizeof(float), st);
   cudaMemsetAsync(m->buf[NPM_BUF_GRADS], 0, m->n_total * sizeof(float), st);
   if (m->priv_mask) {
     const size_t pb = (size_t)m->priv_stride * m->num_sms * 16;
@@ -1250,6 +1259,12 @@ static npm_status accumulate(npm_model* m, const npm_query* q, const float* wix,
   if (const char* e = getenv("NPM_DEBUG")) a.debug = atoi(e);   // measurement only
   a.divergence = m->cfg.divergence;
   a.ws = m->train_ws;
+  if (m->n_alpha) {
+    if (!d.bsdf_pdf) return fail(NPM_ERR_INVALID, "learn_alpha: training records need bsdf_pdf");
+    a.alpha_w = m->buf[NPM_BUF_PARAMS] + m->n_mlp + m->n_grid;
+    a.alpha_g = m->buf[NPM_BUF_GRADS] + m->n_mlp + m->n_grid;
+    a.bsdf_pdf = d.bsdf_pdf;
+  }
   CUDA_TRY(m->wimg.ensure(64 * 1024));
   a.wimg = static_cast<uint8_t*>(m->wimg.p);
   a.wimg_bytes = 64 * 1024;
@@ -1410,6 +1425,8 @@ static npm_status adam_range(npm_model* m, int64_t begin, int64_t count, bool em
   AdamArgs a;
   a.n_total = count;
   a.n_mlp = m->n_mlp - begin < 0 ? 0 : (m->n_mlp - begin > count ? count : m->n_mlp - begin);
+  const int64_t ge = m->n_mlp + m->n_grid - begin;
+  a.grid_end = ge < 0 ? 0 : (ge > count ? count : ge);
   a.p = m->buf[NPM_BUF_PARAMS] + begin; a.g = m->buf[NPM_BUF_GRADS] + begin; a.m = m->buf[NPM_BUF_ADAM_M] + begin;
   a.v = m->buf[NPM_BUF_ADAM_V] + begin; a.e = m->buf[NPM_BUF_EMA] + begin;
   a.lr = c.lr; a.beta1 = c.beta1; a.beta2 = c.beta2; a.eps = c.adam_eps; a.decay = c.ema_decay;
@@ -1498,6 +1515,7 @@ npm_status npm_train_stream(npm_model* m, const npm_query* q, const float* wix, 
     sub.px = sl(d.px); sub.py = sl(d.py); sub.pz = sl(d.pz);
     sub.wox = sl(d.wox); sub.woy = sl(d.woy); sub.woz = sl(d.woz);
     sub.nx = sl(d.nx); sub.ny = sl(d.ny); sub.nz = sl(d.nz); sub.rough = sl(d.rough);
+    sub.bsdf_pdf = sl(d.bsdf_pdf);
     Stager s2{m, st};   // device slices: pass-through
     // one optimisation step per micro-batch: Eq. 9's 1/N over the micro-batch
     npm_status r = accumulate(m, &sub, dwx + a0, dwy + a0, dwz + a0, dtg + a0, channels, dpd + a0, b, st, s2, n);

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
       if (!isfinite(g[q])) { g[q] = 0.0f; nf += 1; }
       gn += (double)g[q] * (double)g[q];
     }
-    const bool grid = 4 * j >= a.n_mlp;
+    const bool grid = 4 * j >= a.n_mlp && 4 * j < a.grid_end;
     const bool any = g[0] != 0.0f || g[1] != 0.0f || g[2] != 0.0f || g[3] != 0.0f;
     float p[4] = {pv.x, pv.y, pv.z, pv.w};
     if (!grid || any) {

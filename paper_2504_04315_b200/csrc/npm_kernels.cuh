@@ -47,6 +47,7 @@ struct QueryArgs {
   float kappa_c, log_c_kc;            // kappa_c and log C(kappa_c) (host-computed)
   int query_groups;                   // 1: two 256-thread CTAs per SM; 2: one CTA, two groups (NPM_QUERY_GROUPS)
   long long* dbg_clock;               // measurement builds (-DNPM_QUERY_STAMPS): [64 tiles][16] stamps of CTA 0
+  const float* alpha_w;               // C-A34 selection head (a [W], c) of `params`, or NULL: use `alpha`
 };
 
 struct TrainArgs {
@@ -78,6 +79,11 @@ struct TrainArgs {
   uint8_t* wimg;
   uint32_t wimg_bytes;
   int ws;
+  // C-A34 selection head (learn_alpha): its parameters / gradient (a [W], c)
+  // and the records' BSDF pdf; alpha_w == NULL: no head
+  const float* alpha_w;
+  float* alpha_g;
+  const float* bsdf_pdf;
   int64_t priv_stride;
   int64_t priv_off[16];
   double* stats;            // [0] loss, [1] unused, then int counters as double
@@ -86,6 +92,7 @@ struct TrainArgs {
 
 struct AdamArgs {
   int64_t n_mlp, n_total;   // of the range processed (a shard: n_mlp relative to its start)
+  int64_t grid_end;         // grid entries are [n_mlp, grid_end) of the range (the C-A34 head follows)
   float *p, *g, *m, *v, *e;
   float lr, beta1, beta2, eps, decay, c1, c2;  // c1 = 1/(1-b1^t), c2 = 1/(1-b2^t)
   int ema;                  // 1: EMA in the same pass; 0: Adam only (ZeRO-1 shard, EMA after the all-gather)

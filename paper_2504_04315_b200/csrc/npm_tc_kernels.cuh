@@ -67,7 +67,7 @@ struct TC {
   static constexpr uint32_t SMEM_QUERY = MISC_Q + 64;
   // ---- two-group query map (one 512-thread CTA per SM, one weight copy):
   // weights, bias | group g: buffer A, buffer B, head reductions | misc
-  static constexpr uint32_t QRED_BYTES = (3u * 2u + 3u + 2u) * R * 4u;   // TPR = 2 slots
+  static constexpr uint32_t QRED_BYTES = (3u * 2u + 3u + 2u + 2u) * R * 4u;   // TPR = 2 slots (+ C-A34 logit parts)
   static constexpr uint32_t QG0 = (WBYTES + BBYTES + 1023u) & ~1023u;
   static constexpr uint32_t QGB = (QB + 2u * (W / 8) * CH + QRED_BYTES + 1023u) & ~1023u;
   static constexpr uint32_t MISC_Q2 = QG0 + 2u * QGB;
@@ -342,6 +342,12 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
         h[4 * j + 3] = fmaxf(h[4 * j + 3] + bb.w, 0.0f);
       }
       tc::store_feats<WQ>(xbuf[dst], xbuf[dst] + xlo[dst], R, r, q * WQ, h);
+      if (COMBINED && k == NL - 2 && a.alpha_w) {   // C-A34: this part's a . h_{L-1}
+        float zp = 0.0f;
+#pragma unroll
+        for (int j = 0; j < WQ; ++j) zp = fmaf(__ldg(a.alpha_w + q * WQ + j), h[j], zp);
+        red[(11 + q) * R + r] = zp;   // read after the next CTA / group barrier
+      }
     }
     {
       constexpr int k = NL - 1, src = k & 1;
@@ -455,7 +461,15 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
                                COMBINED ? __ldg(a.u + 3 * n + ic) : 1.0f);
       else u = philox_uniforms4(a.seed, (uint64_t)ic + a.offset);
       // f-1: BSDF with probability alpha (C-A25), else the guide
-      const bool use_bsdf = COMBINED && u.w < a.alpha;
+      // selection probability: the caller's alpha, or the learned alpha(x) (C-A34)
+      float alpha = a.alpha;
+      if (COMBINED && a.alpha_w) {
+        float z = __ldg(a.alpha_w + W);
+#pragma unroll
+        for (int qq = 0; qq < TPR; ++qq) z += red[(11 + qq) * R + r];
+        alpha = 1.0f / (1.0f + __expf(-z));
+      }
+      const bool use_bsdf = COMBINED && u.w < alpha;
       const bool before = u.x < B[q] * invS;                 // an earlier quarter owns u1
       const bool after = u.x >= B[q + 1] * invS && q < TPR - 1;   // a later part owns u1
       if (use_bsdf) {
@@ -504,7 +518,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
             t = 2;
           } else {
             // one-sample balance heuristic p~ = alpha p_bsdf + (1 - alpha) V
-            p = a.alpha * bsdf_pdf(nx, ny, nz, ox, oy, oz) + (1.0f - a.alpha) * V;
+            p = alpha * bsdf_pdf(nx, ny, nz, ox, oy, oz) + (1.0f - alpha) * V;
           }
           if (a.gpdf) a.gpdf[i] = V;
           if (a.tech) a.tech[i] = t;
@@ -1124,16 +1138,23 @@ struct TcLaunch {
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
     if constexpr (!N::PRODUCT && N::K == 8) {
       if (a.ws) {   // warp-specialised kernel (npm_train_ws.cuh)
-        using T = ws::WS<N>;
-        if (!a.wimg || a.wimg_bytes < T::WIMG) return -1;
+        if (!a.wimg || a.wimg_bytes < ws::WS<N>::WIMG) return -1;
+        if (a.alpha_w && (!a.alpha_g || !a.bsdf_pdf)) return -1;
         ws::prep_wimg_kernel<N><<<8, 256, 0, st>>>(a.params, a.wimg);
-        cudaFuncSetAttribute(ws::train_ws_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
-        const int64_t ntiles = (a.n + T::R - 1) / T::R;
-        const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
-        ws::train_ws_kernel<N><<<blocks, T::THREADS, T::SMEM, st>>>(a);
+        auto go = [&](auto AHC) {
+          constexpr bool AH = decltype(AHC)::value;
+          using T = ws::WS<N, AH>;
+          cudaFuncSetAttribute(ws::train_ws_kernel<N, AH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
+          const int64_t ntiles = (a.n + T::R - 1) / T::R;
+          const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
+          ws::train_ws_kernel<N, AH><<<blocks, T::THREADS, T::SMEM, st>>>(a);
+        };
+        if (a.alpha_w) go(std::true_type{});
+        else go(std::false_type{});
         return 2;
       }
     }
+    if (a.alpha_w) return -1;   // the C-A34 head is trained by the warp-specialised kernel only
     // two 64-sample tiles per CTA (tc_train64_kernel)
     using T64 = TC64<N>;
     cudaFuncSetAttribute(tc_train64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T64::SMEM);

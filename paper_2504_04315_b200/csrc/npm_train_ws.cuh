@@ -34,7 +34,7 @@ namespace ws {
 #define NPM_WS_PAIRS true
 #endif
 
-template <class N>
+template <class N, bool AH = false>
 struct WS {
   using B = TC<N>;
   static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN, L = N::L, K = N::K, NG = N::NGRID;
@@ -52,33 +52,56 @@ struct WS {
   static constexpr uint32_t a1k(uint32_t x) { return (x + 1023u) & ~1023u; }
   static constexpr uint32_t X0_BYTES = 2u * (ZF / 8) * CHR;
   static constexpr uint32_t XH_BYTES = 2u * (HF / 8) * CHR;
-  static constexpr uint32_t D_BYTES = 2u * (NOUT / 8) * CHR;
-  static constexpr int RDF = 12;             // row data: ux uy uz valid | wx wy wz | t0 t1 t2 | pdf | -
+  // AH (C-A34 head trained): delta_{NL-1} gets one more chunk whose first
+  // column holds dM2/dz, and dW_{NL-1}'s MMA runs XD = 16 columns wider (M = 128
+  // needs N % 16 == 0) so it also yields the head's gradient.  Only column NOUT
+  // is read back: the MMA's second extra chunk reads whatever follows (the lo
+  // half's first chunk / the X0 stage) into columns that are never used.
+  static constexpr int XC = AH ? 8 : 0, XD = AH ? 16 : 0;
+  static constexpr uint32_t D_BYTES = 2u * ((NOUT + XC) / 8) * CHR;
+  static constexpr uint32_t AH_BYTES = AH ? 4u * (W + 4) : 0u;
+  // row data [RDF][R] f32: slots 3 valid | 4-6 w_i | 7-9 target | 10 pdf |
+  // 11 p_bsdf (AH).  It also carries the head's exchange between the row's two
+  // threads (no separate buffer: the 164 KB carve-out leaves L1 92 KB -- the
+  // gathers run ~6 % slower per 32 KB less L1): slots 0/1 the softmax max of
+  // thread h (written before the first pair barrier, no other reader), slots
+  // 4+2h / 5+2h its sums (written after that barrier, when both threads have
+  // read the row's inputs); AH: the logit parts in slots 2 / 12.
+  static constexpr int RDF = AH ? 13 : 11;
   static constexpr uint32_t RD_BYTES = RDF * R * 4;
-  static constexpr uint32_t DZ_BYTES = (uint32_t)L * R * 16 + 4u * R * 4;   // [L][R] float4 + [4][R]
+  static constexpr uint32_t DZ_BYTES = (uint32_t)L * R * 16;   // [L][R] float4
   static constexpr uint32_t OFF_X1 = a1k(WIMG);
   __host__ __device__ static constexpr uint32_t xhoff(int k) { return OFF_X1 + (uint32_t)(k - 1) * XH_BYTES; }
   static constexpr uint32_t OFF_D = OFF_X1 + (uint32_t)(NL - 1) * XH_BYTES;
   static constexpr uint32_t OFF_X0 = OFF_D + D_BYTES;
-  // X0 stages: 2 when they fit (gathers run a full tile ahead), else 1
-  static constexpr uint32_t fixed_tail(int s0) {
-    return OFF_X0 + (uint32_t)s0 * (X0_BYTES + RD_BYTES) + DZ_BYTES + 3u * TPR * R * 4u + 256u;
-  }
-  static constexpr int S0 = fixed_tail(2) <= 220u * 1024u ? 2 : 1;
+  // X0 stages.  One: with two (gathers a full tile ahead) the memory warps'
+  // extra in-flight loads slowed the chain more than the overlap gained
+  // (B200 c2, same box: S0 = 2 545 us, S0 = 1 525 us); the 2-stage protocol
+  // stays selectable for measurement (-DNPM_WS_S0=2).
+#ifdef NPM_WS_S0   // measurement override
+  static constexpr int S0 = NPM_WS_S0;
+#else
+  static constexpr int S0 = 1;
+#endif
+  static_assert(S0 == 1 || S0 == 2, "X0 stages");
   // delta_{NL-1} in D; delta_k (k < NL-1) over X_{k+1} (its ones chunk stays).
   // (Measured on B200 c2: a separate delta buffer letting each backward
   // epilogue run under the dW MMAs did not shorten the backward phases.)
   __host__ __device__ static constexpr uint32_t dboff(int k) { return k == NL - 1 ? OFF_D : xhoff(k + 1); }
-  __host__ __device__ static constexpr uint32_t dfeat(int k) { return k == NL - 1 ? (uint32_t)NOUT : (uint32_t)HF; }
+  __host__ __device__ static constexpr uint32_t dfeat(int k) { return k == NL - 1 ? (uint32_t)(NOUT + XC) : (uint32_t)HF; }
   static constexpr uint32_t OFF_RD = OFF_X0 + (uint32_t)S0 * X0_BYTES;
   static constexpr uint32_t OFF_DZ = OFF_RD + (uint32_t)S0 * RD_BYTES;
-  static constexpr uint32_t OFF_XCH = (OFF_DZ + DZ_BYTES + 15u) & ~15u;   // head exchange [TPR][3][R] f32
-  static constexpr uint32_t OFF_BAR = OFF_XCH + 3u * TPR * R * 4u;
+  // C-A34 selection head: its parameters (a [W], c)
+  static constexpr uint32_t OFF_AH = (OFF_DZ + DZ_BYTES + 15u) & ~15u;
+  static constexpr uint32_t OFF_BAR = OFF_AH + AH_BYTES;
   // mbarriers: [0] weights, [1] mma, [2] dz full, [3] dz empty, [4..4+S0) x0 full, [4+S0..4+2 S0) x0 empty,
   // [4+2 S0] head start (the scatter of tile k-1 waits for tile k's head)
   static constexpr int NBAR = 5 + 2 * S0;
   static constexpr uint32_t OFF_TSLOT = OFF_BAR + 8u * NBAR;
-  static constexpr uint32_t SMEM_RAW = OFF_TSLOT + 16u;
+#ifndef NPM_WS_SMEM_PAD   // measurement knob: extra dynamic smem (a smaller L1 carve-out)
+#define NPM_WS_SMEM_PAD 0
+#endif
+  static constexpr uint32_t SMEM_RAW = OFF_TSLOT + 16u + NPM_WS_SMEM_PAD;
   // dW^T MMAs read M_k / 8 feature chunks from a lo base (M_k = 64 or 128):
   // the rows past X_k's features are garbage rows of dW^T (ignored) but the
   // reads must stay inside the allocation
@@ -96,7 +119,7 @@ struct WS {
   static constexpr int C_ACC = 0, C_DZ = 64;
   static_assert(W <= 64 && NOUT <= 64 && NG <= 64, "accumulator columns");
   __host__ __device__ static constexpr int dwcol(int k) { return 128 + B::osum(k); }
-  static_assert(128 + N::osum(NL) <= 512, "TMEM columns");
+  static_assert(128 + N::osum(NL) + XD <= 512, "TMEM columns");
   static constexpr int TCOLS = 512;
 };
 
@@ -196,9 +219,11 @@ __global__ void __launch_bounds__(256) prep_wimg_kernel(const float* __restrict_
   }
 }
 
-template <class N>
-__global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a) {
-  using T = WS<N>;
+// AH: the C-A34 selection head is trained (a learn_alpha model); a separate
+// instantiation so the plain kernel carries none of its code
+template <class N, bool AH>
+__global__ void __launch_bounds__(WS<N, AH>::THREADS, 1) train_ws_kernel(TrainArgs a) {
+  using T = WS<N, AH>;
   using TB = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W, NOUT = N::NOUT, L = N::L, NG = N::NGRID, NIN = N::NIN;
   constexpr int R = T::R;
@@ -272,11 +297,18 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
     const int r = ((warp & 3) << 5) | lane;
     const uint32_t lad = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane field
     // zero the dW^T accumulators (all later MMAs accumulate); halves by column
-    for (int col = 16 * h; col < N::osum(NL); col += 16 * TPR) tc::tmem_zero16(tbase + lad + (uint32_t)(128 + col));
+    for (int col = 16 * h; col < N::osum(NL) + T::XD; col += 16 * TPR) tc::tmem_zero16(tbase + lad + (uint32_t)(128 + col));
     tc::tmem_wait_st();
     mbar_wait_t(bar_w, 0);
     const float* bias = reinterpret_cast<const float*>(smem + TB::WBYTES);
-    float* xch = reinterpret_cast<float*>(smem + T::OFF_XCH);   // [TPR h][3][R] head exchange
+    static_assert(TPR == 2, "the head exchange uses row-data slots of two threads");
+    // C-A34 selection head (AH): its parameters in smem
+    constexpr bool ahead = AH;
+    float* ah_s = reinterpret_cast<float*>(smem + T::OFF_AH);
+    if (ahead) {
+      for (int j = tid; j < W + 1; j += T::CHAIN_THREADS) ah_s[j] = __ldg(a.alpha_w + j);
+      tc::named_sync(1u, (uint32_t)T::CHAIN_THREADS);
+    }
     const uint32_t wsb = sb;   // weight image at smem offset 0
     uint32_t phase = 0;
     double loss = 0.0;
@@ -293,12 +325,8 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
       tc::fence_after_sync();
     };
     // previous tile's dz -> dz stage (run while the next tile's first MMA
-    // executes).  Its row data (position, validity) is read from its row-data
-    // stage here: that stage is refilled only by the gather of tile kk + S0,
-    // which the memory warps start after scattering tile kk, i.e. after the
-    // dz_full this epilogue arrives on.
+    // executes); the memory warps keep the rows' positions in registers
     auto dz_epilogue = [&](int kk) {
-      const float* rdp = reinterpret_cast<const float*>(smem + T::OFF_RD + (uint32_t)(kk % S0) * T::RD_BYTES);
       float v[NG / TPR];
       tc::tmem_ldn<NG / TPR>(tbase + lad + (uint32_t)(T::C_DZ + h * (NG / TPR)), v);
       tc::tmem_wait_ld();
@@ -307,10 +335,6 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
 #pragma unroll
       for (int l = 0; l < LH; ++l)
         dz[(h * LH + l) * R + r] = make_float4(v[4 * l], v[4 * l + 1], v[4 * l + 2], v[4 * l + 3]);
-      if (h == 0) {
-        float* uu = reinterpret_cast<float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
-        uu[r] = rdp[r]; uu[R + r] = rdp[R + r]; uu[2 * R + r] = rdp[2 * R + r]; uu[3 * R + r] = rdp[3 * R + r];
-      }
       mbar_arrive(bar_dzf);
     };
     const bool stamp = (a.debug & 4) && blockIdx.x == 0 && tid == 0;
@@ -333,7 +357,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
       // this row's head inputs are read from the row-data stage at the head
       // (the stage is refilled only after bwd_0 completes): no registers held
       // across the forward epilogues (they spilled there)
-      const float* rd = reinterpret_cast<const float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
+      float* rd = reinterpret_cast<float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
       if (kt > 0) dz_epilogue(kt - 1);
       NPM_WS_STAMP(2);
       // ---- forward
@@ -354,7 +378,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
         const float* b = bias + TB::boff(k) / 4;
         if (k < NL - 1) {
           const uint32_t xh = sb + T::xhoff(k + 1), xl = xh + (T::HF / 8) * CHR;
-
+          float zpart = 0.0f;   // C-A34: this thread's part of a . h_{L-1}
 #pragma unroll
           for (int c16 = 0; c16 < WH; c16 += 16) {   // 16 columns at a time (register pressure)
             float v[16];
@@ -363,11 +387,12 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               v[j] = fmaxf(v[j] + b[h * WH + c16 + j], 0.0f);
-
+              if (k == NL - 2 && ahead) zpart = fmaf(ah_s[h * WH + c16 + j], v[j], zpart);
             }
             tc::store_chunk(xh, xl, R, r, h * (WH / 8) + c16 / 8, v);
             tc::store_chunk(xh, xl, R, r, h * (WH / 8) + c16 / 8 + 1, v + 8);
           }
+          if (k == NL - 2 && ahead) rd[(h == 0 ? 2 : 12) * R + r] = zpart;   // read after the head's first exchange
         } else {
           if (tid == 0) mbar_arrive(bar_hs);   // the memory warps may scatter now
           // ---- Eq. 9 head (C-O12, C-O13): row r, lobes [h K/2, (h+1) K/2)
@@ -415,11 +440,9 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
           }
           // softmax max / normaliser / mixture sum across the row's two threads
           NPM_WS_STAMP(12);
-          xch[(h * 3 + 0) * R + r] = mloc;
+          rd[h * R + r] = mloc;
           psync();
-          float M = xch[0 * R + r];
-#pragma unroll
-          for (int q = 1; q < TPR; ++q) M = fmaxf(M, xch[(q * 3 + 0) * R + r]);
+          const float M = fmaxf(rd[r], rd[R + r]);
           float e[KH], S = 0.0f, P = 0.0f;
 #pragma unroll
           for (int m = 0; m < KH; ++m) {
@@ -427,14 +450,12 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
             S += e[m];
             P += e[m] * vv[m];
           }
-          xch[(h * 3 + 1) * R + r] = S;
-          xch[(h * 3 + 2) * R + r] = P;
+          rd[(4 + 2 * h) * R + r] = S;
+          rd[(5 + 2 * h) * R + r] = P;
           psync();
           NPM_WS_STAMP(14);
           // the same association order on every thread of the row: parts 0, 1, ...
-          float St = 0.0f, Pt = 0.0f;
-#pragma unroll
-          for (int q = 0; q < TPR; ++q) { St += xch[(q * 3 + 1) * R + r]; Pt += xch[(q * 3 + 2) * R + r]; }
+          const float St = 0.0f + rd[4 * R + r] + rd[6 * R + r], Pt = 0.0f + rd[5 * R + r] + rd[7 * R + r];
           const float invS = 1.0f / St;
           const float Vb = fmaxf(Pt * invS, kVFloor);
           const float invV = 1.0f / Vb;
@@ -458,11 +479,34 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
             dt[m] = sgk * wdth * th[m] * (1.0f - th[m]);
             dp[m] = sgk * wdph * ph[m] * (1.0f - ph[m]);
           }
-          const uint32_t dh = sb + T::OFF_D, dlo = dh + (NOUT / 8) * CHR;
+          const uint32_t dh = sb + T::OFF_D, dlo = dh + (T::dfeat(NL - 1) / 8) * CHR;
           tc::store_feats<KH>(dh, dlo, R, r, h * KH, dl);
           tc::store_feats<KH>(dh, dlo, R, r, K + h * KH, dk);
           tc::store_feats<KH>(dh, dlo, R, r, 2 * K + h * KH, dt);
           tc::store_feats<KH>(dh, dlo, R, r, 3 * K + h * KH, dp);
+          if (ahead) {
+            // ---- C-A34: second-moment gradient of the selection head.  Logit
+            // z = c + a . h_{L-1} (parts of both threads, the same order on each);
+            // dM2/dz = -(1/N) D^2 (p_b - V) alpha (1 - alpha) / (p~_alpha^2 p~_s)
+            float z = ah_s[W];
+            z += rd[2 * R + r];
+            z += rd[12 * R + r];
+            const float al = 1.0f / (1.0f + __expf(-z));
+            const float pb = rd[11 * R + r];
+            const float Vm = Pt * invS;                  // V(w_i), not floored (C-A34)
+            const float pa = al * pb + (1.0f - al) * Vm;
+            const bool aok = use && isfinite(pb) && pb >= 0.0f && pa > 0.0f;
+            const float q1 = aok ? t / pa : 0.0f;
+            const float gz = aok ? (float)(-(double)(q1 * q1 * (pb - Vm) * al * (1.0f - al) / p) * a.inv_n_global)
+                                 : 0.0f;
+            // dM2/d(a, c) = sum_rows gz (h_{L-1}, 1): gz goes to delta_{NL-1}'s
+            // column NOUT (the rest of the XD extra columns zero), so the dW_{NL-1}
+            // MMA (X_{NL-1}^T delta, ones chunk included) accumulates it in TMEM
+            if (h == 0) {
+              float gzc[8] = {gz, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+              tc::store_chunk(dh, dlo, R, r, NOUT / 8, gzc);
+            }
+          }
           if (h == 0) {
             c_drop += drop; c_zero += zero;
             if (use) {
@@ -487,7 +531,8 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
             const uint32_t xl = kk == 0 ? x0l : xh + (T::HF / 8) * CHR;
             issue_dx_r<R>(tbase + (kk == 0 ? T::C_DZ : T::C_ACC), dh, dl, w, w + TB::wbytes(kk), TB::out(kk),
                           kk > 0 ? W : NG);
-            issue_dw_m<R, T::dwm(kk)>(tbase + (uint32_t)T::dwcol(kk), xh, xl, dh, dl, TB::out(kk));
+            issue_dw_m<R, T::dwm(kk)>(tbase + (uint32_t)T::dwcol(kk), xh, xl, dh, dl,
+                                      TB::out(kk) + (kk == NL - 1 ? T::XD : 0));
             tc::mma_commit(bar_mma);
             if (kk == 0) tc::mma_commit(bar_x0e + s);   // X0 stage free once dW_0 has read it
           });
@@ -559,6 +604,18 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
         for (int o = 0; o < oh; ++o) atomicAdd(gp + o, vv[o]);
       }
     }
+    if constexpr (AH) {   // C-A34: the head's gradient, column NOUT of dW^T_{NL-1} -> GRADS
+      float gv[1];
+      tc::tmem_ldn<1>(tbase + lad + (uint32_t)(T::dwcol(NL - 1) + NOUT), gv);
+      tc::tmem_wait_ld();
+      int f = r;
+      bool ok = h == 0;
+      if (T::dwm(NL - 1) == 64) {
+        f = 16 * (warp & 3) + (lane & 15);
+        ok = ok && lane < 16;
+      }
+      if (ok && f <= W) atomicAdd(a.alpha_g + f, gv[0]);   // f = W: the ones row, dM2/dc
+    }
     loss = warp_sum_d(loss);
     c_used = warp_sum_u(c_used); c_zero = warp_sum_u(c_zero); c_drop = warp_sum_u(c_drop);
     if (lane == 0 && h == 0) {
@@ -587,6 +644,8 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
 #else
 #define NPM_WS_MSTAMP(kk, idx) do { } while (0)
 #endif
+    float sux = 0.f, suy = 0.f, suz = 0.f;   // the row's position in the tile to scatter
+    bool svalid = false;
     auto scatter = [&](int kd) {
       mbar_wait_idle(bar_dzf, (uint32_t)(kd & 1));
       NPM_WS_MSTAMP(kd + 1, 4);
@@ -597,9 +656,8 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
       if (kd + 1 < kt_end) mbar_wait_idle(bar_hs, (uint32_t)((kd + 1) & 1));
       NPM_WS_MSTAMP(kd + 1, 5);
       const float4* dz = reinterpret_cast<const float4*>(smem + T::OFF_DZ);
-      const float* uu = reinterpret_cast<const float*>(smem + T::OFF_DZ + (uint32_t)L * R * 16);
-      const float ux = uu[row], uy = uu[R + row], uz = uu[2 * R + row];
-      const bool valid = uu[3 * R + row] != 0.0f;
+      const float ux = sux, uy = suy, uz = suz;
+      const bool valid = svalid;
       float4 d[LP];
 #pragma unroll
       for (int l = 0; l < LP; ++l) d[l] = dz[(part * LP + l) * R + row];
@@ -636,7 +694,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
         uy = normalize_axis(__ldg(a.py + i), a.grid.lo[1], a.grid.inv[1]);
         uz = normalize_axis(__ldg(a.pz + i), a.grid.lo[2], a.grid.inv[2]);
       }
-      float hin[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f};
+      float hin[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f, 0.f};
       if (part == 0 && valid) {
         hin[0] = __ldg(a.wx + i); hin[1] = __ldg(a.wy + i); hin[2] = __ldg(a.wz + i);
         hin[3] = __ldg(a.target + i);
@@ -645,6 +703,7 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
           hin[5] = __ldg(a.target + 2 * a.target_stride + i);
         }
         hin[6] = __ldg(a.spdf + i);
+        if (AH) hin[7] = __ldg(a.bsdf_pdf + i);   // C-A34
       }
       const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (T::ZF / 8) * CHR;
       // all of this thread's levels in registers, then wait for the stage
@@ -671,14 +730,15 @@ __global__ void __launch_bounds__(WS<N>::THREADS, 1) train_ws_kernel(TrainArgs a
       for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
       if (part == 0) {
         float* rd = reinterpret_cast<float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
-        rd[row] = ux; rd[R + row] = uy; rd[2 * R + row] = uz; rd[3 * R + row] = valid ? 1.0f : 0.0f;
+        rd[3 * R + row] = valid ? 1.0f : 0.0f;
 #pragma unroll
-        for (int q = 0; q < 7; ++q) rd[(4 + q) * R + row] = hin[q];
+        for (int q = 0; q < (AH ? 8 : 7); ++q) rd[(4 + q) * R + row] = hin[q];
       }
       tc::fence_proxy_async();
       mbar_arrive(bar_x0f + s);
       NPM_WS_MSTAMP(kt, 3);
       if (kt > 0) scatter(kt - 1);
+      sux = ux; suy = uy; suz = uz; svalid = valid;
     }
     if (kt > 0) scatter(kt - 1);
 #undef NPM_WS_MSTAMP

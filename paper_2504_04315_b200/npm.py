@@ -41,7 +41,7 @@ class npm_config(ctypes.Structure):
                 ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
                 ("adam_eps", ctypes.c_float), ("ema_decay", ctypes.c_float),
                 ("kappa_min", ctypes.c_float), ("kappa_max", ctypes.c_float),
-                ("init_seed", ctypes.c_uint64), ("divergence", ctypes.c_int32)]
+                ("init_seed", ctypes.c_uint64), ("divergence", ctypes.c_int32), ("learn_alpha", ctypes.c_int32)]
 
 
 _FP = ctypes.POINTER(ctypes.c_float)
@@ -49,7 +49,8 @@ _FP = ctypes.POINTER(ctypes.c_float)
 
 class npm_query(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64)] + [(k, ctypes.c_void_p) for k in
-                                          ("px", "py", "pz", "wox", "woy", "woz", "nx", "ny", "nz", "rough")]
+                                          ("px", "py", "pz", "wox", "woy", "woz", "nx", "ny", "nz", "rough",
+                                           "bsdf_pdf")]
 
 
 class npm_step_stats(ctypes.Structure):
@@ -188,11 +189,11 @@ def npm_destroy(h):
     _check(_lib.npm_destroy(h))
 
 
-def make_query(n, px, py, pz, wox=None, woy=None, woz=None, nx=None, ny=None, nz=None, rough=None):
+def make_query(n, px, py, pz, wox=None, woy=None, woz=None, nx=None, ny=None, nz=None, rough=None, bsdf_pdf=None):
     q = npm_query()
     q.n = int(n)
-    for k, v in zip(("px", "py", "pz", "wox", "woy", "woz", "nx", "ny", "nz", "rough"),
-                    (px, py, pz, wox, woy, woz, nx, ny, nz, rough)):
+    for k, v in zip(("px", "py", "pz", "wox", "woy", "woz", "nx", "ny", "nz", "rough", "bsdf_pdf"),
+                    (px, py, pz, wox, woy, woz, nx, ny, nz, rough, bsdf_pdf)):
         setattr(q, k, _ptr(v))
     return q
 
@@ -410,7 +411,8 @@ class Model:
         self.device = torch.device("cuda", device)
         self.h = npm_create(self.cfg, device)
         self.n_grid, self.n_mlp = npm_param_count(self.h)
-        self.n_params = self.n_grid + self.n_mlp
+        self.n_alpha = (self.cfg.mlp_width + 1 + 3) // 4 * 4 if self.cfg.learn_alpha else 0
+        self.n_params = self.n_grid + self.n_mlp + self.n_alpha
         self.K = self.cfg.n_lobes
         self.L = self.cfg.n_levels
         self.F = self.cfg.n_features
@@ -442,16 +444,18 @@ class Model:
     def _empty(self, *shape, dtype=None):
         return self.torch.empty(*shape, device=self.device, dtype=dtype or self.torch.float32)
 
-    def query(self, x, wo=None, nrm=None, rough=None):
-        """x: [3, n]; product mode also wo [3, n], nrm [3, n], rough [n]."""
+    def query(self, x, wo=None, nrm=None, rough=None, bsdf_pdf=None):
+        """x: [3, n]; product mode also wo [3, n], nrm [3, n], rough [n];
+        bsdf_pdf [n]: training records of a learn_alpha model (C-A34)."""
         x = self._f32(x)
-        keep = [x]
+        pb = self._f32(bsdf_pdf)
+        keep = [x, pb]
         if self.product:
             wo, nrm, rough = self._f32(wo), self._f32(nrm), self._f32(rough)
             keep += [wo, nrm, rough]
-            q = make_query(x.shape[1], x[0], x[1], x[2], wo[0], wo[1], wo[2], nrm[0], nrm[1], nrm[2], rough)
+            q = make_query(x.shape[1], x[0], x[1], x[2], wo[0], wo[1], wo[2], nrm[0], nrm[1], nrm[2], rough, pb)
         else:
-            q = make_query(x.shape[1], x[0], x[1], x[2])
+            q = make_query(x.shape[1], x[0], x[1], x[2], bsdf_pdf=pb)
         q._keep = keep
         return q
 

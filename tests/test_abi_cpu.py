@@ -34,9 +34,10 @@ def test_struct_sizes_match_c_layout():
     # the library reports its compiled struct sizes (npm_abi_sizes)
     assert npm.npm_abi_sizes() == (ctypes.sizeof(npm.npm_config), ctypes.sizeof(npm.npm_query),
                                    ctypes.sizeof(npm.npm_step_stats))
-    # npm_config: 10 int32 + 6 float + 7 float + pad + uint64 + int32 divergence + pad
+    # npm_config: 10 int32 + 6 float + 7 float + pad + uint64 + int32 divergence + int32 learn_alpha
     assert ctypes.sizeof(npm.npm_config) == 10 * 4 + 6 * 4 + 7 * 4 + 4 + 8 + 4 + 4
-    assert ctypes.sizeof(npm.npm_query) == 8 + 10 * 8
+    # npm_query: n + 11 pointers (px..rough, bsdf_pdf)
+    assert ctypes.sizeof(npm.npm_query) == 8 + 11 * 8
     assert ctypes.sizeof(npm.npm_step_stats) == 6 * 8
 
 

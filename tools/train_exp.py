@@ -1,7 +1,7 @@
 """Measurement experiment (not part of the product): time the fused training
 kernel at c2 under different record orders / knobs, to see what the grid
 stage costs.  Usage: python tools/train_exp.py <variant>  (prints one line).
-Variants: shuffled, sorted (records Morton-sorted on the host by their
+Variants: shuffled, alpha (a learn_alpha model), sorted (records Morton-sorted on the host by their
 finest-level cell), and the env knobs NPM_DEBUG (bit 0: skip the scatter),
 NPM_BIN_TRAIN, NPM_PRIV set by the caller."""
 import os
@@ -33,14 +33,19 @@ def main():
     name = os.environ.get("EXP_WORKLOAD", "c2")
     cfg = CONFIGS[name]
     n = cfg["n"]
-    m = npm.Model(0, **cfg["model"])
+    alpha = variant == "alpha"     # learn_alpha model (f-4', C-A34): the selection head's cost
+    m = npm.Model(0, learn_alpha=int(alpha), **cfg["model"])
     tb = synth.training_batch(n, seed=200)
     if variant == "sorted":
         o = morton_order(tb["x"])
         tb = {k: (v[..., o] if isinstance(v, np.ndarray) and v.shape[-1] == n else v) for k, v in tb.items()}
     dev = torch.device("cuda", 0)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    q = m.query(T(tb["x"]))
+    pb = None
+    if alpha:
+        from oracle import guide   # measurement tool: the stand-in BSDF pdf of the records' directions
+        pb = T(guide.bsdf_pdf(tb["nrm"].astype(np.float64), tb["wi"].astype(np.float64)).astype(np.float32))
+    q = m.query(T(tb["x"]), bsdf_pdf=pb)
     wi, tg, pd = T(tb["wi"]), T(tb["target"]), T(tb["pdf"])
     for _ in range(3):
         m.accumulate_grads(q, wi, tg, pd, want_stats=False)
