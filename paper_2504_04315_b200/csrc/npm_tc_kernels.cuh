@@ -229,28 +229,34 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
   uint32_t phase = 0;
   const uint32_t xbuf[2] = {sb + gbase + T::QA, sb + gbase + T::QB};
   const uint32_t xlo[2] = {(uint32_t)(T::QAF / 8) * CH, (uint32_t)(W / 8) * CH};
-  // index + normalised position of this thread's row, prefetched one tile
-  // ahead (issued while the current tile's first MMA runs): the
-  // perm -> x -> gathers load chain was a third of the stall samples
+  // this thread's row, prefetched: the sample index two tiles ahead, the raw
+  // position one tile ahead (issued while the current tile's first MMA runs;
+  // normalised at use so nothing waits on the loads before the next tile)
   struct RowIn {
     int64_t i;
     bool valid;
-    float ux, uy, uz;
+    float x, y, z;
   };
-  auto load_row = [&](int64_t tl, RowIn& o) {
+  auto load_idx = [&](int64_t tl, int64_t& i, bool& v) {
     const int64_t slot = tl * R + r;                   // processing slot (spatially binned order)
-    o.valid = slot < n;
-    o.i = o.valid ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
-    o.ux = o.uy = o.uz = 0.0f;
-    if (o.valid && !a.feat_in) {
-      o.ux = normalize_axis(__ldg(a.px + o.i), a.grid.lo[0], a.grid.inv[0]);
-      o.uy = normalize_axis(__ldg(a.py + o.i), a.grid.lo[1], a.grid.inv[1]);
-      o.uz = normalize_axis(__ldg(a.pz + o.i), a.grid.lo[2], a.grid.inv[2]);
-    }
+    v = slot < n;
+    i = v ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;   // sample index
+  };
+  auto load_row = [&](int64_t i, bool v, RowIn& o) {
+    o.valid = v;
+    o.i = i;
+    o.x = o.y = o.z = 0.0f;
+    if (v && !a.feat_in) { o.x = __ldg(a.px + i); o.y = __ldg(a.py + i); o.z = __ldg(a.pz + i); }
   };
   RowIn nx_row;
+  int64_t nx_i = 0;
+  bool nx_v = false;
   const int64_t tile0 = (int64_t)blockIdx.x * GROUPS + g, tstep = (int64_t)gridDim.x * GROUPS;
-  if (tile0 < ntiles) load_row(tile0, nx_row);
+  if (tile0 < ntiles) {
+    load_idx(tile0, nx_i, nx_v);
+    load_row(nx_i, nx_v, nx_row);
+    if (tile0 + tstep < ntiles) load_idx(tile0 + tstep, nx_i, nx_v);
+  }
   int qt = 0;
 #ifdef NPM_QUERY_STAMPS
   const bool qstamp = a.dbg_clock && blockIdx.x == 0 && threadIdx.x == 0 && MODE == 0;
@@ -271,10 +277,30 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
 #pragma unroll
         for (int j = 0; j < GQ; ++j) g[j] = __ldg(a.feat_in + (int64_t)(q * GQ + j) * n + i);
       } else if (valid) {
-        const float ux = row.ux, uy = row.uy, uz = row.uz;
+        const float ux = normalize_axis(row.x, a.grid.lo[0], a.grid.inv[0]);
+        const float uy = normalize_axis(row.y, a.grid.lo[1], a.grid.inv[1]);
+        const float uz = normalize_axis(row.z, a.grid.lo[2], a.grid.inv[2]);
+#ifdef NPM_Q_PIPE   // level l + 1's loads issued before level l's blend
+        LevelCorners lcn;
+        float4 vn[8];
+        level_corners(a.grid, q * LQ, ux, uy, uz, lcn);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) vn[c] = __ldg(tab + a.grid.off[q * LQ] + lcn.idx[c]);
+#endif
 #pragma unroll
         for (int ll = 0; ll < LQ; ++ll) {
           const int l = q * LQ + ll;
+#ifdef NPM_Q_PIPE
+          float4 v[8];
+          LevelCorners lc = lcn;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = vn[c];
+          if (ll + 1 < LQ) {
+            level_corners(a.grid, l + 1, ux, uy, uz, lcn);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) vn[c] = __ldg(tab + a.grid.off[l + 1] + lcn.idx[c]);
+          }
+#else
           LevelCorners lc;
           level_corners(a.grid, l, ux, uy, uz, lc);
           // 8 single loads here: the binned query gathers are coherent already and
@@ -284,6 +310,7 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
           float4 v[8];
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[c] = __ldg(t + lc.idx[c]);
+#endif
           float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -326,7 +353,10 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
         issue_fwd(tbase, xbuf[src], xbuf[src] + xlo[src], w, w + T::wbytes(k), T::in_p(k), T::out(k));
         tc::mma_commit(mbar);
       }
-      if (k == 0 && tile + tstep < ntiles) load_row(tile + tstep, nx_row);
+      if (k == 0 && tile + tstep < ntiles) {
+        load_row(nx_i, nx_v, nx_row);
+        if (tile + 2 * tstep < ntiles) load_idx(tile + 2 * tstep, nx_i, nx_v);
+      }
       wait_mma(mbar, phase);
       QSTAMP(2 + 2 * k);
       float h[WQ];
@@ -472,13 +502,10 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
       const bool use_bsdf = COMBINED && u.w < alpha;
       const bool before = u.x < B[q] * invS;                 // an earlier quarter owns u1
       const bool after = u.x >= B[q + 1] * invS && q < TPR - 1;   // a later part owns u1
-      if (use_bsdf) {
-        if (q == 0) {
-          float wx, wy, wz;
-          bsdf_sample(__ldg(a.bnx + ic), __ldg(a.bny + ic), __ldg(a.bnz + ic), u.x, u.y, wx, wy, wz);
-          red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
-        }
-      } else if (!before && !after) {
+      // the part owning u1 hands its chosen lobe (kappa, mu) to part 0, which
+      // alone runs the sampler (one warp of the pair instead of both):
+      // rows 0 / 1 (softmax maxima, dead after the second barrier) and 6 / 7
+      if (!use_bsdf && !before && !after) {
         int sel = KQ - 1;
         float cum = B[q];
 #pragma unroll
@@ -490,8 +517,13 @@ __global__ void __launch_bounds__(GROUPS * TPR * R, GROUPS == 2 ? 1 : 4 / TPR) t
 #pragma unroll
         for (int j = 1; j < KQ; ++j)
           if (sel == j) { kk = kap[j]; mmx = mx[j]; mmy = my[j]; mmz = mz[j]; }
+        red[r] = kk; red[R + r] = mmx; red[(3 * TPR) * R + r] = mmy; red[(3 * TPR + 1) * R + r] = mmz;
+      }
+      psync();
+      if (q == 0) {
         float wx, wy, wz;
-        lobe_sample(kk, mmx, mmy, mmz, u.y, u.z, wx, wy, wz);
+        if (use_bsdf) bsdf_sample(__ldg(a.bnx + ic), __ldg(a.bny + ic), __ldg(a.bnz + ic), u.x, u.y, wx, wy, wz);
+        else lobe_sample(red[r], red[R + r], red[(3 * TPR) * R + r], red[(3 * TPR + 1) * R + r], u.y, u.z, wx, wy, wz);
         red[(3 * TPR) * R + r] = wx; red[(3 * TPR) * R + R + r] = wy; red[(3 * TPR) * R + 2 * R + r] = wz;
       }
       psync();
