@@ -108,6 +108,7 @@ struct npm_model {
   bool pipeline = true;    // NPM_PIPELINE=0 disables
   int pipe_chunks = 3;     // NPM_PIPE_CHUNKS (c2 e2e: 2 -> 1.31, 3 -> 1.32, 4 -> 1.28, 8 -> 1.13 G/s)
   int query_groups = 1;    // NPM_QUERY_GROUPS
+  int query_ws = 1;        // NPM_QUERY_WS
 };
 
 namespace {
@@ -359,6 +360,7 @@ void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryA
   a.log_kmin = logf(m->cfg.kappa_min);
   a.log_kmax = logf(m->cfg.kappa_max);
   a.query_groups = m->query_groups;
+  a.qws = m->query_ws;
   a.alpha_w = m->n_alpha ? a.params + m->n_mlp + m->n_grid : nullptr;
 }
 
@@ -631,6 +633,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // weights) gains (c4 query 2.38 -> 2.05 ms); c2 / c5 lose 5 % / 3 %.
   m->query_groups = c.mode == NPM_PRODUCT ? 2 : 1;
   if (const char* e = getenv("NPM_QUERY_GROUPS")) m->query_groups = atoi(e) == 2 ? 2 : 1;
+  if (const char* e = getenv("NPM_QUERY_WS")) m->query_ws = atoi(e);
   if (cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     delete m;
     return fail(NPM_ERR_CUDA, "no CUDA device");

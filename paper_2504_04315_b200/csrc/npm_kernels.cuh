@@ -48,6 +48,7 @@ struct QueryArgs {
   int query_groups;                   // 1: two 256-thread CTAs per SM; 2: one CTA, two groups (NPM_QUERY_GROUPS)
   long long* dbg_clock;               // measurement builds (-DNPM_QUERY_STAMPS): [64 tiles][16] stamps of CTA 0
   const float* alpha_w;               // C-A34 selection head (a [W], c) of `params`, or NULL: use `alpha`
+  int qws;                            // warp-specialised kernel for plain sample / pdf calls (NPM_QUERY_WS)
 };
 
 struct TrainArgs {

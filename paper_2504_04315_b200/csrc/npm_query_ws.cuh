@@ -1,0 +1,316 @@
+// npm_query_ws.cuh -- warp-specialised fused query kernel for the radiance
+// shapes with K = 8 lobes (c1, c2 / c3, c5): guide sampling (C-O10),
+// the pdf at the sample and the pdf at a caller direction (Eq. 3 mixture,
+// P:201-206), one persistent 512-thread CTA per SM.
+//
+//   warps 0-3, 4-7  CHAIN groups g = 0, 1: group g runs the CTA's tiles
+//       kt = g, g + 2, ... (a tile = 128 rows = the MMA M; thread = one row =
+//       one TMEM lane).  Per tile: the layer-0 MMA from the X0 stage, then per
+//       layer the epilogue (bias, ReLU, split-bf16 into the group's hidden
+//       buffer) and the next MMA, then the Table 1 head for all K lobes of the
+//       row (no exchange between threads): softmax, pdf at w_q, the lobe
+//       choice (C-A17), the Jakob sampler in the Duff ONB and the pdf at the
+//       sample.  The two groups interleave: one's MMA round trips and head
+//       overlap the other's.
+//   warps 8-15  MEMORY: thread (part, row), part = which half of the L grid
+//       levels.  For every tile in order: normalise x (C-O1), the 8 corners
+//       per level (Eq. 13, C-O3/C-O4), gather + blend (C-O5) into an X0 stage
+//       (split bf16, chunk-major) and the row data (sample index, validity,
+//       w_q, the three uniforms: caller's or Philox of the sample index,
+//       C-A18) into its row-data stage; S stages, so the gathers run ahead of
+//       the chains.
+//
+// mbarriers: x0f[s] (256 memory arrivals: stage filled), x0e[s] (128 chain
+// arrivals of the consuming group after its layer-0 MMA completed and the row
+// data is in registers: stage free), mma[g] (tcgen05.commit of group g).
+// Replaces the r01 query kernel for plain sample / pdf calls (the variants
+// with decode outputs, f-1, f-2 and the product shape keep it).
+#pragma once
+
+namespace qws {
+
+template <class N>
+struct QW {
+  using B = TC<N>;
+  static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN, L = N::L, K = N::K;
+  static constexpr int R = 128;
+  static constexpr uint32_t CHR = R * 16;
+  static constexpr int KIN = B::KIN;
+  static_assert(!N::PRODUCT && K == 8 && KIN == NIN && L % 4 == 0 && W % 16 == 0, "query_ws shape");
+  static constexpr int GROUPS = 2, CHAIN_THREADS = GROUPS * R, MEM_THREADS = 256;
+  static constexpr int THREADS = CHAIN_THREADS + MEM_THREADS;
+  static constexpr int RDF = 8;   // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u
+  static constexpr uint32_t X0_BYTES = 2u * (KIN / 8) * CHR;
+  static constexpr uint32_t H_BYTES = 2u * (W / 8) * CHR;
+  static constexpr uint32_t RD_BYTES = RDF * R * 4;
+  static constexpr uint32_t a1k(uint32_t x) { return (x + 1023u) & ~1023u; }
+  static constexpr uint32_t OFF_W = 0, OFF_B = B::WBYTES;
+  static constexpr uint32_t OFF_H = a1k(B::WBYTES + B::BBYTES);
+  static constexpr uint32_t OFF_X0 = OFF_H + GROUPS * H_BYTES;
+  // stages: 3 where the layout stays under the 164 KB carve-out (L1 for the gathers)
+  static constexpr int S = OFF_X0 + 3u * (X0_BYTES + RD_BYTES) + 1024u <= 164u * 1024u ? 3 : 2;
+  static constexpr uint32_t OFF_RD = OFF_X0 + (uint32_t)S * X0_BYTES;
+  static constexpr uint32_t OFF_BAR = OFF_RD + (uint32_t)S * RD_BYTES;
+  static constexpr int NBAR = 2 * S + GROUPS;
+  static constexpr uint32_t OFF_TSLOT = OFF_BAR + 8u * NBAR;
+  static constexpr uint32_t SMEM = OFF_TSLOT + 16u;
+  static_assert(SMEM <= 227u * 1024u, "query_ws smem");
+  static constexpr int TCOLS = 512;   // whole TMEM, base 0; group g: columns [64 g, 64 g + 64)
+  static_assert(W <= 64 && NOUT <= 64, "accumulator columns");
+};
+
+template <class N>
+__global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a) {
+  using T = QW<N>;
+  using TB = TC<N>;
+  constexpr int NL = N::NL, K = N::K, W = N::W, L = N::L, KIN = T::KIN;
+  constexpr int R = T::R, S = T::S;
+  constexpr uint32_t CHR = T::CHR;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+  uint64_t* bar_x0f = bars;
+  uint64_t* bar_x0e = bars + S;
+  uint64_t* bar_mma = bars + 2 * S;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_TSLOT);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(bar_x0f + s, T::MEM_THREADS);
+      tc::mbar_init(bar_x0e + s, R);
+    }
+    for (int g = 0; g < T::GROUPS; ++g) tc::mbar_init(bar_mma + g, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, (uint32_t)T::TCOLS);
+  stage_weights_tc<N>(a.params, smem, T::OFF_W, T::OFF_B);
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (*tslot != 0u) __trap();   // constant TMEM base 0 (the whole allocation)
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + R - 1) / R, tstride = gridDim.x;
+  const bool want_pdf = a.pdf != nullptr;
+
+  if (warp < 8) {
+    // =========================== CHAIN =====================================
+    const int g = warp >> 2;
+    const int gt = tid & (R - 1);                                 // thread in group = row
+    const int r = gt;
+    const uint32_t lad = (uint32_t)((warp & 3) * 32) << 16;       // TMEM lane field
+    const uint32_t tacc = (uint32_t)(64 * g);
+    const uint32_t hh = sb + T::OFF_H + (uint32_t)g * T::H_BYTES, hl = hh + (W / 8) * CHR;
+    const float* bias = reinterpret_cast<const float*>(smem + T::OFF_B);
+    uint64_t* bmma = bar_mma + g;
+    uint32_t phase = 0;
+    auto handoff = [&]() {
+      tc::fence_proxy_async();
+      tc::fence_before_sync();
+      tc::named_sync(1u + (uint32_t)g, (uint32_t)R);
+    };
+    auto wait_mma = [&]() {
+      ws::mbar_wait_t(bmma, phase);
+      phase ^= 1u;
+      tc::fence_after_sync();
+    };
+    int kt = g;
+    for (int64_t tile = blockIdx.x + (int64_t)g * tstride; tile < ntiles; tile += 2 * tstride, kt += 2) {
+      const int s = kt % S;
+      const uint32_t x0h = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, x0l = x0h + (KIN / 8) * CHR;
+      ws::mbar_wait_t(bar_x0f + s, (uint32_t)((kt / S) & 1));
+      tc::fence_after_sync();
+      if (gt == 0) {
+        const uint32_t w = sb + T::OFF_W + TB::woff(0);
+        issue_fwd(tacc, x0h, x0l, w, w + TB::wbytes(0), KIN, TB::out(0));
+        tc::mma_commit(bmma);
+      }
+      const float* rd = reinterpret_cast<const float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
+      const int64_t i = (int64_t)__float_as_uint(rd[r]);
+      const bool valid = rd[R + r] != 0.0f;
+      const float qx = rd[2 * R + r], qy = rd[3 * R + r], qz = rd[4 * R + r];
+      const float u1 = rd[5 * R + r], u2 = rd[6 * R + r], u3 = rd[7 * R + r];
+      wait_mma();
+      ws::mbar_arrive(bar_x0e + s);   // X0 read by the MMA, row data in registers
+      // ---- hidden layers: epilogue of layer k, MMA of layer k + 1
+#pragma unroll
+      for (int k = 0; k < NL - 1; ++k) {
+        const float* b = bias + TB::boff(k) / 4;
+#pragma unroll
+        for (int c16 = 0; c16 < W; c16 += 16) {
+          float v[16];
+          tc::tmem_ldn<16>(lad + tacc + (uint32_t)c16, v);
+          tc::tmem_wait_ld();
+          const float4* b4 = reinterpret_cast<const float4*>(b + c16);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 bb = b4[j];
+            v[4 * j] = fmaxf(v[4 * j] + bb.x, 0.0f);
+            v[4 * j + 1] = fmaxf(v[4 * j + 1] + bb.y, 0.0f);
+            v[4 * j + 2] = fmaxf(v[4 * j + 2] + bb.z, 0.0f);
+            v[4 * j + 3] = fmaxf(v[4 * j + 3] + bb.w, 0.0f);
+          }
+          tc::store_chunk(hh, hl, R, r, c16 / 8, v);
+          tc::store_chunk(hh, hl, R, r, c16 / 8 + 1, v + 8);
+        }
+        handoff();
+        if (gt == 0) {
+          tc::fence_after_sync();
+          const uint32_t w = sb + T::OFF_W + TB::woff(k + 1);
+          issue_fwd(tacc, hh, hl, w, w + TB::wbytes(k + 1), TB::in_p(k + 1), TB::out(k + 1));
+          tc::mma_commit(bmma);
+        }
+        wait_mma();
+      }
+      // ---- Table 1 head, all K lobes of this row
+      float lp[K], kp[K], tp[K], pp[K];
+      tc::tmem_ldn<K>(lad + tacc, lp);
+      tc::tmem_ldn<K>(lad + tacc + (uint32_t)K, kp);
+      tc::tmem_ldn<K>(lad + tacc + (uint32_t)(2 * K), tp);
+      tc::tmem_ldn<K>(lad + tacc + (uint32_t)(3 * K), pp);
+      tc::tmem_wait_ld();
+      // the group's next layer-0 MMA overwrites these columns: every thread's
+      // read first
+      tc::fence_before_sync();
+      tc::named_sync(1u + (uint32_t)g, (uint32_t)R);
+#ifdef NPM_QWS_NOHEAD   // measurement variant: no Table 1 head
+      if (valid) a.spdf[i] = lp[0] + kp[1] + tp[2] + pp[3] + qx + u1 + u2 + u3 + qy + qz;
+      continue;
+#endif
+      const float* b = bias + TB::boff(NL - 1) / 4;
+      float kap[K], mx[K], my[K], mz[K], nrm[K];
+      float M = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        lp[j] += b[j];
+        M = fmaxf(M, lp[j]);
+        kap[j] = __expf(fminf(fmaxf(kp[j] + b[K + j], a.log_kmin), a.log_kmax));
+        float th, ph, st, ct, sp, cp;
+        lobe_angles(tp[j] + b[2 * K + j], pp[j] + b[3 * K + j], kap[j], th, ph, st, ct, sp, cp);
+        mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
+        float em;
+        nrm[j] = lobe_norm(kap[j], em);
+      }
+      float e[K], Ssum = 0.0f, P = 0.0f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        e[j] = __expf(lp[j] - M);
+        Ssum += e[j];
+        if (want_pdf) P += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], qx, qy, qz);
+      }
+      const float invS = 1.0f / Ssum;
+      if (want_pdf && valid) a.pdf[i] = P * invS;
+      if (a.do_sample) {
+        // i* = min{i : u1 < C_i}, C_i = sum_{j<=i} lambda_j; K-1 if none (C-A17)
+        int sel = K - 1;
+        float cum = 0.0f;
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) {
+          cum += e[j];
+          if (sel == K - 1 && u1 < cum * invS) sel = j;
+        }
+        float kk = kap[0], mmx = mx[0], mmy = my[0], mmz = mz[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j)
+          if (sel == j) { kk = kap[j]; mmx = mx[j]; mmy = my[j]; mmz = mz[j]; }
+        float wx, wy, wz;
+        lobe_sample(kk, mmx, mmy, mmz, u2, u3, wx, wy, wz);
+        float P2 = 0.0f;
+#pragma unroll
+        for (int j = 0; j < K; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
+        if (valid) {
+          a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
+          a.spdf[i] = P2 * invS;
+        }
+      }
+    }
+  } else {
+    // =========================== MEMORY ====================================
+    const int m = tid - T::CHAIN_THREADS;
+    const int row = m & (R - 1), part = m >> 7;
+    constexpr int LP = L / 2;
+    const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
+    // the row's sample index is loaded two tiles ahead and its raw position
+    // one tile ahead, so the perm -> x -> corner-index chain of dependent
+    // loads is off the gathers' path
+    auto load_idx = [&](int64_t tl, int64_t& i, bool& v) {
+      const int64_t slot = tl * R + row;
+      v = slot < n;
+      i = v ? (a.perm ? (int64_t)__ldg(a.perm + slot) : slot) : 0;
+    };
+    auto load_x = [&](int64_t i, bool v, float* x) {
+      x[0] = x[1] = x[2] = 0.0f;
+      if (v) { x[0] = __ldg(a.px + i); x[1] = __ldg(a.py + i); x[2] = __ldg(a.pz + i); }
+    };
+    int64_t i_n = 0, i_nn = 0;
+    bool v_n = false, v_nn = false;
+    float x_n[3];
+    if (blockIdx.x < ntiles) load_idx(blockIdx.x, i_n, v_n);
+    load_x(i_n, v_n, x_n);
+    if (blockIdx.x + tstride < ntiles) load_idx(blockIdx.x + tstride, i_nn, v_nn);
+    int kt = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += tstride, ++kt) {
+      const int s = kt % S;
+      const int64_t i = i_n;
+      const bool valid = v_n;
+      const float x0 = x_n[0], x1 = x_n[1], x2 = x_n[2];
+      i_n = i_nn; v_n = v_nn;
+      load_x(i_n, v_n, x_n);
+      v_nn = false;
+      if (tile + 2 * tstride < ntiles) load_idx(tile + 2 * tstride, i_nn, v_nn);
+      float ux = 0.f, uy = 0.f, uz = 0.f;
+      if (valid) {
+        ux = normalize_axis(x0, a.grid.lo[0], a.grid.inv[0]);
+        uy = normalize_axis(x1, a.grid.lo[1], a.grid.inv[1]);
+        uz = normalize_axis(x2, a.grid.lo[2], a.grid.inv[2]);
+      }
+      float ex[3] = {0.f, 0.f, 0.f};   // part 0: w_q; part 1: the uniforms
+      if (part == 0) {
+        if (want_pdf) { ex[0] = __ldg(a.wx + i); ex[1] = __ldg(a.wy + i); ex[2] = __ldg(a.wz + i); }
+      } else if (a.do_sample) {
+        if (a.u) {
+          ex[0] = __ldg(a.u + i); ex[1] = __ldg(a.u + n + i); ex[2] = __ldg(a.u + 2 * n + i);
+        } else {
+          const float4 u = philox_uniforms4(a.seed, (uint64_t)i + a.offset);
+          ex[0] = u.x; ex[1] = u.y; ex[2] = u.z;
+        }
+      }
+      float gf[4 * LP];
+#pragma unroll
+      for (int q = 0; q < LP; ++q) {
+        float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
+#ifdef NPM_QWS_NOGATHER   // measurement variant: no grid gathers
+        if (false) {
+#else
+        if (valid) {
+#endif
+          const int l = part * LP + q;
+          LevelCorners lc;
+          level_corners(a.grid, l, ux, uy, uz, lc);
+          gl = gather_level<false>(tab, a.grid.off[l], lc);
+        }
+        gf[4 * q] = gl.x; gf[4 * q + 1] = gl.y; gf[4 * q + 2] = gl.z; gf[4 * q + 3] = gl.w;
+      }
+      ws::mbar_wait_idle(bar_x0e + s, (uint32_t)(((kt / S) & 1) ^ 1));
+      const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (KIN / 8) * CHR;
+#pragma unroll
+      for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
+      float* rd = reinterpret_cast<float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
+      if (part == 0) {
+        rd[row] = __uint_as_float((uint32_t)i);
+        rd[R + row] = valid ? 1.0f : 0.0f;
+        rd[2 * R + row] = ex[0]; rd[3 * R + row] = ex[1]; rd[4 * R + row] = ex[2];
+      } else {
+        rd[5 * R + row] = ex[0]; rd[6 * R + row] = ex[1]; rd[7 * R + row] = ex[2];
+      }
+      tc::fence_proxy_async();
+      ws::mbar_arrive(bar_x0f + s);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(*tslot, (uint32_t)T::TCOLS);
+}
+
+}  // namespace qws

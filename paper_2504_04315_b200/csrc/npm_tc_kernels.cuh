@@ -1140,11 +1140,23 @@ __global__ void __launch_bounds__(512, 1) tc_train64_kernel(TrainArgs a) {
 }
 
 #include "npm_train_ws.cuh"
+#include "npm_query_ws.cuh"
 
 template <class N>
 struct TcLaunch {
   static int query(const QueryArgs& a, int sms, cudaStream_t st) {
     using T = TC<N>;
+    if constexpr (!N::PRODUCT && N::K == 8) {
+      // warp-specialised kernel for plain sample / pdf calls (npm_query_ws.cuh)
+      if (a.qws && !a.combined && !a.cos_product && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
+        using Q = qws::QW<N>;
+        cudaFuncSetAttribute(qws::query_ws_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
+        const int64_t ntiles = (a.n + Q::R - 1) / Q::R;
+        const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
+        qws::query_ws_kernel<N><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
+        return 1;
+      }
+    }
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA
     // waits interleave); ~104 KB smem each.
     constexpr int TPR = 2;
