@@ -1061,25 +1061,29 @@ npm_status npm_sample(npm_model* m, const npm_query* q, const float* u, uint64_t
   if (dbg && (atoi(dbg) & 4)) {   // measurement only: per-phase stamps of CTA 0 (NPM_QUERY_STAMPS builds)
     CUDA_TRY(m->dbg_clock.ensure(2 * 64 * 16 * sizeof(long long)));
     a.dbg_clock = static_cast<long long*>(m->dbg_clock.p);
-    CUDA_TRY(cudaMemsetAsync(a.dbg_clock, 0, 64 * 16 * sizeof(long long), st));
+    CUDA_TRY(cudaMemsetAsync(a.dbg_clock, 0, 2 * 64 * 16 * sizeof(long long), st));
   }
   r = query_launch(m, a, st);
   if (r != NPM_OK) return r;
   if (a.dbg_clock) {
-    long long h[64 * 16];
+    long long h[2 * 64 * 16];
     CUDA_TRY(cudaMemcpyAsync(h, a.dbg_clock, sizeof(h), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    double since[16] = {};
-    int cs = 0;
-    for (int t = 1; t < 63; ++t) {
-      if (h[(t + 1) * 16] == 0) break;
-      for (int j = 1; j < 16; ++j) if (h[t * 16 + j]) since[j] += (double)(h[t * 16 + j] - h[t * 16]);
-      since[15] += (double)(h[(t + 1) * 16] - h[t * 16]);
-      ++cs;
+    for (int ser = 0; ser < 2; ++ser) {   // series 0: chain / r01 kernel; 1: query_ws memory warps
+      const long long* hs = h + ser * 64 * 16;
+      double since[16] = {};
+      int cs = 0;
+      for (int t = 1; t < 63; ++t) {
+        if (hs[(t + 1) * 16] == 0) break;
+        for (int j = 1; j < 15; ++j) if (hs[t * 16 + j]) since[j] += (double)(hs[t * 16 + j] - hs[t * 16]);
+        since[15] += (double)(hs[(t + 1) * 16] - hs[t * 16]);
+        ++cs;
+      }
+      if (!cs) continue;
+      fprintf(stderr, "NPM_QSTAMPS%s tiles=%d", ser ? "_MEM" : "", cs);
+      for (int j = 1; j < 16; ++j) fprintf(stderr, " s%d=%.0f", j, since[j] / cs);
+      fprintf(stderr, "\n");
     }
-    fprintf(stderr, "NPM_QSTAMPS tiles=%d", cs);
-    for (int j = 1; j < 16; ++j) fprintf(stderr, " s%d=%.0f", j, cs ? since[j] / cs : 0.0);
-    fprintf(stderr, "\n");
   }
   CUDA_TRY(s.finish());
   return NPM_OK;

@@ -29,6 +29,9 @@
 
 namespace qws {
 
+// MP: memory parts (levels L / MP per thread).  2: 8 memory warps, every
+// warp at 128 registers.  4 (measurement): 16 memory warps at 64 registers and
+// the chain at 112 via setmaxnreg -- no faster (the chain is the bound).
 template <class N>
 struct QW {
   using B = TC<N>;
@@ -37,8 +40,19 @@ struct QW {
   static constexpr uint32_t CHR = R * 16;
   static constexpr int KIN = B::KIN;
   static_assert(!N::PRODUCT && K == 8 && KIN == NIN && L % 4 == 0 && W % 16 == 0, "query_ws shape");
-  static constexpr int GROUPS = 2, CHAIN_THREADS = GROUPS * R, MEM_THREADS = 256;
+#ifdef NPM_QWS_MP   // measurement override (4: B200 c2 233 us vs 229 us with 2)
+  static constexpr int MP = NPM_QWS_MP;
+#else
+  static constexpr int MP = 2;
+#endif
+  static_assert((L / MP) % 2 == 0, "two levels (8 features) per X0 chunk");
+  static constexpr int GROUPS = 2, CHAIN_THREADS = GROUPS * R, MEM_THREADS = MP * R;
+  // MP = 4 register split (setmaxnreg moves registers only within the CTA's
+  // launch allocation, 768 x 80): 256 x 112 + 512 x 64 = 768 x 80 (the chain
+  // code needs 92)
+  static constexpr int CHAIN_REGS = 112, MEM_REGS = 64, LAUNCH_REGS = 80;
   static constexpr int THREADS = CHAIN_THREADS + MEM_THREADS;
+  static_assert(MP != 4 || CHAIN_THREADS * CHAIN_REGS + MEM_THREADS * MEM_REGS <= THREADS * LAUNCH_REGS, "regs");
   static constexpr int RDF = 8;   // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u
   static constexpr uint32_t X0_BYTES = 2u * (KIN / 8) * CHR;
   static constexpr uint32_t H_BYTES = 2u * (W / 8) * CHR;
@@ -95,6 +109,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
 
   if (warp < 8) {
     // =========================== CHAIN =====================================
+    if constexpr (T::MP == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(T::CHAIN_REGS));
     const int g = warp >> 2;
     const int gt = tid & (R - 1);                                 // thread in group = row
     const int r = gt;
@@ -114,11 +129,19 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       phase ^= 1u;
       tc::fence_after_sync();
     };
+#ifdef NPM_QWS_STAMPS   // measurement builds: phase stamps of CTA 0, group 0, row 0
+    const bool stamp = a.dbg_clock && blockIdx.x == 0 && g == 0 && gt == 0;
+#define QWS_STAMP(idx) do { if (stamp && kt / 2 < 64) a.dbg_clock[(kt / 2) * 16 + (idx)] = clock64(); } while (0)
+#else
+#define QWS_STAMP(idx) do { } while (0)
+#endif
     int kt = g;
     for (int64_t tile = blockIdx.x + (int64_t)g * tstride; tile < ntiles; tile += 2 * tstride, kt += 2) {
+      QWS_STAMP(0);
       const int s = kt % S;
       const uint32_t x0h = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, x0l = x0h + (KIN / 8) * CHR;
       ws::mbar_wait_t(bar_x0f + s, (uint32_t)((kt / S) & 1));
+      QWS_STAMP(1);
       tc::fence_after_sync();
       if (gt == 0) {
         const uint32_t w = sb + T::OFF_W + TB::woff(0);
@@ -131,29 +154,30 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       const float qx = rd[2 * R + r], qy = rd[3 * R + r], qz = rd[4 * R + r];
       const float u1 = rd[5 * R + r], u2 = rd[6 * R + r], u3 = rd[7 * R + r];
       wait_mma();
+      QWS_STAMP(2);
       ws::mbar_arrive(bar_x0e + s);   // X0 read by the MMA, row data in registers
       // ---- hidden layers: epilogue of layer k, MMA of layer k + 1
 #pragma unroll
       for (int k = 0; k < NL - 1; ++k) {
         const float* b = bias + TB::boff(k) / 4;
+        // all W columns in flight at once (one TMEM round trip)
+        float v[W];
 #pragma unroll
-        for (int c16 = 0; c16 < W; c16 += 16) {
-          float v[16];
-          tc::tmem_ldn<16>(lad + tacc + (uint32_t)c16, v);
-          tc::tmem_wait_ld();
-          const float4* b4 = reinterpret_cast<const float4*>(b + c16);
+        for (int c16 = 0; c16 < W; c16 += 16) tc::tmem_ldn<16>(lad + tacc + (uint32_t)c16, v + c16);
+        tc::tmem_wait_ld();
+        const float4* b4 = reinterpret_cast<const float4*>(b);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 bb = b4[j];
-            v[4 * j] = fmaxf(v[4 * j] + bb.x, 0.0f);
-            v[4 * j + 1] = fmaxf(v[4 * j + 1] + bb.y, 0.0f);
-            v[4 * j + 2] = fmaxf(v[4 * j + 2] + bb.z, 0.0f);
-            v[4 * j + 3] = fmaxf(v[4 * j + 3] + bb.w, 0.0f);
-          }
-          tc::store_chunk(hh, hl, R, r, c16 / 8, v);
-          tc::store_chunk(hh, hl, R, r, c16 / 8 + 1, v + 8);
+        for (int j = 0; j < W / 4; ++j) {
+          const float4 bb = b4[j];
+          v[4 * j] = fmaxf(v[4 * j] + bb.x, 0.0f);
+          v[4 * j + 1] = fmaxf(v[4 * j + 1] + bb.y, 0.0f);
+          v[4 * j + 2] = fmaxf(v[4 * j + 2] + bb.z, 0.0f);
+          v[4 * j + 3] = fmaxf(v[4 * j + 3] + bb.w, 0.0f);
         }
+#pragma unroll
+        for (int c8 = 0; c8 < W / 8; ++c8) tc::store_chunk(hh, hl, R, r, c8, v + 8 * c8);
         handoff();
+        QWS_STAMP(3 + 2 * k);
         if (gt == 0) {
           tc::fence_after_sync();
           const uint32_t w = sb + T::OFF_W + TB::woff(k + 1);
@@ -161,6 +185,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           tc::mma_commit(bmma);
         }
         wait_mma();
+        QWS_STAMP(4 + 2 * k);
       }
       // ---- Table 1 head, all K lobes of this row
       float lp[K], kp[K], tp[K], pp[K];
@@ -173,6 +198,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       // read first
       tc::fence_before_sync();
       tc::named_sync(1u + (uint32_t)g, (uint32_t)R);
+      QWS_STAMP(3 + 2 * (NL - 1));
 #ifdef NPM_QWS_NOHEAD   // measurement variant: no Table 1 head
       if (valid) a.spdf[i] = lp[0] + kp[1] + tp[2] + pp[3] + qx + u1 + u2 + u3 + qy + qz;
       continue;
@@ -180,16 +206,32 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       const float* b = bias + TB::boff(NL - 1) / 4;
       float kap[K], mx[K], my[K], mz[K], nrm[K];
       float M = -INFINITY;
+      bool conc = false;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
+      for (int j = 0; j < K; ++j) {   // branch-free over the lobes (they interleave)
         lp[j] += b[j];
+        tp[j] += b[2 * K + j];
+        pp[j] += b[3 * K + j];
         M = fmaxf(M, lp[j]);
         kap[j] = __expf(fminf(fmaxf(kp[j] + b[K + j], a.log_kmin), a.log_kmax));
         float th, ph, st, ct, sp, cp;
-        lobe_angles(tp[j] + b[2 * K + j], pp[j] + b[3 * K + j], kap[j], th, ph, st, ct, sp, cp);
+        lobe_angles<false>(tp[j], pp[j], kap[j], th, ph, st, ct, sp, cp);
         mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
         float em;
-        nrm[j] = lobe_norm(kap[j], em);
+        nrm[j] = lobe_norm_fast(kap[j], em);
+        conc |= kap[j] > 1e3f;
+      }
+      // concentrated lobes: Table 1's angles precisely (lobe_angles<true>, C-A33),
+      // only in warps that have one
+      if (__any_sync(0xffffffffu, conc)) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          if (kap[j] > 1e3f) {
+            float th, ph, st, ct, sp, cp;
+            lobe_angles<true>(tp[j], pp[j], kap[j], th, ph, st, ct, sp, cp);
+            mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
+          }
+        }
       }
       float e[K], Ssum = 0.0f, P = 0.0f;
 #pragma unroll
@@ -223,12 +265,15 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           a.spdf[i] = P2 * invS;
         }
       }
+      QWS_STAMP(4 + 2 * (NL - 1));
     }
+#undef QWS_STAMP
   } else {
     // =========================== MEMORY ====================================
+    if constexpr (T::MP == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(T::MEM_REGS));
     const int m = tid - T::CHAIN_THREADS;
     const int row = m & (R - 1), part = m >> 7;
-    constexpr int LP = L / 2;
+    constexpr int LP = L / T::MP;
     const float4* tab = reinterpret_cast<const float4*>(a.params + N::N_MLP);
     // the row's sample index is loaded two tiles ahead and its raw position
     // one tile ahead, so the perm -> x -> corner-index chain of dependent
@@ -248,8 +293,15 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
     if (blockIdx.x < ntiles) load_idx(blockIdx.x, i_n, v_n);
     load_x(i_n, v_n, x_n);
     if (blockIdx.x + tstride < ntiles) load_idx(blockIdx.x + tstride, i_nn, v_nn);
+#ifdef NPM_QWS_STAMPS
+    const bool mstamp = a.dbg_clock && blockIdx.x == 0 && m == 0;
+#define QWS_MSTAMP(idx) do { if (mstamp && kt < 64) a.dbg_clock[64 * 16 + kt * 16 + (idx)] = clock64(); } while (0)
+#else
+#define QWS_MSTAMP(idx) do { } while (0)
+#endif
     int kt = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += tstride, ++kt) {
+      QWS_MSTAMP(0);
       const int s = kt % S;
       const int64_t i = i_n;
       const bool valid = v_n;
@@ -267,7 +319,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       float ex[3] = {0.f, 0.f, 0.f};   // part 0: w_q; part 1: the uniforms
       if (part == 0) {
         if (want_pdf) { ex[0] = __ldg(a.wx + i); ex[1] = __ldg(a.wy + i); ex[2] = __ldg(a.wz + i); }
-      } else if (a.do_sample) {
+      } else if (part == 1 && a.do_sample) {
         if (a.u) {
           ex[0] = __ldg(a.u + i); ex[1] = __ldg(a.u + n + i); ex[2] = __ldg(a.u + 2 * n + i);
         } else {
@@ -291,7 +343,9 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
         }
         gf[4 * q] = gl.x; gf[4 * q + 1] = gl.y; gf[4 * q + 2] = gl.z; gf[4 * q + 3] = gl.w;
       }
+      QWS_MSTAMP(1);
       ws::mbar_wait_idle(bar_x0e + s, (uint32_t)(((kt / S) & 1) ^ 1));
+      QWS_MSTAMP(2);
       const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (KIN / 8) * CHR;
 #pragma unroll
       for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
@@ -300,12 +354,14 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
         rd[row] = __uint_as_float((uint32_t)i);
         rd[R + row] = valid ? 1.0f : 0.0f;
         rd[2 * R + row] = ex[0]; rd[3 * R + row] = ex[1]; rd[4 * R + row] = ex[2];
-      } else {
+      } else if (part == 1) {
         rd[5 * R + row] = ex[0]; rd[6 * R + row] = ex[1]; rd[7 * R + row] = ex[2];
       }
       tc::fence_proxy_async();
       ws::mbar_arrive(bar_x0f + s);
+      QWS_MSTAMP(3);
     }
+#undef QWS_MSTAMP
   }
   tc::fence_before_sync();
   __syncthreads();

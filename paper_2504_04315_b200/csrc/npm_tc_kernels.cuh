@@ -1150,6 +1150,14 @@ struct TcLaunch {
       // warp-specialised kernel for plain sample / pdf calls (npm_query_ws.cuh)
       if (a.qws && !a.combined && !a.cos_product && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
         using Q = qws::QW<N>;
+        if (Q::MP == 4) {   // the setmaxnreg split assumes the launch allocation (a hang otherwise)
+          static int regs = -1;
+          if (regs < 0) {
+            cudaFuncAttributes fa;
+            regs = cudaFuncGetAttributes(&fa, qws::query_ws_kernel<N>) == cudaSuccess ? fa.numRegs : 0;
+          }
+          if (regs != Q::LAUNCH_REGS) return -1;
+        }
         cudaFuncSetAttribute(qws::query_ws_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
         const int64_t ntiles = (a.n + Q::R - 1) / Q::R;
         const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
