@@ -151,6 +151,12 @@ __device__ __forceinline__ void ld_pair(const float4* p, float4& lo, float4& hi)
       : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
       : "l"(p));
 }
+// the same 32-byte load allocating in L1 (coherent, binned query gathers)
+__device__ __forceinline__ void ld_pair_l1(const float4* p, float4& lo, float4& hi) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(p));
+}
 
 // The 32-byte pair loads bypass L1 allocation (the training gathers hit L1
 // 8.9 % of the time): B200, c2 train 646 -> 630 us, c5 5.34 -> 5.04 ms.  The
@@ -158,7 +164,7 @@ __device__ __forceinline__ void ld_pair(const float4* p, float4& lo, float4& hi)
 // PAIRS = false: eight plain 16-byte loads (the warp-specialised training
 // kernel's memory warps: fewer ALU / select instructions next to the chain;
 // B200 c2 -1.4 %).
-template <bool PAIRS = true>
+template <bool PAIRS = true, bool L1A = false>
 __device__ __forceinline__ float4 gather_level(const float4* __restrict__ tab, uint32_t off, const LevelCorners& lc) {
   float4 v[8];
   if constexpr (!PAIRS) {
@@ -176,7 +182,8 @@ __device__ __forceinline__ float4 gather_level(const float4* __restrict__ tab, u
   for (int p = 0; p < 4; ++p) {
     const uint32_t e0 = off + lc.idx[2 * p], e1 = off + lc.idx[2 * p + 1];
     float4 lo, hi;
-    ld_pair(tab + (e0 & ~1u), lo, hi);
+    if constexpr (L1A) ld_pair_l1(tab + (e0 & ~1u), lo, hi);
+    else ld_pair(tab + (e0 & ~1u), lo, hi);
     v[2 * p] = (e0 & 1u) ? hi : lo;
     if ((e0 ^ e1) == 1u) v[2 * p + 1] = (e1 & 1u) ? hi : lo;
     else v[2 * p + 1] = __ldg(tab + e1);

@@ -46,7 +46,17 @@ struct QW {
   static constexpr int MP = 2;
 #endif
   static_assert((L / MP) % 2 == 0, "two levels (8 features) per X0 chunk");
-  static constexpr int GROUPS = 2, CHAIN_THREADS = GROUPS * R, MEM_THREADS = MP * R;
+  // TPR: chain threads per row.  1: a thread runs all K lobes of its row (no
+  // exchanges); 2: warps w and w + 4 of a group split the row's columns and
+  // lobes and exchange softmax / mixture sums / the sample through smem
+#ifdef NPM_QWS_TPR   // measurement override (1: B200 c2 232 us vs 210 us with 2)
+  static constexpr int TPR = NPM_QWS_TPR;
+#else
+  static constexpr int TPR = 2;
+#endif
+  static_assert(TPR == 1 || TPR == 2, "threads per row");
+  static constexpr int GROUPS = 2, GROUP_THREADS = TPR * R, CHAIN_THREADS = GROUPS * GROUP_THREADS;
+  static constexpr int MEM_THREADS = MP * R;
   // MP = 4 register split (setmaxnreg moves registers only within the CTA's
   // launch allocation, 768 x 80): 256 x 112 + 512 x 64 = 768 x 80 (the chain
   // code needs 92)
@@ -60,7 +70,12 @@ struct QW {
   static constexpr uint32_t a1k(uint32_t x) { return (x + 1023u) & ~1023u; }
   static constexpr uint32_t OFF_W = 0, OFF_B = B::WBYTES;
   static constexpr uint32_t OFF_H = a1k(B::WBYTES + B::BBYTES);
-  static constexpr uint32_t OFF_X0 = OFF_H + GROUPS * H_BYTES;
+  // TPR = 2 head exchange per group [RED_ROWS][R] f32: 0-1 max, 2-3 sums,
+  // 4-5 pdf at w_q, 6-8 the sample, 9-10 pdf at the sample (part h in row +h)
+  static constexpr int RED_ROWS = TPR == 2 ? 11 : 0;
+  static constexpr uint32_t RED_BYTES = (uint32_t)RED_ROWS * R * 4u;
+  static constexpr uint32_t OFF_RED = OFF_H + GROUPS * H_BYTES;
+  static constexpr uint32_t OFF_X0 = a1k(OFF_RED + GROUPS * RED_BYTES);
   // stages: 3 where the layout stays under the 164 KB carve-out (L1 for the gathers)
   static constexpr int S = OFF_X0 + 3u * (X0_BYTES + RD_BYTES) + 1024u <= 164u * 1024u ? 3 : 2;
   static constexpr uint32_t OFF_RD = OFF_X0 + (uint32_t)S * X0_BYTES;
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(bar_x0f + s, T::MEM_THREADS);
-      tc::mbar_init(bar_x0e + s, R);
+      tc::mbar_init(bar_x0e + s, T::GROUP_THREADS);
     }
     for (int g = 0; g < T::GROUPS; ++g) tc::mbar_init(bar_mma + g, 1);
     tc::fence_mbar_init();
@@ -107,12 +122,17 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
   const int64_t ntiles = (n + R - 1) / R, tstride = gridDim.x;
   const bool want_pdf = a.pdf != nullptr;
 
-  if (warp < 8) {
+  constexpr int TPR = T::TPR;
+  if (warp < T::CHAIN_THREADS / 32) {
     // =========================== CHAIN =====================================
     if constexpr (T::MP == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(T::CHAIN_REGS));
-    const int g = warp >> 2;
-    const int gt = tid & (R - 1);                                 // thread in group = row
-    const int r = gt;
+    const int g = warp / (4 * TPR);
+    const int gt = tid - g * T::GROUP_THREADS;                    // thread in group
+    const int h = (warp >> 2) & (TPR - 1);                        // part of the row
+    const int r = ((warp & 3) << 5) | lane;                       // row = TMEM lane
+    constexpr int WQ = W / TPR, KQ = K / TPR;
+    float* red = reinterpret_cast<float*>(smem + T::OFF_RED + (uint32_t)g * T::RED_BYTES);
+    auto psync = [&]() { tc::named_sync(3u + 4u * (uint32_t)g + (uint32_t)(warp & 3), 64u); };
     const uint32_t lad = (uint32_t)((warp & 3) * 32) << 16;       // TMEM lane field
     const uint32_t tacc = (uint32_t)(64 * g);
     const uint32_t hh = sb + T::OFF_H + (uint32_t)g * T::H_BYTES, hl = hh + (W / 8) * CHR;
@@ -122,7 +142,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
     auto handoff = [&]() {
       tc::fence_proxy_async();
       tc::fence_before_sync();
-      tc::named_sync(1u + (uint32_t)g, (uint32_t)R);
+      tc::named_sync(1u + (uint32_t)g, (uint32_t)T::GROUP_THREADS);
     };
     auto wait_mma = [&]() {
       ws::mbar_wait_t(bmma, phase);
@@ -160,14 +180,14 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
 #pragma unroll
       for (int k = 0; k < NL - 1; ++k) {
         const float* b = bias + TB::boff(k) / 4;
-        // all W columns in flight at once (one TMEM round trip)
-        float v[W];
+        // this part's WQ columns in flight at once (one TMEM round trip)
+        float v[WQ];
 #pragma unroll
-        for (int c16 = 0; c16 < W; c16 += 16) tc::tmem_ldn<16>(lad + tacc + (uint32_t)c16, v + c16);
+        for (int c16 = 0; c16 < WQ; c16 += 16) tc::tmem_ldn<16>(lad + tacc + (uint32_t)(h * WQ + c16), v + c16);
         tc::tmem_wait_ld();
-        const float4* b4 = reinterpret_cast<const float4*>(b);
+        const float4* b4 = reinterpret_cast<const float4*>(b + h * WQ);
 #pragma unroll
-        for (int j = 0; j < W / 4; ++j) {
+        for (int j = 0; j < WQ / 4; ++j) {
           const float4 bb = b4[j];
           v[4 * j] = fmaxf(v[4 * j] + bb.x, 0.0f);
           v[4 * j + 1] = fmaxf(v[4 * j + 1] + bb.y, 0.0f);
@@ -175,7 +195,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           v[4 * j + 3] = fmaxf(v[4 * j + 3] + bb.w, 0.0f);
         }
 #pragma unroll
-        for (int c8 = 0; c8 < W / 8; ++c8) tc::store_chunk(hh, hl, R, r, c8, v + 8 * c8);
+        for (int c8 = 0; c8 < WQ / 8; ++c8) tc::store_chunk(hh, hl, R, r, h * (WQ / 8) + c8, v + 8 * c8);
         handoff();
         QWS_STAMP(3 + 2 * k);
         if (gt == 0) {
@@ -187,28 +207,28 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
         wait_mma();
         QWS_STAMP(4 + 2 * k);
       }
-      // ---- Table 1 head, all K lobes of this row
-      float lp[K], kp[K], tp[K], pp[K];
-      tc::tmem_ldn<K>(lad + tacc, lp);
-      tc::tmem_ldn<K>(lad + tacc + (uint32_t)K, kp);
-      tc::tmem_ldn<K>(lad + tacc + (uint32_t)(2 * K), tp);
-      tc::tmem_ldn<K>(lad + tacc + (uint32_t)(3 * K), pp);
+      // ---- Table 1 head: lobes [h KQ, (h + 1) KQ) of this row
+      float lp[KQ], kp[KQ], tp[KQ], pp[KQ];
+      tc::tmem_ldn<KQ>(lad + tacc + (uint32_t)(h * KQ), lp);
+      tc::tmem_ldn<KQ>(lad + tacc + (uint32_t)(K + h * KQ), kp);
+      tc::tmem_ldn<KQ>(lad + tacc + (uint32_t)(2 * K + h * KQ), tp);
+      tc::tmem_ldn<KQ>(lad + tacc + (uint32_t)(3 * K + h * KQ), pp);
       tc::tmem_wait_ld();
       // the group's next layer-0 MMA overwrites these columns: every thread's
       // read first
       tc::fence_before_sync();
-      tc::named_sync(1u + (uint32_t)g, (uint32_t)R);
+      tc::named_sync(1u + (uint32_t)g, (uint32_t)T::GROUP_THREADS);
       QWS_STAMP(3 + 2 * (NL - 1));
 #ifdef NPM_QWS_NOHEAD   // measurement variant: no Table 1 head
       if (valid) a.spdf[i] = lp[0] + kp[1] + tp[2] + pp[3] + qx + u1 + u2 + u3 + qy + qz;
       continue;
 #endif
-      const float* b = bias + TB::boff(NL - 1) / 4;
-      float kap[K], mx[K], my[K], mz[K], nrm[K];
+      const float* b = bias + TB::boff(NL - 1) / 4 + h * KQ;
+      float kap[KQ], mx[KQ], my[KQ], mz[KQ], nrm[KQ];
       float M = -INFINITY;
       bool conc = false;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {   // branch-free over the lobes (they interleave)
+      for (int j = 0; j < KQ; ++j) {   // branch-free over the lobes (they interleave)
         lp[j] += b[j];
         tp[j] += b[2 * K + j];
         pp[j] += b[3 * K + j];
@@ -225,7 +245,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       // only in warps that have one
       if (__any_sync(0xffffffffu, conc)) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
+        for (int j = 0; j < KQ; ++j) {
           if (kap[j] > 1e3f) {
             float th, ph, st, ct, sp, cp;
             lobe_angles<true>(tp[j], pp[j], kap[j], th, ph, st, ct, sp, cp);
@@ -233,34 +253,66 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           }
         }
       }
-      float e[K], Ssum = 0.0f, P = 0.0f;
+      if constexpr (TPR == 2) {
+        red[h * R + r] = M;
+        psync();
+        M = fmaxf(red[r], red[R + r]);
+      }
+      float e[KQ], Ssum = 0.0f, P = 0.0f;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
+      for (int j = 0; j < KQ; ++j) {
         e[j] = __expf(lp[j] - M);
         Ssum += e[j];
         if (want_pdf) P += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], qx, qy, qz);
       }
-      const float invS = 1.0f / Ssum;
-      if (want_pdf && valid) a.pdf[i] = P * invS;
+      // part boundaries of the lobe CDF: B_h = sum of the earlier parts' e (C-A17)
+      float Bh = 0.0f, Bn = Ssum, invS;
+      if constexpr (TPR == 2) {
+        red[(2 + h) * R + r] = Ssum;
+        red[(4 + h) * R + r] = P;
+        psync();
+        const float S0 = red[2 * R + r], St = S0 + red[3 * R + r];
+        invS = 1.0f / St;
+        Bh = h ? S0 : 0.0f;
+        Bn = h ? St : S0;
+        P = red[4 * R + r] + red[5 * R + r];
+      } else {
+        invS = 1.0f / Ssum;
+      }
+      if (want_pdf && valid && h == 0) a.pdf[i] = P * invS;
       if (a.do_sample) {
-        // i* = min{i : u1 < C_i}, C_i = sum_{j<=i} lambda_j; K-1 if none (C-A17)
-        int sel = K - 1;
-        float cum = 0.0f;
+        // i* = min{i : u1 < C_i}, C_i = sum_{j<=i} lambda_j; K-1 if none (C-A17):
+        // the part whose range [B_h, B_h+1) holds u1 (the last part takes the rest)
+        const bool own = TPR == 1 || (u1 >= Bh * invS && (u1 < Bn * invS || h == TPR - 1));
+        float wx = 0.f, wy = 0.f, wz = 0.f;
+        if (own) {
+          int sel = KQ - 1;
+          float cum = Bh;
 #pragma unroll
-        for (int j = 0; j < K - 1; ++j) {
-          cum += e[j];
-          if (sel == K - 1 && u1 < cum * invS) sel = j;
+          for (int j = 0; j < KQ - 1; ++j) {
+            cum += e[j];
+            if (sel == KQ - 1 && u1 < cum * invS) sel = j;
+          }
+          float kk = kap[0], mmx = mx[0], mmy = my[0], mmz = mz[0];
+#pragma unroll
+          for (int j = 1; j < KQ; ++j)
+            if (sel == j) { kk = kap[j]; mmx = mx[j]; mmy = my[j]; mmz = mz[j]; }
+          lobe_sample(kk, mmx, mmy, mmz, u2, u3, wx, wy, wz);
+          if constexpr (TPR == 2) { red[6 * R + r] = wx; red[7 * R + r] = wy; red[8 * R + r] = wz; }
         }
-        float kk = kap[0], mmx = mx[0], mmy = my[0], mmz = mz[0];
-#pragma unroll
-        for (int j = 1; j < K; ++j)
-          if (sel == j) { kk = kap[j]; mmx = mx[j]; mmy = my[j]; mmz = mz[j]; }
-        float wx, wy, wz;
-        lobe_sample(kk, mmx, mmy, mmz, u2, u3, wx, wy, wz);
+        if constexpr (TPR == 2) {
+          psync();
+          wx = red[6 * R + r]; wy = red[7 * R + r]; wz = red[8 * R + r];
+        }
         float P2 = 0.0f;
 #pragma unroll
-        for (int j = 0; j < K; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
-        if (valid) {
+        for (int j = 0; j < KQ; ++j) P2 += e[j] * lobe_eval(nrm[j], kap[j], mx[j], my[j], mz[j], wx, wy, wz);
+        if constexpr (TPR == 2) {
+          red[(9 + h) * R + r] = P2;
+          psync();
+          P2 = red[9 * R + r] + red[10 * R + r];
+        }
+        if (valid && h == 0) {
           a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
           a.spdf[i] = P2 * invS;
         }
@@ -327,21 +379,21 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           ex[0] = u.x; ex[1] = u.y; ex[2] = u.z;
         }
       }
+      // branch-free over the levels (an invalid row gathers at the AABB corner
+      // and is zeroed), so the compiler can overlap one level's loads with the
+      // previous level's blend
       float gf[4 * LP];
 #pragma unroll
       for (int q = 0; q < LP; ++q) {
         float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
-#ifdef NPM_QWS_NOGATHER   // measurement variant: no grid gathers
-        if (false) {
-#else
-        if (valid) {
+#ifndef NPM_QWS_NOGATHER   // measurement variant: no grid gathers
+        const int l = part * LP + q;
+        LevelCorners lc;
+        level_corners(a.grid, l, ux, uy, uz, lc);
+        gl = gather_level<false>(tab, a.grid.off[l], lc);
 #endif
-          const int l = part * LP + q;
-          LevelCorners lc;
-          level_corners(a.grid, l, ux, uy, uz, lc);
-          gl = gather_level<false>(tab, a.grid.off[l], lc);
-        }
-        gf[4 * q] = gl.x; gf[4 * q + 1] = gl.y; gf[4 * q + 2] = gl.z; gf[4 * q + 3] = gl.w;
+        gf[4 * q] = valid ? gl.x : 0.0f; gf[4 * q + 1] = valid ? gl.y : 0.0f;
+        gf[4 * q + 2] = valid ? gl.z : 0.0f; gf[4 * q + 3] = valid ? gl.w : 0.0f;
       }
       QWS_MSTAMP(1);
       ws::mbar_wait_idle(bar_x0e + s, (uint32_t)(((kt / S) & 1) ^ 1));
