@@ -41,7 +41,7 @@ struct QW {
   static constexpr int KIN = B::KIN;
   static_assert(!N::PRODUCT && K == 8 && KIN == NIN && L % 4 == 0 && W % 16 == 0, "query_ws shape");
 #ifdef NPM_QWS_MP   // measurement override (4: B200 c2 233 us vs 229 us with 2)
-  static constexpr int MP = NPM_QWS_MP;
+  static constexpr int MP = L >= 4 * NPM_QWS_MP ? NPM_QWS_MP : 2;
 #else
   static constexpr int MP = 2;
 #endif
@@ -58,10 +58,11 @@ struct QW {
   static constexpr int GROUPS = 2, GROUP_THREADS = TPR * R, CHAIN_THREADS = GROUPS * GROUP_THREADS;
   static constexpr int MEM_THREADS = MP * R;
   // MP = 4 register split (setmaxnreg moves registers only within the CTA's
-  // launch allocation, 768 x 80): 256 x 112 + 512 x 64 = 768 x 80 (the chain
-  // code needs 92)
-  static constexpr int CHAIN_REGS = 112, MEM_REGS = 64, LAUNCH_REGS = 80;
+  // launch allocation): TPR 1: 256 x 112 + 512 x 64 = 768 x 80; TPR 2:
+  // 512 x 80 + 512 x 48 = 1024 x 64
   static constexpr int THREADS = CHAIN_THREADS + MEM_THREADS;
+  static constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;
+  static constexpr int CHAIN_REGS = TPR == 2 ? 80 : 112, MEM_REGS = TPR == 2 ? 48 : 64;
   static_assert(MP != 4 || CHAIN_THREADS * CHAIN_REGS + MEM_THREADS * MEM_REGS <= THREADS * LAUNCH_REGS, "regs");
   static constexpr int RDF = 8;   // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u
   static constexpr uint32_t X0_BYTES = 2u * (KIN / 8) * CHR;
