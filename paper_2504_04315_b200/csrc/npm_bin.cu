@@ -18,6 +18,8 @@
 // inside one chunk's window (~44 MB of SoA I/O at 2^20 queries), which the
 // 126 MB L2 merges before write-back.  Measured on B200 (c3, 8.4 M queries):
 // one global sort made the query kernel 44 % slower per query than at c2.
+#include <cstdlib>
+
 #include "npm_kernels.cuh"
 
 namespace npm {
@@ -190,13 +192,26 @@ int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int
   if (sort_chunk >= n) sort_chunk = n;
   const int nb = bin_hist_entries(n, sort_chunk) / 3;
   cudaMemsetAsync(hist, 0, (size_t)2 * nb * sizeof(uint32_t), st);   // counts + cursors
+  // samples per CTA: small spans (short per-thread loops of dependent loads and
+  // smem atomics, many CTAs in flight) against the per-CTA fixed cost of
+  // scanning / flushing the 4096-bin row (B200 c2, one sort: 4096 per CTA
+  // 33 us, 2048 41 us, 1024 50 us).  NPM_BIN_SPAN (measurement knob): samples
+  // per CTA, a power of two >= 512.
+  static int64_t knob = -1;
+  if (knob < 0) {
+    const char* e = getenv("NPM_BIN_SPAN");
+    knob = e ? atoll(e) : 0;
+  }
+  const int64_t per = knob >= 512 ? knob : 4096;
   int64_t span;
   if (sort_chunk == n) {   // one sort over the whole batch
-    const int64_t want = (n + 4095) / 4096;
-    const int blocks = (int)(want < (int64_t)sms * 2 ? want : (int64_t)sms * 2);
+    const int64_t want = (n + per - 1) / per;
+    const int64_t cap = knob >= 512 ? want : (int64_t)sms * 2;
+    const int blocks = (int)(want < cap ? want : cap);
     span = (n + blocks - 1) / blocks;
   } else {                 // chunks of sort_chunk; CTA spans never straddle a chunk
-    span = sort_chunk / 32;
+    // sort_chunk / 128 = 8192 samples (B200 c3 bin 130 -> 106 us; / 256: 120 us)
+    span = knob >= 512 && sort_chunk % knob == 0 ? knob : sort_chunk / 128;
   }
   const int blocks = (int)((n + span - 1) / span);
   bin_count_kernel<<<blocks, kThreads, 0, st>>>(px, py, pz, n, span, sort_chunk, g, keys, hist);
