@@ -17,10 +17,11 @@ RGB targets are reduced by luminance 0.2126/0.7152/0.0722 (C-A11).
 from dataclasses import dataclass, field
 import numpy as np
 
-from . import grid, mlp, sh, vmf, adam
+from . import grid, mlp, sh, vmf, adam, variance
 
 RADIANCE, PRODUCT = 0, 1
 KL, CHI2 = 0, 1   # training divergence (f-4; "Other divergence metrics are also available")
+VARIANCE_AWARE = 2   # f-4: KL to the second moment, V^2 / int V^2 (reading C-A35; oracle/variance.py)
 LUMA = np.array([0.2126, 0.7152, 0.0722])
 
 
@@ -230,6 +231,18 @@ def gradient(cfg, flat, q, wi, target, sample_pdf, n_global, bsdf_pdf=None):
         ggrads = grid.scatter_grad(q['x'], cfg.aabb_lo, cfg.aabb_hi, cfg.resolutions, cfg.table_sizes,
                                    dz[:gl], cfg.n_features)
         stats = dict(loss_proxy=float((-s * chi).sum()), n_used=int((~dropped & ~zero).sum()),
+                     n_zero_target=int(zero.sum()), n_dropped=int(dropped.sum()))
+        return pack(cfg, mgrads, ggrads, _alpha_block(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf,
+                                                      ~dropped & ~zero, n_global, stats)), stats
+    if cfg.divergence == VARIANCE_AWARE:
+        # f-4 (C-A35): l_n = (a_n / N)(-2 log V(w_n) + log int V^2), a_n = D^_n^2 / p~_n
+        draw, proxy = variance.variance_aware_head(raw, wi, t, np.asarray(sample_pdf, np.float64), n_global,
+                                                   dropped, zero, cfg.n_lobes, cfg.kappa_min, cfg.kappa_max)
+        mgrads, dz = mlp.backward(layers, pres, inputs, draw)
+        gl = cfg.n_levels * cfg.n_features
+        ggrads = grid.scatter_grad(q['x'], cfg.aabb_lo, cfg.aabb_hi, cfg.resolutions, cfg.table_sizes,
+                                   dz[:gl], cfg.n_features)
+        stats = dict(loss_proxy=proxy, n_used=int((~dropped & ~zero).sum()),
                      n_zero_target=int(zero.sum()), n_dropped=int(dropped.sum()))
         return pack(cfg, mgrads, ggrads, _alpha_block(cfg, flat, q, wi, t, sample_pdf, bsdf_pdf,
                                                       ~dropped & ~zero, n_global, stats)), stats
