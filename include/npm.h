@@ -118,7 +118,13 @@ typedef struct {
   float kappa_min, kappa_max;/* clamp of kappa = exp(kappa') (C-A8): 1e-5, 1e5 */
   uint64_t init_seed;        /* parameter initialisation seed (C-A21) */
   int32_t divergence;        /* training objective: 0 = KL (Eq. 8/9), 1 = Pearson chi^2
-                                (f-4; "other divergence metrics", C-A31) */
+                                (f-4; "other divergence metrics", C-A31), 2 = the
+                                variance-aware target (f-4; "(2) the improved
+                                variance-aware target distribution ... could be learned",
+                                reading C-A35): KL from the normalised second moment of the
+                                estimate to V^2 / int V^2, per record (D^^2/p~/N)(-2 log V +
+                                log int V^2), so that V ~ sqrt(E[D^^2]); radiance shapes
+                                with K = 8, exclusive with learn_alpha */
   int32_t learn_alpha;       /* 1: learn the BSDF selection probability (f-4'; "(1) the
                                 BSDF selection probability could also be learned by our
                                 network", reading C-A34): alpha(x) = sigmoid(a . h_{L-1} + c),

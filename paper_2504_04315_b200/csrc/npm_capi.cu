@@ -600,7 +600,12 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   if (c.base_res < 2 || c.max_res < c.base_res || (c.n_levels > 1 && c.max_res <= c.base_res))
     return fail(NPM_ERR_INVALID, "need 2 <= D_1 < D_L");
   if (c.log2_hashmap < 0 || c.log2_hashmap > 30) return fail(NPM_ERR_INVALID, "log2_hashmap out of range");
-  if (c.divergence != 0 && c.divergence != 1) return fail(NPM_ERR_INVALID, "divergence must be 0 (KL) or 1 (chi^2)");
+  if (c.divergence < 0 || c.divergence > 2)
+    return fail(NPM_ERR_INVALID, "divergence must be 0 (KL), 1 (chi^2) or 2 (variance-aware target)");
+  if (c.divergence == 2 && (c.mode != NPM_RADIANCE || c.n_lobes != 8))
+    return fail(NPM_ERR_INVALID, "variance-aware target: radiance-mode shapes with K = 8 only");
+  if (c.divergence == 2 && c.learn_alpha)
+    return fail(NPM_ERR_INVALID, "variance-aware target and learn_alpha are exclusive");
   if (c.learn_alpha != 0 && c.learn_alpha != 1) return fail(NPM_ERR_INVALID, "learn_alpha must be 0 or 1");
   if (c.learn_alpha && (c.mode != NPM_RADIANCE || c.n_lobes != 8))
     return fail(NPM_ERR_INVALID, "learn_alpha: radiance-mode shapes with K = 8 only");
@@ -683,7 +688,7 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // product shape (no warp-specialised instantiation).
   m->train_ws = (m->bin_train || c.mode == NPM_PRODUCT) ? 0 : 1;
   if (const char* e = getenv("NPM_TRAIN_WS")) m->train_ws = atoi(e);
-  if (c.learn_alpha) m->train_ws = 1;   // the selection head lives in the warp-specialised kernel
+  if (c.learn_alpha || c.divergence == 2) m->train_ws = 1;   // (C-A34 / C-A35 live in the warp-specialised kernel)
   // Privatise the scatter of small (coarse) levels when training batches are
   // binned: coherent records then add to the same few coarse entries from
   // every SM and the reductions queue on the same L2 lines.  Each SM

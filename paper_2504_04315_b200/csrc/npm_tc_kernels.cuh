@@ -1193,20 +1193,25 @@ struct TcLaunch {
         if (!a.wimg || a.wimg_bytes < ws::WS<N>::WIMG) return -1;
         if (a.alpha_w && (!a.alpha_g || !a.bsdf_pdf)) return -1;
         ws::prep_wimg_kernel<N><<<8, 256, 0, st>>>(a.params, a.wimg);
-        auto go = [&](auto AHC) {
-          constexpr bool AH = decltype(AHC)::value;
-          using T = ws::WS<N, AH>;
-          cudaFuncSetAttribute(ws::train_ws_kernel<N, AH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
+        auto go = [&](auto AHC, auto VAC) {
+          constexpr bool AH = decltype(AHC)::value, VA = decltype(VAC)::value;
+          using T = ws::WS<N, AH, VA>;
+          cudaFuncSetAttribute(ws::train_ws_kernel<N, AH, VA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)T::SMEM);
           const int64_t ntiles = (a.n + T::R - 1) / T::R;
           const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
-          ws::train_ws_kernel<N, AH><<<blocks, T::THREADS, T::SMEM, st>>>(a);
+          ws::train_ws_kernel<N, AH, VA><<<blocks, T::THREADS, T::SMEM, st>>>(a);
         };
-        if (a.alpha_w) go(std::true_type{});
-        else go(std::false_type{});
+        if (a.alpha_w && a.divergence == 2) return -1;   // one of the two per launch
+        if (a.alpha_w) go(std::true_type{}, std::false_type{});
+        else if (a.divergence == 2) go(std::false_type{}, std::true_type{});
+        else go(std::false_type{}, std::false_type{});
         return 2;
       }
     }
-    if (a.alpha_w) return -1;   // the C-A34 head is trained by the warp-specialised kernel only
+    // the C-A34 head and the variance-aware target (C-A35) are trained by the
+    // warp-specialised kernel only
+    if (a.alpha_w || a.divergence == 2) return -1;
     // two 64-sample tiles per CTA (tc_train64_kernel)
     using T64 = TC64<N>;
     cudaFuncSetAttribute(tc_train64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T64::SMEM);

@@ -34,7 +34,7 @@ namespace ws {
 #define NPM_WS_PAIRS true
 #endif
 
-template <class N, bool AH = false>
+template <class N, bool AH = false, bool VA = false>
 struct WS {
   using B = TC<N>;
   static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN, L = N::L, K = N::K, NG = N::NGRID;
@@ -60,6 +60,9 @@ struct WS {
   static constexpr int XC = AH ? 8 : 0, XD = AH ? 16 : 0;
   static constexpr uint32_t D_BYTES = 2u * ((NOUT + XC) / 8) * CHR;
   static constexpr uint32_t AH_BYTES = AH ? 4u * (W + 4) : 0u;
+  // VA (f-4 variance-aware target, C-A35): every lobe's (kappa, mu, e) of the
+  // row for the pairwise terms of int V^2, [5 K][R] f32
+  static constexpr uint32_t VX_BYTES = VA ? 5u * K * R * 4u : 0u;
   // row data [RDF][R] f32: slots 3 valid | 4-6 w_i | 7-9 target | 10 pdf |
   // 11 p_bsdf (AH).  It also carries the head's exchange between the row's two
   // threads (no separate buffer: the 164 KB carve-out leaves L1 92 KB -- the
@@ -93,7 +96,8 @@ struct WS {
   static constexpr uint32_t OFF_DZ = OFF_RD + (uint32_t)S0 * RD_BYTES;
   // C-A34 selection head: its parameters (a [W], c)
   static constexpr uint32_t OFF_AH = (OFF_DZ + DZ_BYTES + 15u) & ~15u;
-  static constexpr uint32_t OFF_BAR = OFF_AH + AH_BYTES;
+  static constexpr uint32_t OFF_VX = OFF_AH + AH_BYTES;
+  static constexpr uint32_t OFF_BAR = OFF_VX + VX_BYTES;
   // mbarriers: [0] weights, [1] mma, [2] dz full, [3] dz empty, [4..4+S0) x0 full, [4+S0..4+2 S0) x0 empty,
   // [4+2 S0] head start (the scatter of tile k-1 waits for tile k's head)
   static constexpr int NBAR = 5 + 2 * S0;
@@ -219,11 +223,12 @@ __global__ void __launch_bounds__(256) prep_wimg_kernel(const float* __restrict_
   }
 }
 
-// AH: the C-A34 selection head is trained (a learn_alpha model); a separate
-// instantiation so the plain kernel carries none of its code
-template <class N, bool AH>
-__global__ void __launch_bounds__(WS<N, AH>::THREADS, 1) train_ws_kernel(TrainArgs a) {
-  using T = WS<N, AH>;
+// AH: the C-A34 selection head is trained (a learn_alpha model); VA: the
+// variance-aware target (divergence 2, C-A35).  Separate instantiations so the
+// plain kernel carries none of their code.
+template <class N, bool AH, bool VA>
+__global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(TrainArgs a) {
+  using T = WS<N, AH, VA>;
   using TB = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W, NOUT = N::NOUT, L = N::L, NG = N::NGRID, NIN = N::NIN;
   constexpr int R = T::R;
@@ -452,6 +457,18 @@ __global__ void __launch_bounds__(WS<N, AH>::THREADS, 1) train_ws_kernel(TrainAr
           }
           rd[(4 + 2 * h) * R + r] = S;
           rd[(5 + 2 * h) * R + r] = P;
+          float* vx = reinterpret_cast<float*>(smem + T::OFF_VX);
+          if constexpr (VA) {   // this part's lobes for the pairwise terms (read after the barrier)
+#pragma unroll
+            for (int m = 0; m < KH; ++m) {
+              const int j = h * KH + m;
+              vx[(5 * j) * R + r] = kap[m];
+              vx[(5 * j + 1) * R + r] = mx[m];
+              vx[(5 * j + 2) * R + r] = my[m];
+              vx[(5 * j + 3) * R + r] = mz[m];
+              vx[(5 * j + 4) * R + r] = e[m];
+            }
+          }
           psync();
           NPM_WS_STAMP(14);
           // the same association order on every thread of the row: parts 0, 1, ...
@@ -460,24 +477,96 @@ __global__ void __launch_bounds__(WS<N, AH>::THREADS, 1) train_ws_kernel(TrainAr
           const float Vb = fmaxf(Pt * invS, kVFloor);
           const float invV = 1.0f / Vb;
           // f-4 (C-A31): chi^2 scales Eq. 9's record weight by D^ / V
-          const float chi = a.divergence ? (use ? t * invV : 0.0f) : 1.0f;
-          const float sd = s_ * chi;
+          const float chi = a.divergence == 1 ? (use ? t * invV : 0.0f) : 1.0f;
+          // f-4 (C-A35): the variance-aware target weighs -2 log V by a = D^^2 / p~
+          const float a_n = use ? ratio * t : 0.0f;
+          const float sd = VA ? (use ? (float)(-2.0 * (double)a_n * a.inv_n_global) : 0.0f) : s_ * chi;
+          const float wzn = VA && use ? (float)((double)a_n * a.inv_n_global) : 0.0f;
+          // d log Z / d (lambda', kappa', theta', phi') of this part's lobes, Z = int V^2
+          float zl[KH], zk[KH], zt[KH], zp[KH];
+          float logZ = 0.0f;
+          if constexpr (VA) {
+            // pairwise closed form (C-A35): I_ij = C_i C_j / C(r_ij) e^{r_ij - k_i - k_j}
+            // = C_i C_j 2 pi (1 - e^{-2r}) / r e^{r - k_i - k_j} with
+            // r - k_i - k_j = -k_i k_j |mu_i - mu_j|^2 / (r + k_i + k_j) (no cancellation);
+            // Langevin(r) / r from the same 1 - e^{-2r} (series below r = 1/2)
+            auto cnorm = [](float k) {   // C(k) 2 pi = k / (1 - e^{-2k}), -> 1/2 at 0
+              const float kk = fmaxf(k, 1e-30f);
+              return __fdividef(kk, one_minus_exp_neg(2.0f * kk));
+            };
+            auto lox_from = [](float x, float om, float inv_x) {   // (coth x - 1/x) / x, om = 1 - e^{-2x}
+              const float x2 = x * x;
+              const float ser = 0.33333334f - x2 * (0.022222223f - x2 * (0.0021164022f - x2 * 0.00021164022f));
+              return x < 0.5f ? ser : (__fdividef(2.0f, om) - 1.0f - inv_x) * inv_x;
+            };
+            float A[KH], Bk[KH], Bx[KH], By[KH], Bz[KH], Ck[KH];
+#pragma unroll
+            for (int m = 0; m < KH; ++m) {
+              A[m] = Bk[m] = Bx[m] = By[m] = Bz[m] = 0.0f;
+              Ck[m] = cnorm(kap[m]) * 0.15915494f;   // C(k_i) 2 pi * C(k_j) 2 pi / (2 pi)
+            }
+#pragma unroll 2
+            for (int j = 0; j < K; ++j) {
+              const float kj = vx[(5 * j) * R + r], jx = vx[(5 * j + 1) * R + r], jy = vx[(5 * j + 2) * R + r],
+                          jz = vx[(5 * j + 3) * R + r], ej = vx[(5 * j + 4) * R + r];
+              const float Cj = ej * cnorm(kj);
+#pragma unroll
+              for (int m = 0; m < KH; ++m) {
+                const float dx = mx[m] - jx, dy = my[m] - jy, dz = mz[m] - jz;
+                const float d2 = dx * dx + dy * dy + dz * dz;
+                const float sk = kap[m] + kj, pk = kap[m] * kj;
+                const float rr = fmaxf(sqrtf(fmaxf(sk * sk - pk * d2, 0.0f)), 1e-30f);
+                const float ex = -__fdividef(pk * d2, rr + sk);
+                const float om = one_minus_exp_neg(2.0f * rr);
+                const float inv_r = __fdividef(1.0f, rr);
+                const float wI = Ck[m] * Cj * om * inv_r * __expf(ex);   // e_j I_ij
+                A[m] += wI;
+                const float q = wI * lox_from(rr, om, inv_r);
+                Bk[m] += q * (kap[m] + kj * (1.0f - 0.5f * d2));
+                Bx[m] += q * kj * jx; By[m] += q * kj * jy; Bz[m] += q * kj * jz;
+              }
+            }
+            float Zh = 0.0f;
+#pragma unroll
+            for (int m = 0; m < KH; ++m) Zh += e[m] * A[m];
+            rd[h * R + r] = Zh;   // rows 0 / 1 (the maxima) are dead after the second barrier
+            psync();
+            const float Zs = 0.0f + rd[r] + rd[R + r];   // sum_ij e_i e_j I_ij = Z S^2
+            const float invZs = 1.0f / Zs;
+            logZ = __logf(Zs * invS * invS);
+#pragma unroll
+            for (int m = 0; m < KH; ++m) {
+              const float gi = e[m] * A[m] * invZs;            // sum_j G_ij
+              const float lam = e[m] * invS;
+              const float f = 2.0f * e[m] * invZs;
+              zl[m] = 2.0f * (gi - lam);
+              const float omk = one_minus_exp_neg(2.0f * kap[m]), ik = __fdividef(1.0f, kap[m]);
+              const float dkz = -2.0f * kap[m] * lox_from(kap[m], omk, ik) * gi + f * Bk[m];
+              zk[m] = (kp[m] < a.log_kmin || kp[m] > a.log_kmax) ? 0.0f : kap[m] * dkz;
+              const float gx = f * kap[m] * Bx[m], gy = f * kap[m] * By[m], gz = f * kap[m] * Bz[m];
+              zt[m] = kPi * (cth[m] * cph[m] * gx + cth[m] * sph[m] * gy - sth[m] * gz) * th[m] * (1.0f - th[m]);
+              zp[m] = kTwoPi * (-sth[m] * sph[m] * gx + sth[m] * cph[m] * gy) * ph[m] * (1.0f - ph[m]);
+            }
+          }
           float dl[KH], dk[KH], dt[KH], dp[KH];
 #pragma unroll
           for (int m = 0; m < KH; ++m) {
             const float lam = e[m] * invS;
             const float gam = lam * vv[m] * invV;
             dl[m] = sd * (gam - lam);
+            if constexpr (VA) dl[m] += wzn * zl[m];
             const float dx = mx[m] - wx, dy = my[m] - wy, dz = mz[m] - wz;
             const float d2 = dx * dx + dy * dy + dz * dz;
             // 2 kappa e^{-2 kappa} / (1 - e^{-2 kappa}) with em = 1 - e^{-2 kappa}
             const float dkk = sd * gam * (1.0f - kap[m] * 0.5f * d2 - __fdividef(2.0f * kap[m] * (1.0f - emk[m]), emk[m]));
             dk[m] = (kp[m] < a.log_kmin || kp[m] > a.log_kmax) ? 0.0f : dkk;   // C-A8
+            if constexpr (VA) dk[m] += wzn * zk[m];
             const float wdth = kPi * (cth[m] * cph[m] * wx + cth[m] * sph[m] * wy - sth[m] * wz);
             const float wdph = kTwoPi * (-sth[m] * sph[m] * wx + sth[m] * cph[m] * wy);
             const float sgk = sd * gam * kap[m];
             dt[m] = sgk * wdth * th[m] * (1.0f - th[m]);
             dp[m] = sgk * wdph * ph[m] * (1.0f - ph[m]);
+            if constexpr (VA) { dt[m] += wzn * zt[m]; dp[m] += wzn * zp[m]; }
           }
           const uint32_t dh = sb + T::OFF_D, dlo = dh + (T::dfeat(NL - 1) / 8) * CHR;
           tc::store_feats<KH>(dh, dlo, R, r, h * KH, dl);
@@ -510,7 +599,8 @@ __global__ void __launch_bounds__(WS<N, AH>::THREADS, 1) train_ws_kernel(TrainAr
           if (h == 0) {
             c_drop += drop; c_zero += zero;
             if (use) {
-              loss += a.divergence ? -(double)sd : (double)s_ * (double)logf(Vb);   // chi^2: (D^/p~)(D^/V)/N
+              if constexpr (VA) loss += (double)wzn * (-2.0 * (double)logf(Vb) + (double)logZ);
+              else loss += a.divergence ? -(double)sd : (double)s_ * (double)logf(Vb);   // chi^2: (D^/p~)(D^/V)/N
               c_used += 1;
             }
           }

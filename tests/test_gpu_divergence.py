@@ -65,4 +65,4 @@ def test_chi2_training_descends():
 
 def test_bad_divergence_rejected():
     with pytest.raises(npm.NpmError):
-        npm.Model(0, **dict(CONFIGS["c1"]["model"], divergence=2))
+        npm.Model(0, **dict(CONFIGS["c1"]["model"], divergence=3))

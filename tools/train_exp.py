@@ -1,7 +1,7 @@
 """Measurement experiment (not part of the product): time the fused training
 kernel at c2 under different record orders / knobs, to see what the grid
 stage costs.  Usage: python tools/train_exp.py <variant>  (prints one line).
-Variants: shuffled, alpha (a learn_alpha model), sorted (records Morton-sorted on the host by their
+Variants: shuffled, alpha (a learn_alpha model), va (the variance-aware target), sorted (records Morton-sorted on the host by their
 finest-level cell), and the env knobs NPM_DEBUG (bit 0: skip the scatter),
 NPM_BIN_TRAIN, NPM_PRIV set by the caller."""
 import os
@@ -34,7 +34,8 @@ def main():
     cfg = CONFIGS[name]
     n = cfg["n"]
     alpha = variant == "alpha"     # learn_alpha model (f-4', C-A34): the selection head's cost
-    m = npm.Model(0, learn_alpha=int(alpha), **cfg["model"])
+    model = dict(cfg["model"], divergence=2) if variant == "va" else cfg["model"]   # C-A35
+    m = npm.Model(0, learn_alpha=int(alpha), **model)
     tb = synth.training_batch(n, seed=200)
     if variant == "sorted":
         o = morton_order(tb["x"])
