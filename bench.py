@@ -365,6 +365,32 @@ def main():
                                                            True, cw[0], cw[1], cw[2], cp, wq[0], wq[1], wq[2], pq_,
                                                            stream=stream))
     f2 = {"cosine_product_sample_plus_pdf_ms": t_cos, "queries_per_s": n / (t_cos / 1e3), "kappa_c": 2.1438}
+    # ---- f-4 context (c2 shape): one training step (Eq. 9 kernel + Adam) per objective on
+    # the same records and parameters: KL (the bench's), Pearson chi^2 (C-A31), the
+    # variance-aware target (C-A35) and KL + the learned selection probability (C-A34)
+    f4 = None
+    if name in ("c2", "c1") and world == 1:
+        try:
+            wsq = (twi * T(tb["nrm"])).sum(0).clamp_min(0) / np.pi   # the records' stand-in BSDF pdf (C-A24)
+            p0 = m.get(npm.BUF_PARAMS)
+            f4 = {}
+            for key, kw in (("kl", {}), ("chi2", {"divergence": 1}), ("variance_aware", {"divergence": 2}),
+                            ("learned_alpha", {"learn_alpha": 1})):
+                m4 = npm.Model(local, **dict(cfg["model"], **kw))
+                if "learn_alpha" in kw:
+                    pf = torch.zeros(m4.n_params, device=dev)
+                    pf[:p0.numel()] = p0
+                    m4.set(npm.BUF_PARAMS, pf)
+                    q4 = m4.query(tx, bsdf_pdf=wsq)
+                else:
+                    m4.set(npm.BUF_PARAMS, p0)
+                    q4 = m4.query(tx)
+                t4 = timed_ms(lambda: (m4.accumulate_grads(q4, twi, ttg, tpd, want_stats=False),
+                                       m4.optimizer_step(False)))
+                f4[key] = {"train_step_ms": t4, "records_per_s": n / (t4 / 1e3)}
+                m4.close()
+        except Exception as exc:   # context only; never fail the bench line on it
+            f4 = {"error": str(exc)}
     f1 = {"combined_sample_ms": t_comb, "combined_sample_queries_per_s": n / (t_comb / 1e3), "alpha": 0.5,
           "unwind_ms": t_unw, "unwind_records_per_s": Dp * npaths / (t_unw / 1e3),
           "unwind_bytes_per_record": 4 * (3 + 3 + 1 + 1 + 3) + 4 / Dp,
@@ -579,7 +605,8 @@ def main():
                 "roofline": roof, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in prof.items() if v[0]},
                 "clocks": clk.summary(), "cpu_baseline": cpu, "strong_c3": strong, "paper_context": paper_ctx,
                 "f1_guided_mis": f1,
-                "f2_cosine_product": f2}
+                "f2_cosine_product": f2,
+                "f4_objectives": f4}
         print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
