@@ -85,12 +85,15 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 // <L_i(x_{v+1})>, backward along each path; a successor
 // with p~ <= 0 or non-finite ends the path (C-A27); v >= depth -> 0.
 // D^ = <L_i> (radiance) or f_s <L_i> cos (product, Eq. 12).  Thread per path;
-// every [.][v][n] access is coalesced over paths.  For D <= MAXD all of a
-// path's inputs are loaded into registers before the (sequential) recurrence,
-// so the loads of all vertices are in flight at once (a path batch has few
-// threads: n = records / D).
+// every [.][v][n] access is coalesced over paths.  For D <= MAXD a path's
+// cos / pdf and then each channel's le / fs are loaded into registers before
+// the (sequential) recurrence, so the loads of all vertices are in flight at
+// once (a path batch has few threads: n = records / D).  128-thread CTAs,
+// >= 7 per SM (<= 72 registers): a c2 frame (115,200 8-vertex paths) runs as
+// one wave of one path per thread (the all-channels-at-once form took 255
+// registers for MAXD = 8: one CTA per SM, three grid-stride rounds, 26.6 us).
 template <int MAXD>
-__global__ void __launch_bounds__(256) unwind_kernel(UnwindArgs a) {
+__global__ void __launch_bounds__(128, 7) unwind_kernel(UnwindArgs a) {
   const int64_t n = a.n;
   const int D = a.max_depth, C = a.channels;
   const float* __restrict__ le = a.le;
@@ -100,34 +103,37 @@ __global__ void __launch_bounds__(256) unwind_kernel(UnwindArgs a) {
   float* __restrict__ out = a.target;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int d = min(max(__ldg(a.depth + p), 0), D);
-    float L[3][MAXD], F[3][MAXD], cs[MAXD], pd[MAXD];
+    // the path's cos / pdf, then one channel at a time (its le / fs loads all
+    // in flight; 2 x MAXD + 2 x MAXD values in registers instead of 8 x MAXD)
+    float cs[MAXD], pd[MAXD];
 #pragma unroll
     for (int v = 0; v < MAXD; ++v) {
       const int64_t at = (int64_t)v * n + p;
       const bool in = v < d;
       cs[v] = in ? __ldg(cosv + at) : 0.0f;
       pd[v] = in ? __ldg(pdf + at) : 0.0f;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const bool inc = in && c < C;
-        L[c][v] = inc ? __ldg(le + (int64_t)c * D * n + at) : 0.0f;
-        F[c][v] = inc ? __ldg(fs + (int64_t)c * D * n + at) : 0.0f;
-      }
     }
-    float li[3] = {0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int c = 0; c < C; ++c) {
+      float L[MAXD], F[MAXD];
 #pragma unroll
-    for (int v = MAXD - 1; v >= 0; --v) {
-      if (v >= D) continue;
-      const int64_t at = (int64_t)v * n + p;
-      const float q = v + 1 < MAXD ? pd[v + 1 < MAXD ? v + 1 : v] : 0.0f;   // p~ at the successor
-      const bool cont = v + 1 < d && isfinite(q) && q > 0.0f;
+      for (int v = 0; v < MAXD; ++v) {
+        const int64_t at = (int64_t)c * D * n + (int64_t)v * n + p;
+        const bool in = v < d;
+        L[v] = in ? __ldg(le + at) : 0.0f;
+        F[v] = in ? __ldg(fs + at) : 0.0f;
+      }
+      float li = 0.0f;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (c >= C) continue;
-        float acc = L[c][v];
-        if (cont) acc += __fdiv_rn(F[c][v + 1 < MAXD ? v + 1 : v] * cs[v + 1 < MAXD ? v + 1 : v], q) * li[c];
-        li[c] = v < d ? acc : 0.0f;
-        out[(int64_t)c * D * n + at] = a.product ? F[c][v] * li[c] * cs[v] : li[c];
+      for (int v = MAXD - 1; v >= 0; --v) {
+        if (v >= D) continue;
+        const int vn = v + 1 < MAXD ? v + 1 : v;
+        const float q = v + 1 < MAXD ? pd[vn] : 0.0f;   // p~ at the successor
+        const bool cont = v + 1 < d && isfinite(q) && q > 0.0f;
+        float acc = L[v];
+        if (cont) acc += __fdiv_rn(F[vn] * cs[vn], q) * li;
+        li = v < d ? acc : 0.0f;
+        out[(int64_t)c * D * n + (int64_t)v * n + p] = a.product ? F[v] * li * cs[v] : li;
       }
     }
   }
@@ -291,12 +297,17 @@ int launch_fold_priv(const FoldArgs& a, int sms, cudaStream_t st) {
 
 int launch_unwind(const UnwindArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0 || a.max_depth == 0) return 0;
-  const int64_t need = (a.n + 255) / 256;
-  const int blocks = (int)(need < (int64_t)sms * 8 ? need : (int64_t)sms * 8);
-  if (a.max_depth <= 4) unwind_kernel<4><<<blocks, 256, 0, st>>>(a);
-  else if (a.max_depth <= 8) unwind_kernel<8><<<blocks, 256, 0, st>>>(a);
-  else if (a.max_depth <= 16) unwind_kernel<16><<<blocks, 256, 0, st>>>(a);
-  else unwind_long_kernel<<<blocks, 256, 0, st>>>(a);
+  if (a.max_depth > 16) {
+    const int64_t need = (a.n + 255) / 256;
+    const int blocks = (int)(need < (int64_t)sms * 8 ? need : (int64_t)sms * 8);
+    unwind_long_kernel<<<blocks, 256, 0, st>>>(a);
+    return 1;
+  }
+  const int64_t need = (a.n + 127) / 128;
+  const int blocks = (int)(need < (int64_t)sms * 7 ? need : (int64_t)sms * 7);   // one wave
+  if (a.max_depth <= 4) unwind_kernel<4><<<blocks, 128, 0, st>>>(a);
+  else if (a.max_depth <= 8) unwind_kernel<8><<<blocks, 128, 0, st>>>(a);
+  else unwind_kernel<16><<<blocks, 128, 0, st>>>(a);
   return 1;
 }
 
