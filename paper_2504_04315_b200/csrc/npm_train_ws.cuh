@@ -100,7 +100,7 @@ struct WS {
   static constexpr uint32_t OFF_BAR = OFF_VX + VX_BYTES;
   // mbarriers: [0] weights, [1] mma, [2] dz full, [3] dz empty, [4..4+S0) x0 full, [4+S0..4+2 S0) x0 empty,
   // [4+2 S0] head start (the scatter of tile k-1 waits for tile k's head)
-  static constexpr int NBAR = 5 + 2 * S0;
+  static constexpr int NBAR = 6 + 2 * S0;   // + [5 + 2 S0]: the backward dW^T batches (second issuer)
   static constexpr uint32_t OFF_TSLOT = OFF_BAR + 8u * NBAR;
 #ifndef NPM_WS_SMEM_PAD   // measurement knob: extra dynamic smem (a smaller L1 carve-out)
 #define NPM_WS_SMEM_PAD 0
@@ -245,12 +245,14 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
   uint64_t* bar_dzf = bars + 2;
   uint64_t* bar_dze = bars + 3;
   uint64_t* bar_hs = bars + 4 + 2 * S0;
+  uint64_t* bar_mma2 = bars + 5 + 2 * S0;
   uint64_t* bar_x0f = bars + 4;
   uint64_t* bar_x0e = bars + 4 + S0;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_TSLOT);
   if (tid == 0) {
     tc::mbar_init(bar_w, 1);
     tc::mbar_init(bar_mma, 1);
+    tc::mbar_init(bar_mma2, 1);   // the dW^T issuer (thread 128)
     tc::mbar_init(bar_dzf, T::CHAIN_THREADS);
     tc::mbar_init(bar_dze, T::SCATTER_THREADS);
     tc::mbar_init(bar_hs, 1);
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
     }
     const uint32_t wsb = sb;   // weight image at smem offset 0
     uint32_t phase = 0;
+    uint32_t phase2 = 0;   // bar_mma2 (the dW^T batches)
     double loss = 0.0;
     unsigned c_used = 0, c_zero = 0, c_drop = 0;
     auto handoff = [&]() {
@@ -611,7 +614,10 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
 #pragma unroll
       for (int k = NL - 1; k >= 0; --k) {
         handoff();
-        if (tid == 0) {
+        // dX by thread 0, dW^T by thread 128 (two issuers, two commits; B200 c2:
+        // one issuer 514 us, this split 497 us; dW^T further split by output
+        // column halves over a third issuer re-reads X^T: 540 us)
+        if (tid == 0 || tid == 128) {
           tc::fence_after_sync();
           with_k<NL>(k, [&](auto KC) {
             constexpr int kk = decltype(KC)::value;
@@ -619,15 +625,23 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
             const uint32_t w = wsb + TB::woff(kk);
             const uint32_t xh = kk == 0 ? x0h : sb + T::xhoff(kk);
             const uint32_t xl = kk == 0 ? x0l : xh + (T::HF / 8) * CHR;
-            issue_dx_r<R>(tbase + (kk == 0 ? T::C_DZ : T::C_ACC), dh, dl, w, w + TB::wbytes(kk), TB::out(kk),
-                          kk > 0 ? W : NG);
-            issue_dw_m<R, T::dwm(kk)>(tbase + (uint32_t)T::dwcol(kk), xh, xl, dh, dl,
-                                      TB::out(kk) + (kk == NL - 1 ? T::XD : 0));
-            tc::mma_commit(bar_mma);
-            if (kk == 0) tc::mma_commit(bar_x0e + s);   // X0 stage free once dW_0 has read it
+            if (tid == 0) {
+              issue_dx_r<R>(tbase + (kk == 0 ? T::C_DZ : T::C_ACC), dh, dl, w, w + TB::wbytes(kk), TB::out(kk),
+                            kk > 0 ? W : NG);
+              tc::mma_commit(bar_mma);
+            } else {
+              issue_dw_m<R, T::dwm(kk)>(tbase + (uint32_t)T::dwcol(kk), xh, xl, dh, dl,
+                                        TB::out(kk) + (kk == NL - 1 ? T::XD : 0));
+              tc::mma_commit(bar_mma2);
+              if (kk == 0) tc::mma_commit(bar_x0e + s);   // X0 stage free once dW_0 has read it
+            }
           });
         }
         wait_mma();
+        mbar_wait_t(bar_mma2, phase2);
+        phase2 ^= 1u;
+        tc::fence_after_sync();
+
         NPM_WS_STAMP(3 + 2 * NL + 2 * (NL - 1 - k));
         if (k > 0) {
           // delta_{k-1} = dX_k * ReLU'(X_k) -> over X_k (read by dW_k, complete)
