@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(const float* __rest
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const uint32_t k = bin_key(px, py, pz, i, g);
     keys[i] = k;
-    atomicAdd(h + (k >> 3), 1u);
+    atomicAdd(h + (k >> (15 - kBinBits)), 1u);
   }
   __syncthreads();
   hist += (i0 / sort_chunk) * kBins;   // this span's sort-chunk row
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
     }
   }
   __syncthreads();
-  for (int64_t i = i0 + t; i < i1; i += blockDim.x) atomicAdd(h + (keys[i] >> 3), 1u);
+  for (int64_t i = i0 + t; i < i1; i += blockDim.x) atomicAdd(h + (keys[i] >> (15 - kBinBits)), 1u);
   __syncthreads();
   cursor += row * kBins;
   for (int b2 = t; b2 < kBins; b2 += blockDim.x) {
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads) bin_place_kernel(const uint32_t* __r
   __syncthreads();
   for (int64_t i = i0 + t; i < i1; i += blockDim.x) {
     const uint32_t k = keys[i];
-    const uint32_t slot = atomicAdd(h + (k >> 3), 1u);
+    const uint32_t slot = atomicAdd(h + (k >> (15 - kBinBits)), 1u);
     // pack: the sub-cell rides in the top 3 bits for bin_refine (n < 2^29)
     perm[slot] = (uint32_t)i | (pack ? (k & 7u) << 29 : 0u);
   }

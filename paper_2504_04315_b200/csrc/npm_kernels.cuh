@@ -145,7 +145,11 @@ namespace npm {
 // code of their cell in a 16^3 grid over the AABB, so that the 32 samples of a
 // warp are spatially clustered and their grid gathers / scatter-adds touch
 // few cache lines.  perm[t] = original index of the t-th processed sample.
+#ifdef NPM_BIN_BITS   // measurement override (bins = 2^bits Morton cells; 12 = 16^3)
+constexpr int kBinBits = NPM_BIN_BITS;
+#else
 constexpr int kBinBits = 12;
+#endif
 constexpr int64_t kSortChunk = 1 << 20;   // sort-chunk for L2-resident tables (npm_capi.cu)
 int bin_hist_entries(int64_t n, int64_t sort_chunk);   // histogram entries launch_bin needs
 int launch_bin(const float* px, const float* py, const float* pz, int64_t n, int64_t sort_chunk, bool refine,
