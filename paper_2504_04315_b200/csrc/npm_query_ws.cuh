@@ -1,18 +1,21 @@
 // npm_query_ws.cuh -- warp-specialised fused query kernel for the radiance
 // shapes with K = 8 lobes (c1, c2 / c3, c5): guide sampling (C-O10),
 // the pdf at the sample and the pdf at a caller direction (Eq. 3 mixture,
-// P:201-206), one persistent 512-thread CTA per SM.
+// P:201-206), one persistent 768-thread CTA per SM.
 //
-//   warps 0-3, 4-7  CHAIN groups g = 0, 1: group g runs the CTA's tiles
-//       kt = g, g + 2, ... (a tile = 128 rows = the MMA M; thread = one row =
-//       one TMEM lane).  Per tile: the layer-0 MMA from the X0 stage, then per
-//       layer the epilogue (bias, ReLU, split-bf16 into the group's hidden
-//       buffer) and the next MMA, then the Table 1 head for all K lobes of the
-//       row (no exchange between threads): softmax, pdf at w_q, the lobe
-//       choice (C-A17), the Jakob sampler in the Duff ONB and the pdf at the
-//       sample.  The two groups interleave: one's MMA round trips and head
-//       overlap the other's.
-//   warps 8-15  MEMORY: thread (part, row), part = which half of the L grid
+//   warps 0-7, 8-15  CHAIN groups g = 0, 1: group g runs the CTA's tiles
+//       kt = g, g + 2, ... (a tile = 128 rows = the MMA M; row r = TMEM lane
+//       r, its two threads are warps w and w + 4 of the group, each owning
+//       half the columns and lobes).  Per tile: the layer-0 MMA from the X0
+//       stage (smem), then per layer the epilogue (bias, ReLU, split-bf16) and
+//       the next MMA, whose A operand the epilogue writes straight into TMEM
+//       (tcgen05.st; `tcgen05.mma ... [a_tmem]`), then the Table 1 head:
+//       softmax, pdf at w_q, the lobe choice (C-A17), the Jakob sampler in the
+//       Duff ONB and the pdf at the sample, the two threads of a row exchanging
+//       their partial sums through smem behind a 64-thread pair barrier.  The
+//       two groups interleave: one's MMA round trips and head overlap the
+//       other's.
+//   warps 16-23  MEMORY: thread (part, row), part = which half of the L grid
 //       levels.  For every tile in order: normalise x (C-O1), the 8 corners
 //       per level (Eq. 13, C-O3/C-O4), gather + blend (C-O5) into an X0 stage
 //       (split bf16, chunk-major) and the row data (sample index, validity,
@@ -20,11 +23,11 @@
 //       C-A18) into its row-data stage; S stages, so the gathers run ahead of
 //       the chains.
 //
-// mbarriers: x0f[s] (256 memory arrivals: stage filled), x0e[s] (128 chain
-// arrivals of the consuming group after its layer-0 MMA completed and the row
-// data is in registers: stage free), mma[g] (tcgen05.commit of group g).
-// Replaces the r01 query kernel for plain sample / pdf calls (the variants
-// with decode outputs, f-1, f-2 and the product shape keep it).
+// mbarriers: x0f[s] (memory arrivals: stage filled), x0e[s] (the consuming
+// group's arrivals after its layer-0 MMA completed and the row data is in
+// registers: stage free), mma[g] (tcgen05.commit of group g).
+// Used for plain sample / pdf calls (the variants with decode outputs, f-1,
+// f-2 and the product shape keep the r01 kernel).
 #pragma once
 
 namespace qws {
@@ -66,6 +69,11 @@ struct QW {
   static_assert(MP != 4 || CHAIN_THREADS * CHAIN_REGS + MEM_THREADS * MEM_REGS <= THREADS * LAUNCH_REGS, "regs");
   static constexpr int RDF = 8;   // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u
   static constexpr uint32_t X0_BYTES = 2u * (KIN / 8) * CHR;
+  // hidden-activation buffers: used only by the smem-A measurement variant
+  // (NPM_QWS_SMEMA); with the A operand in TMEM they stay allocated as a gap
+  // between the weights and the X0 stages -- the compact layout measured
+  // slower on B200 (c2 212 vs 206 us, c5 3164 vs 3032 us; a pad at the end of
+  // the layout instead: 212 us), cause not identified
   static constexpr uint32_t H_BYTES = 2u * (W / 8) * CHR;
   static constexpr uint32_t RD_BYTES = RDF * R * 4;
   static constexpr uint32_t a1k(uint32_t x) { return (x + 1023u) & ~1023u; }
@@ -136,7 +144,14 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
     auto psync = [&]() { tc::named_sync(3u + 4u * (uint32_t)g + (uint32_t)(warp & 3), 64u); };
     const uint32_t lad = (uint32_t)((warp & 3) * 32) << 16;       // TMEM lane field
     const uint32_t tacc = (uint32_t)(64 * g);
+#ifdef NPM_QWS_SMEMA
     const uint32_t hh = sb + T::OFF_H + (uint32_t)g * T::H_BYTES, hl = hh + (W / 8) * CHR;
+#endif
+#ifndef NPM_QWS_SMEMA
+    // A operand of the hidden layers in TMEM: hi at columns 256 + 64 g, lo 32 further
+    const uint32_t tah = (uint32_t)(256 + 64 * g), tal = tah + (uint32_t)(W / 2);
+    static_assert(W / 2 <= 32, "A columns per group");
+#endif
     const float* bias = reinterpret_cast<const float*>(smem + T::OFF_B);
     uint64_t* bmma = bar_mma + g;
     uint32_t phase = 0;
@@ -195,6 +210,45 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           v[4 * j + 2] = fmaxf(v[4 * j + 2] + bb.z, 0.0f);
           v[4 * j + 3] = fmaxf(v[4 * j + 3] + bb.w, 0.0f);
         }
+#ifndef NPM_QWS_SMEMA
+        // the next layer's A operand straight into tensor memory (split-bf16 hi /
+        // lo, two features per column): no smem round trip, no proxy fence
+        {
+          uint32_t ph[WQ / 2], pl[WQ / 2];
+#pragma unroll
+          for (int q = 0; q < WQ / 2; ++q) tc::split_pack(v[2 * q], v[2 * q + 1], ph[q], pl[q]);
+          if constexpr (WQ / 2 >= 16) {
+#pragma unroll
+            for (int c = 0; c < WQ / 2; c += 16) {
+              tc::tmem_st16(lad + tah + (uint32_t)(h * (WQ / 2) + c), ph + c);
+              tc::tmem_st16(lad + tal + (uint32_t)(h * (WQ / 2) + c), pl + c);
+            }
+          } else {
+            static_assert(WQ / 2 == 8, "columns per row part");
+            tc::tmem_st8(lad + tah + (uint32_t)(h * 8), ph);
+            tc::tmem_st8(lad + tal + (uint32_t)(h * 8), pl);
+          }
+          tc::tmem_wait_st();
+          tc::fence_before_sync();
+          tc::named_sync(1u + (uint32_t)g, (uint32_t)T::GROUP_THREADS);
+        }
+        QWS_STAMP(3 + 2 * k);
+        if (gt == 0) {
+          tc::fence_after_sync();
+          const uint32_t w = sb + T::OFF_W + TB::woff(k + 1);
+          const int out = TB::out(k + 1);
+          const uint32_t idesc = tc::idesc_bf16(R, out, false, false);
+          const uint64_t bh = tc::sdesc(w, out * 16, 128), bl = tc::sdesc(w + TB::wbytes(k + 1), out * 16, 128);
+#pragma unroll
+          for (int ks = 0; ks < TB::in_p(k + 1) / 16; ++ks) {
+            const uint64_t wa = (uint64_t)(ks * 2 * out * 16) >> 4;
+            tc::mma_bf16_ts(tacc, tah + 8u * ks, bh + wa, idesc, ks > 0 ? 1u : 0u);
+            tc::mma_bf16_ts(tacc, tah + 8u * ks, bl + wa, idesc, 1u);
+            tc::mma_bf16_ts(tacc, tal + 8u * ks, bh + wa, idesc, 1u);
+          }
+          tc::mma_commit(bmma);
+        }
+#else
 #pragma unroll
         for (int c8 = 0; c8 < WQ / 8; ++c8) tc::store_chunk(hh, hl, R, r, h * (WQ / 8) + c8, v + 8 * c8);
         handoff();
@@ -205,6 +259,7 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           issue_fwd(tacc, hh, hl, w, w + TB::wbytes(k + 1), TB::in_p(k + 1), TB::out(k + 1));
           tc::mma_commit(bmma);
         }
+#endif
         wait_mma();
         QWS_STAMP(4 + 2 * k);
       }
