@@ -156,3 +156,46 @@ def test_frame_step_equals_sample_then_train_step(pipelined):
     assert abs(s0["grad_norm_sq"] - s1["grad_norm_sq"]) <= 1e-3 * s1["grad_norm_sq"]
     d = np.abs(par0.astype(np.float64) - par1)
     assert d.max() <= 2 * 5e-3 + 1e-6 and (d == 0).mean() > 0.9
+
+
+@pytest.mark.parametrize("kind", ["learn_alpha", "variance_aware"])
+def test_frame_step_with_the_f4_objectives(kind):
+    """npm_frame_step from pinned host buffers on a learn_alpha model (records
+    carry p_bsdf, staged path: C-A34) and a variance-aware model (divergence
+    2, C-A35): the same statistics and parameters as npm_sample +
+    npm_train_step on the same host buffers."""
+    from workloads.configs import CONFIGS
+    from oracle import guide as oguide
+    n = 300007   # >= 2 pipeline chunks (the variance-aware model takes the pipelined path)
+    b = synth.query_batch(n, seed=53)
+    tb = synth.training_batch(n, seed=54)
+    pb = oguide.bsdf_pdf(tb["nrm"].astype(np.float64), tb["wi"].astype(np.float64)).astype(np.float32)
+    H = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    kw = dict(learn_alpha=1) if kind == "learn_alpha" else dict(divergence=2)
+    res = []
+    for fused in (True, False):
+        m = npm.Model(0, **dict(CONFIGS["c2"]["model"], **kw))
+        hx, hw, tx, twi, ttg, tpd, hpb = (H(b["x"]), H(b["wq"]), H(tb["x"]), H(tb["wi"]), H(tb["target"]),
+                                          H(tb["pdf"]), H(pb))
+        hq = npm.make_query(n, hx[0], hx[1], hx[2])
+        ht = npm.make_query(n, tx[0], tx[1], tx[2], bsdf_pdf=hpb if kind == "learn_alpha" else None)
+        wi, pdf, pdfq = H(np.zeros((3, n), np.float32)), H(np.zeros(n, np.float32)), H(np.zeros(n, np.float32))
+        if fused:
+            st = npm.npm_frame_step(m.h, hq, None, 5, 77, 1, wi[0], wi[1], wi[2], pdf, hw[0], hw[1], hw[2], pdfq,
+                                    ht, twi[0], twi[1], twi[2], ttg, 1, tpd, n)
+        else:
+            npm.npm_sample(m.h, hq, None, 5, 77, 1, wi[0], wi[1], wi[2], pdf, hw[0], hw[1], hw[2], pdfq)
+            st = npm.npm_train_step(m.h, ht, twi[0], twi[1], twi[2], ttg, 1, tpd, n)
+        torch.cuda.synchronize()
+        res.append((wi.numpy().copy(), st, m.get(npm.BUF_PARAMS).cpu().numpy()))
+        m.close()
+    (w0, s0, par0), (w1, s1, par1) = res
+    assert np.array_equal(w0, w1)
+    for k in ("n_used", "n_zero_target", "n_dropped", "n_nonfinite_grad"):
+        assert s0[k] == s1[k], k
+    assert abs(s0["loss_proxy"] - s1["loss_proxy"]) <= 1e-5 * abs(s1["loss_proxy"])
+    d = np.abs(par0.astype(np.float64) - par1)
+    assert d.max() <= 2 * 5e-3 + 1e-6 and (d == 0).mean() > 0.9
+    if kind == "learn_alpha":   # the selection head moved away from 0 in both
+        head = par0[-((CONFIGS["c2"]["model"].get("mlp_width", 64) + 1 + 3) // 4 * 4):]
+        assert np.abs(head).max() > 0
