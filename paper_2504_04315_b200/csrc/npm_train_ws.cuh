@@ -446,18 +446,18 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
             const float nrm = lobe_norm_fast(kap[m], emk[m]);
             vv[m] = lobe_eval(nrm, kap[m], mx[m], my[m], mz[m], wx, wy, wz);
           }
-          // softmax max / normaliser / mixture sum across the row's two threads
+          // softmax normaliser / mixture sum across the row's two threads in ONE
+          // exchange: each part's sums relative to its own maximum m_h, rescaled
+          // by e^{m_h - M} after the barrier (M = max(m_0, m_1))
           NPM_WS_STAMP(12);
-          rd[h * R + r] = mloc;
-          psync();
-          const float M = fmaxf(rd[r], rd[R + r]);
           float e[KH], S = 0.0f, P = 0.0f;
 #pragma unroll
           for (int m = 0; m < KH; ++m) {
-            e[m] = __expf(lp[m] - M);
+            e[m] = __expf(lp[m] - mloc);
             S += e[m];
             P += e[m] * vv[m];
           }
+          rd[h * R + r] = mloc;
           rd[(4 + 2 * h) * R + r] = S;
           rd[(5 + 2 * h) * R + r] = P;
           float* vx = reinterpret_cast<float*>(smem + T::OFF_VX);
@@ -469,13 +469,20 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
               vx[(5 * j + 1) * R + r] = mx[m];
               vx[(5 * j + 2) * R + r] = my[m];
               vx[(5 * j + 3) * R + r] = mz[m];
-              vx[(5 * j + 4) * R + r] = e[m];
+              vx[(5 * j + 4) * R + r] = e[m];   // relative to m_h (rescaled by the reader)
             }
           }
           psync();
           NPM_WS_STAMP(14);
-          // the same association order on every thread of the row: parts 0, 1, ...
-          const float St = 0.0f + rd[4 * R + r] + rd[6 * R + r], Pt = 0.0f + rd[5 * R + r] + rd[7 * R + r];
+          const float m0 = rd[r], m1 = rd[R + r], Mx = fmaxf(m0, m1);
+          const float c0 = __expf(m0 - Mx), c1 = __expf(m1 - Mx);
+          // the same association order on every thread of the row: parts 0, 1
+          const float St = rd[4 * R + r] * c0 + rd[6 * R + r] * c1, Pt = rd[5 * R + r] * c0 + rd[7 * R + r] * c1;
+          {
+            const float ch = h ? c1 : c0;
+#pragma unroll
+            for (int m = 0; m < KH; ++m) e[m] *= ch;   // now e^{l - M}
+          }
           const float invS = 1.0f / St;
           const float Vb = fmaxf(Pt * invS, kVFloor);
           const float invV = 1.0f / Vb;
@@ -511,7 +518,7 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
 #pragma unroll 2
             for (int j = 0; j < K; ++j) {
               const float kj = vx[(5 * j) * R + r], jx = vx[(5 * j + 1) * R + r], jy = vx[(5 * j + 2) * R + r],
-                          jz = vx[(5 * j + 3) * R + r], ej = vx[(5 * j + 4) * R + r];
+                          jz = vx[(5 * j + 3) * R + r], ej = vx[(5 * j + 4) * R + r] * (j < KH ? c0 : c1);
               const float Cj = ej * cnorm(kj);
 #pragma unroll
               for (int m = 0; m < KH; ++m) {
@@ -532,9 +539,9 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
             float Zh = 0.0f;
 #pragma unroll
             for (int m = 0; m < KH; ++m) Zh += e[m] * A[m];
-            rd[h * R + r] = Zh;   // rows 0 / 1 (the maxima) are dead after the second barrier
+            rd[(2 + h) * R + r] = Zh;   // rows 2 / 3 (unused in this mode / the validity flag, read before the barrier)
             psync();
-            const float Zs = 0.0f + rd[r] + rd[R + r];   // sum_ij e_i e_j I_ij = Z S^2
+            const float Zs = 0.0f + rd[2 * R + r] + rd[3 * R + r];   // sum_ij e_i e_j I_ij = Z S^2
             const float invZs = 1.0f / Zs;
             logZ = __logf(Zs * invS * invS);
 #pragma unroll
