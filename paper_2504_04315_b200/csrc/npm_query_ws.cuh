@@ -35,7 +35,8 @@ namespace qws {
 // MP: memory parts (levels L / MP per thread).  2: 8 memory warps, every
 // warp at 128 registers.  4 (measurement): 16 memory warps at 64 registers and
 // the chain at 112 via setmaxnreg -- no faster (the chain is the bound).
-template <class N>
+// MODE 0: guide sampling / pdf; 1: combined BSDF / guide one-sample MIS (f-1)
+template <class N, int MODE = 0>
 struct QW {
   using B = TC<N>;
   static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN, L = N::L, K = N::K;
@@ -67,7 +68,8 @@ struct QW {
   static constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;
   static constexpr int CHAIN_REGS = TPR == 2 ? 80 : 112, MEM_REGS = TPR == 2 ? 48 : 64;
   static_assert(MP != 4 || CHAIN_THREADS * CHAIN_REGS + MEM_THREADS * MEM_REGS <= THREADS * LAUNCH_REGS, "regs");
-  static constexpr int RDF = 8;   // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u
+  // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u | MODE 1: 8 u_sel, 9-11 normal
+  static constexpr int RDF = MODE == 1 ? 12 : 8;
   static constexpr uint32_t X0_BYTES = 2u * (KIN / 8) * CHR;
   // hidden-activation buffers: used only by the smem-A measurement variant
   // (NPM_QWS_SMEMA); with the A operand in TMEM they stay allocated as a gap
@@ -81,7 +83,7 @@ struct QW {
   static constexpr uint32_t OFF_H = a1k(B::WBYTES + B::BBYTES);
   // TPR = 2 head exchange per group [RED_ROWS][R] f32: 0-1 max, 2-3 sums,
   // 4-5 pdf at w_q, 6-8 the sample, 9-10 pdf at the sample (part h in row +h)
-  static constexpr int RED_ROWS = TPR == 2 ? 11 : 0;
+  static constexpr int RED_ROWS = TPR == 2 ? (MODE == 1 ? 13 : 11) : 0;   // MODE 1: 11-12 logit parts (C-A34)
   static constexpr uint32_t RED_BYTES = (uint32_t)RED_ROWS * R * 4u;
   static constexpr uint32_t OFF_RED = OFF_H + GROUPS * H_BYTES;
   static constexpr uint32_t OFF_X0 = a1k(OFF_RED + GROUPS * RED_BYTES);
@@ -97,9 +99,10 @@ struct QW {
   static_assert(W <= 64 && NOUT <= 64, "accumulator columns");
 };
 
-template <class N>
-__global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a) {
-  using T = QW<N>;
+template <class N, int MODE>
+__global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(QueryArgs a) {
+  using T = QW<N, MODE>;
+  constexpr bool COMBINED = MODE == 1;
   using TB = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W, L = N::L, KIN = T::KIN;
   constexpr int R = T::R, S = T::S;
@@ -189,6 +192,8 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       const bool valid = rd[R + r] != 0.0f;
       const float qx = rd[2 * R + r], qy = rd[3 * R + r], qz = rd[4 * R + r];
       const float u1 = rd[5 * R + r], u2 = rd[6 * R + r], u3 = rd[7 * R + r];
+      float u4 = 1.0f, bnx = 0.0f, bny = 0.0f, bnz = 1.0f;
+      if constexpr (COMBINED) { u4 = rd[8 * R + r]; bnx = rd[9 * R + r]; bny = rd[10 * R + r]; bnz = rd[11 * R + r]; }
       wait_mma();
       QWS_STAMP(2);
       ws::mbar_arrive(bar_x0e + s);   // X0 read by the MMA, row data in registers
@@ -209,6 +214,12 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           v[4 * j + 1] = fmaxf(v[4 * j + 1] + bb.y, 0.0f);
           v[4 * j + 2] = fmaxf(v[4 * j + 2] + bb.z, 0.0f);
           v[4 * j + 3] = fmaxf(v[4 * j + 3] + bb.w, 0.0f);
+        }
+        if (COMBINED && k == NL - 2 && a.alpha_w) {   // C-A34: this part's a . h_{L-1}
+          float zp = 0.0f;
+#pragma unroll
+          for (int j = 0; j < WQ; ++j) zp = fmaf(__ldg(a.alpha_w + h * WQ + j), v[j], zp);
+          red[(11 + h) * R + r] = zp;   // read after the next group barrier
         }
 #ifndef NPM_QWS_SMEMA
         // the next layer's A operand straight into tensor memory (split-bf16 hi /
@@ -339,8 +350,22 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
       if (a.do_sample) {
         // i* = min{i : u1 < C_i}, C_i = sum_{j<=i} lambda_j; K-1 if none (C-A17):
         // the part whose range [B_h, B_h+1) holds u1 (the last part takes the rest)
-        const bool own = TPR == 1 || (u1 >= Bh * invS && (u1 < Bn * invS || h == TPR - 1));
+        // f-1: BSDF with probability alpha (C-A25), else the guide; alpha the
+        // caller's or the learned alpha(x) (C-A34)
+        float alpha = a.alpha;
+        if (COMBINED && a.alpha_w) {
+          float z = __ldg(a.alpha_w + W);
+#pragma unroll
+          for (int qq = 0; qq < TPR; ++qq) z += red[(11 + qq) * R + r];
+          alpha = 1.0f / (1.0f + __expf(-z));
+        }
+        const bool use_bsdf = COMBINED && u4 < alpha;
+        const bool own = !use_bsdf && (TPR == 1 || (u1 >= Bh * invS && (u1 < Bn * invS || h == TPR - 1)));
         float wx = 0.f, wy = 0.f, wz = 0.f;
+        if (COMBINED && use_bsdf && h == 0) {
+          bsdf_sample(bnx, bny, bnz, u1, u2, wx, wy, wz);
+          if constexpr (TPR == 2) { red[6 * R + r] = wx; red[7 * R + r] = wy; red[8 * R + r] = wz; }
+        }
         if (own) {
           int sel = KQ - 1;
           float cum = Bh;
@@ -369,8 +394,26 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
           P2 = red[9 * R + r] + red[10 * R + r];
         }
         if (valid && h == 0) {
-          a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
-          a.spdf[i] = P2 * invS;
+          if constexpr (COMBINED) {
+            float V = P2 * invS, ox = wx, oy = wy, oz = wz, pc;
+            int32_t tq = use_bsdf ? 0 : 1;
+            if (!use_bsdf && !(isfinite(V) && V >= kVFloor)) {   // guide pdf underflow (C-A26)
+              bsdf_sample(bnx, bny, bnz, u1, u2, ox, oy, oz);
+              pc = bsdf_pdf(bnx, bny, bnz, ox, oy, oz);
+              V = 0.0f;
+              tq = 2;
+            } else {
+              // one-sample balance heuristic p~ = alpha p_bsdf + (1 - alpha) V
+              pc = alpha * bsdf_pdf(bnx, bny, bnz, ox, oy, oz) + (1.0f - alpha) * V;
+            }
+            if (a.gpdf) a.gpdf[i] = V;
+            if (a.tech) a.tech[i] = tq;
+            a.sx[i] = ox; a.sy[i] = oy; a.sz[i] = oz;
+            a.spdf[i] = pc;
+          } else {
+            a.sx[i] = wx; a.sy[i] = wy; a.sz[i] = wz;
+            a.spdf[i] = P2 * invS;
+          }
         }
       }
       QWS_STAMP(4 + 2 * (NL - 1));
@@ -424,15 +467,20 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
         uy = normalize_axis(x1, a.grid.lo[1], a.grid.inv[1]);
         uz = normalize_axis(x2, a.grid.lo[2], a.grid.inv[2]);
       }
-      float ex[3] = {0.f, 0.f, 0.f};   // part 0: w_q; part 1: the uniforms
+      // part 0: w_q (and the normal, MODE 1); part 1: the uniforms
+      float ex[4] = {0.f, 0.f, 0.f, 1.f}, nn[3] = {0.f, 0.f, 1.f};
       if (part == 0) {
         if (want_pdf) { ex[0] = __ldg(a.wx + i); ex[1] = __ldg(a.wy + i); ex[2] = __ldg(a.wz + i); }
+        if constexpr (COMBINED) {
+          if (valid) { nn[0] = __ldg(a.bnx + i); nn[1] = __ldg(a.bny + i); nn[2] = __ldg(a.bnz + i); }
+        }
       } else if (part == 1 && a.do_sample) {
         if (a.u) {
           ex[0] = __ldg(a.u + i); ex[1] = __ldg(a.u + n + i); ex[2] = __ldg(a.u + 2 * n + i);
+          if constexpr (COMBINED) ex[3] = __ldg(a.u + 3 * n + i);
         } else {
           const float4 u = philox_uniforms4(a.seed, (uint64_t)i + a.offset);
-          ex[0] = u.x; ex[1] = u.y; ex[2] = u.z;
+          ex[0] = u.x; ex[1] = u.y; ex[2] = u.z; ex[3] = u.w;
         }
       }
       // branch-free over the levels (an invalid row gathers at the AABB corner
@@ -462,8 +510,10 @@ __global__ void __launch_bounds__(QW<N>::THREADS, 1) query_ws_kernel(QueryArgs a
         rd[row] = __uint_as_float((uint32_t)i);
         rd[R + row] = valid ? 1.0f : 0.0f;
         rd[2 * R + row] = ex[0]; rd[3 * R + row] = ex[1]; rd[4 * R + row] = ex[2];
+        if constexpr (COMBINED) { rd[9 * R + row] = nn[0]; rd[10 * R + row] = nn[1]; rd[11 * R + row] = nn[2]; }
       } else if (part == 1) {
         rd[5 * R + row] = ex[0]; rd[6 * R + row] = ex[1]; rd[7 * R + row] = ex[2];
+        if constexpr (COMBINED) rd[8 * R + row] = ex[3];
       }
       tc::fence_proxy_async();
       ws::mbar_arrive(bar_x0f + s);

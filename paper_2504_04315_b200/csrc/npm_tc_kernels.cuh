@@ -1147,22 +1147,27 @@ struct TcLaunch {
   static int query(const QueryArgs& a, int sms, cudaStream_t st) {
     using T = TC<N>;
     if constexpr (!N::PRODUCT && N::K == 8) {
-      // warp-specialised kernel for plain sample / pdf calls (npm_query_ws.cuh)
-      if (a.qws && !a.combined && !a.cos_product && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
-        using Q = qws::QW<N>;
-        if (Q::MP == 4) {   // the setmaxnreg split assumes the launch allocation (a hang otherwise)
-          static int regs = -1;
-          if (regs < 0) {
-            cudaFuncAttributes fa;
-            regs = cudaFuncGetAttributes(&fa, qws::query_ws_kernel<N>) == cudaSuccess ? fa.numRegs : 0;
+      // warp-specialised kernel for sample / pdf and combined-MIS calls (npm_query_ws.cuh)
+      if (a.qws && !a.cos_product && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
+        auto go = [&](auto MC) -> int {
+          constexpr int MODE = decltype(MC)::value;
+          using Q = qws::QW<N, MODE>;
+          if (Q::MP == 4) {   // the setmaxnreg split assumes the launch allocation (a hang otherwise)
+            static int regs = -1;
+            if (regs < 0) {
+              cudaFuncAttributes fa;
+              regs = cudaFuncGetAttributes(&fa, qws::query_ws_kernel<N, MODE>) == cudaSuccess ? fa.numRegs : 0;
+            }
+            if (regs != Q::LAUNCH_REGS) return -1;
           }
-          if (regs != Q::LAUNCH_REGS) return -1;
-        }
-        cudaFuncSetAttribute(qws::query_ws_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
-        const int64_t ntiles = (a.n + Q::R - 1) / Q::R;
-        const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
-        qws::query_ws_kernel<N><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
-        return 1;
+          cudaFuncSetAttribute(qws::query_ws_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Q::SMEM);
+          const int64_t ntiles = (a.n + Q::R - 1) / Q::R;
+          const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
+          qws::query_ws_kernel<N, MODE><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
+          return 1;
+        };
+        return a.combined ? go(std::integral_constant<int, 1>{}) : go(std::integral_constant<int, 0>{});
       }
     }
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA
