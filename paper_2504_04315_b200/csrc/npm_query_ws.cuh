@@ -35,7 +35,8 @@ namespace qws {
 // MP: memory parts (levels L / MP per thread).  2: 8 memory warps, every
 // warp at 128 registers.  4 (measurement): 16 memory warps at 64 registers and
 // the chain at 112 via setmaxnreg -- no faster (the chain is the bound).
-// MODE 0: guide sampling / pdf; 1: combined BSDF / guide one-sample MIS (f-1)
+// MODE 0: guide sampling / pdf; 1: combined BSDF / guide one-sample MIS (f-1);
+// 2: the mixture times the cosine lobe about the normal (f-2)
 template <class N, int MODE = 0>
 struct QW {
   using B = TC<N>;
@@ -68,8 +69,9 @@ struct QW {
   static constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;
   static constexpr int CHAIN_REGS = TPR == 2 ? 80 : 112, MEM_REGS = TPR == 2 ? 48 : 64;
   static_assert(MP != 4 || CHAIN_THREADS * CHAIN_REGS + MEM_THREADS * MEM_REGS <= THREADS * LAUNCH_REGS, "regs");
-  // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u | MODE 1: 8 u_sel, 9-11 normal
-  static constexpr int RDF = MODE == 1 ? 12 : 8;
+  // row data [RDF][R]: 0 sample index (bits) | 1 valid | 2-4 w_q | 5-7 u | MODE 1: 8 u_sel;
+  // MODE 1, 2: 9-11 normal
+  static constexpr int RDF = MODE >= 1 ? 12 : 8;
   static constexpr uint32_t X0_BYTES = 2u * (KIN / 8) * CHR;
   // hidden-activation buffers: used only by the smem-A measurement variant
   // (NPM_QWS_SMEMA); with the A operand in TMEM they stay allocated as a gap
@@ -102,7 +104,7 @@ struct QW {
 template <class N, int MODE>
 __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(QueryArgs a) {
   using T = QW<N, MODE>;
-  constexpr bool COMBINED = MODE == 1;
+  constexpr bool COMBINED = MODE == 1, COSPROD = MODE == 2;
   using TB = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W, L = N::L, KIN = T::KIN;
   constexpr int R = T::R, S = T::S;
@@ -193,7 +195,8 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
       const float qx = rd[2 * R + r], qy = rd[3 * R + r], qz = rd[4 * R + r];
       const float u1 = rd[5 * R + r], u2 = rd[6 * R + r], u3 = rd[7 * R + r];
       float u4 = 1.0f, bnx = 0.0f, bny = 0.0f, bnz = 1.0f;
-      if constexpr (COMBINED) { u4 = rd[8 * R + r]; bnx = rd[9 * R + r]; bny = rd[10 * R + r]; bnz = rd[11 * R + r]; }
+      if constexpr (COMBINED) u4 = rd[8 * R + r];
+      if constexpr (COMBINED || COSPROD) { bnx = rd[9 * R + r]; bny = rd[10 * R + r]; bnz = rd[11 * R + r]; }
       wait_mma();
       QWS_STAMP(2);
       ws::mbar_arrive(bar_x0e + s);   // X0 read by the MMA, row data in registers
@@ -318,6 +321,16 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
             lobe_angles<true>(tp[j], pp[j], kap[j], th, ph, st, ct, sp, cp);
             mx[j] = st * cp; my[j] = st * sp; mz[j] = ct;
           }
+        }
+      }
+      if constexpr (COSPROD) {   // f-2: times the cosine lobe about n, renormalised via the logits
+        M = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < KQ; ++j) {
+          lp[j] += vmf_product_inplace(mx[j], my[j], mz[j], kap[j], bnx, bny, bnz, a.kappa_c, a.log_c_kc);
+          float em;
+          nrm[j] = lobe_norm(fmaxf(kap[j], 1e-30f), em);
+          M = fmaxf(M, lp[j]);
         }
       }
       if constexpr (TPR == 2) {
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
       float ex[4] = {0.f, 0.f, 0.f, 1.f}, nn[3] = {0.f, 0.f, 1.f};
       if (part == 0) {
         if (want_pdf) { ex[0] = __ldg(a.wx + i); ex[1] = __ldg(a.wy + i); ex[2] = __ldg(a.wz + i); }
-        if constexpr (COMBINED) {
+        if constexpr (COMBINED || COSPROD) {
           if (valid) { nn[0] = __ldg(a.bnx + i); nn[1] = __ldg(a.bny + i); nn[2] = __ldg(a.bnz + i); }
         }
       } else if (part == 1 && a.do_sample) {
@@ -510,7 +523,7 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
         rd[row] = __uint_as_float((uint32_t)i);
         rd[R + row] = valid ? 1.0f : 0.0f;
         rd[2 * R + row] = ex[0]; rd[3 * R + row] = ex[1]; rd[4 * R + row] = ex[2];
-        if constexpr (COMBINED) { rd[9 * R + row] = nn[0]; rd[10 * R + row] = nn[1]; rd[11 * R + row] = nn[2]; }
+        if constexpr (COMBINED || COSPROD) { rd[9 * R + row] = nn[0]; rd[10 * R + row] = nn[1]; rd[11 * R + row] = nn[2]; }
       } else if (part == 1) {
         rd[5 * R + row] = ex[0]; rd[6 * R + row] = ex[1]; rd[7 * R + row] = ex[2];
         if constexpr (COMBINED) rd[8 * R + row] = ex[3];

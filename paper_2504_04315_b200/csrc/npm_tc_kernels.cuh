@@ -1148,7 +1148,7 @@ struct TcLaunch {
     using T = TC<N>;
     if constexpr (!N::PRODUCT && N::K == 8) {
       // warp-specialised kernel for sample / pdf and combined-MIS calls (npm_query_ws.cuh)
-      if (a.qws && !a.cos_product && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
+      if (a.qws && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
         auto go = [&](auto MC) -> int {
           constexpr int MODE = decltype(MC)::value;
           using Q = qws::QW<N, MODE>;
@@ -1167,7 +1167,8 @@ struct TcLaunch {
           qws::query_ws_kernel<N, MODE><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
           return 1;
         };
-        return a.combined ? go(std::integral_constant<int, 1>{}) : go(std::integral_constant<int, 0>{});
+        return a.combined ? go(std::integral_constant<int, 1>{})
+                          : a.cos_product ? go(std::integral_constant<int, 2>{}) : go(std::integral_constant<int, 0>{});
       }
     }
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA
