@@ -44,7 +44,10 @@ struct QW {
   static constexpr int R = 128;
   static constexpr uint32_t CHR = R * 16;
   static constexpr int KIN = B::KIN;
-  static_assert(!N::PRODUCT && K == 8 && KIN == NIN && L % 4 == 0 && W % 16 == 0, "query_ws shape");
+  // radiance shapes with K = 8; the product shape (K = 16, X0 = grid features
+  // + SH4(w_o) + SH4(n) + roughness, padded to KIN = 80) for plain sample / pdf
+  static_assert((N::PRODUCT ? (K == 16 && MODE == 0 && KIN == 80 && L == 8) : (K == 8 && KIN == NIN)) &&
+                L % 4 == 0 && W % 16 == 0, "query_ws shape");
 #ifdef NPM_QWS_MP   // measurement override (4: B200 c2 233 us vs 229 us with 2)
   static constexpr int MP = L >= 4 * NPM_QWS_MP ? NPM_QWS_MP : 2;
 #else
@@ -482,6 +485,13 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
       }
       // part 0: w_q (and the normal, MODE 1); part 1: the uniforms
       float ex[4] = {0.f, 0.f, 0.f, 1.f}, nn[3] = {0.f, 0.f, 1.f};
+      float cv[4] = {0.f, 0.f, 1.f, 0.f};   // product conditioning: part 0 w_o, part 1 n + roughness
+      if constexpr (N::PRODUCT) {
+        if (valid) {
+          if (part == 0) { cv[0] = __ldg(a.wox + i); cv[1] = __ldg(a.woy + i); cv[2] = __ldg(a.woz + i); }
+          else { cv[0] = __ldg(a.nx + i); cv[1] = __ldg(a.ny + i); cv[2] = __ldg(a.nz + i); cv[3] = __ldg(a.rough + i); }
+        }
+      }
       if (part == 0) {
         if (want_pdf) { ex[0] = __ldg(a.wx + i); ex[1] = __ldg(a.wy + i); ex[2] = __ldg(a.wz + i); }
         if constexpr (COMBINED || COSPROD) {
@@ -518,6 +528,22 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
       const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (KIN / 8) * CHR;
 #pragma unroll
       for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
+      if constexpr (N::PRODUCT) {   // [32, 48) SH4(w_o) by part 0; [48, 64) SH4(n), [64, 80) roughness by part 1
+        float e16[16];
+        if (valid) sh4(cv[0], cv[1], cv[2], e16);
+        else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) e16[j] = 0.0f;
+        }
+        tc::store_chunk(xh, xl, R, row, 4 + 2 * part, e16);
+        tc::store_chunk(xh, xl, R, row, 5 + 2 * part, e16 + 8);
+        if (part == 1) {
+          float ro[8] = {valid ? cv[3] : 0.0f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          const float z8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          tc::store_chunk(xh, xl, R, row, 8, ro);
+          tc::store_chunk(xh, xl, R, row, 9, z8);
+        }
+      }
       float* rd = reinterpret_cast<float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
       if (part == 0) {
         rd[row] = __uint_as_float((uint32_t)i);

@@ -1146,9 +1146,10 @@ template <class N>
 struct TcLaunch {
   static int query(const QueryArgs& a, int sms, cudaStream_t st) {
     using T = TC<N>;
-    if constexpr (!N::PRODUCT && N::K == 8) {
+    if constexpr ((!N::PRODUCT && N::K == 8) || (N::PRODUCT && N::K == 16)) {
       // warp-specialised kernel for sample / pdf and combined-MIS calls (npm_query_ws.cuh)
-      if (a.qws && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu) {
+      if (a.qws && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu &&
+          (!N::PRODUCT || (!a.combined && !a.cos_product))) {
         auto go = [&](auto MC) -> int {
           constexpr int MODE = decltype(MC)::value;
           using Q = qws::QW<N, MODE>;
@@ -1167,8 +1168,10 @@ struct TcLaunch {
           qws::query_ws_kernel<N, MODE><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
           return 1;
         };
-        return a.combined ? go(std::integral_constant<int, 1>{})
-                          : a.cos_product ? go(std::integral_constant<int, 2>{}) : go(std::integral_constant<int, 0>{});
+        if constexpr (N::PRODUCT) return go(std::integral_constant<int, 0>{});
+        else return a.combined ? go(std::integral_constant<int, 1>{})
+                               : a.cos_product ? go(std::integral_constant<int, 2>{})
+                                               : go(std::integral_constant<int, 0>{});
       }
     }
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA

@@ -20,10 +20,11 @@ def main():
     cfg = CONFIGS[name]
     n = cfg["n"]
     m = npm.Model(0, **cfg["model"])
-    qb = synth.query_batch(n, seed=100)
+    prod = cfg["model"].get("mode", 0) == 1
+    qb = synth.query_batch(n, seed=100, product=prod)
     dev = torch.device("cuda", 0)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    q = m.query(T(qb["x"]))
+    q = m.query(T(qb["x"]), *([T(qb["wo"]), T(qb["nrm"]), T(qb["rough"])] if prod else []))
     wq = T(qb["wq"])
     for i in range(3):
         m.sample(q, seed=1, offset=i * n, use_ema=True, wq=wq)
