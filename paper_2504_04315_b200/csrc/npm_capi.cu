@@ -684,9 +684,8 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // Training kernel per shape (B200 measurements): the warp-
   // specialised kernel for L2-resident tables (c2 612 vs 632 us; c3 equal);
   // the r01 two-group kernel for HBM-resident tables, whose binned,
-  // privatised scatter it does not have (c5 4.8 vs 6.3 ms), and for the
-  // product shape (no warp-specialised instantiation).
-  m->train_ws = (m->bin_train || c.mode == NPM_PRODUCT) ? 0 : 1;
+  // privatised scatter it does not have (c5 4.8 vs 6.3 ms).
+  m->train_ws = m->bin_train ? 0 : 1;
   if (const char* e = getenv("NPM_TRAIN_WS")) m->train_ws = atoi(e);
   if (c.learn_alpha || c.divergence == 2) m->train_ws = 1;   // (C-A34 / C-A35 live in the warp-specialised kernel)
   // Privatise the scatter of small (coarse) levels when training batches are

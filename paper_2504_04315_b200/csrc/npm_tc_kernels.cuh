@@ -1197,7 +1197,7 @@ struct TcLaunch {
     return 1;
   }
   static int train(const TrainArgs& a, int sms, cudaStream_t st) {
-    if constexpr (!N::PRODUCT && N::K == 8) {
+    if constexpr ((!N::PRODUCT && N::K == 8) || (N::PRODUCT && N::K == 16 && N::L == 8)) {
       if (a.ws) {   // warp-specialised kernel (npm_train_ws.cuh)
         if (!a.wimg || a.wimg_bytes < ws::WS<N>::WIMG) return -1;
         if (a.alpha_w && (!a.alpha_g || !a.bsdf_pdf)) return -1;
@@ -1212,9 +1212,14 @@ struct TcLaunch {
           ws::train_ws_kernel<N, AH, VA><<<blocks, T::THREADS, T::SMEM, st>>>(a);
         };
         if (a.alpha_w && a.divergence == 2) return -1;   // one of the two per launch
-        if (a.alpha_w) go(std::true_type{}, std::false_type{});
-        else if (a.divergence == 2) go(std::false_type{}, std::true_type{});
-        else go(std::false_type{}, std::false_type{});
+        if constexpr (N::PRODUCT) {   // (the product shape: Eq. 9 / chi^2 only)
+          if (a.alpha_w || a.divergence == 2) return -1;
+          go(std::false_type{}, std::false_type{});
+        } else {
+          if (a.alpha_w) go(std::true_type{}, std::false_type{});
+          else if (a.divergence == 2) go(std::false_type{}, std::true_type{});
+          else go(std::false_type{}, std::false_type{});
+        }
         return 2;
       }
     }

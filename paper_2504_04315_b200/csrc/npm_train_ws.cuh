@@ -41,7 +41,10 @@ struct WS {
   static constexpr int R = 128;              // rows per tile = MMA M
   static constexpr uint32_t CHR = R * 16;    // bytes of one 8-feature chunk of a tile
   static constexpr int ZF = B::ZF, HF = B::HF, KIN = B::KIN;
-  static_assert(!N::PRODUCT && K == 8 && L % 2 == 0 && W % 32 == 0, "warp-specialised kernel shape");
+  // radiance K = 8, or the product shape (K = 16, 8 levels; X0 = grid | SH4(w_o) |
+  // SH4(n) | roughness, ones at NIN = 65 written per tile by the memory warps)
+  static_assert((N::PRODUCT ? (K == 16 && L == 8 && ZF == 80 && !AH && !VA) : K == 8) && L % 2 == 0 &&
+                W % 32 == 0, "warp-specialised kernel shape");
   static constexpr int TPR = 2;   // chain threads per row (B200 c2: 2 -> 520 us, 4 -> 561 us without the scatter)
   static constexpr int CHAIN_THREADS = TPR * R, MEM_THREADS = 256, THREADS = CHAIN_THREADS + MEM_THREADS;
   static constexpr int GATHER_THREADS = MEM_THREADS, SCATTER_THREADS = MEM_THREADS;
@@ -268,8 +271,11 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
     const float e1[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, e0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int s = 0; s < S0; ++s) {
       const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (T::ZF / 8) * CHR;
+      // (product: NIN = 65 shares chunk 8 with the roughness -- the memory warps
+      // write that chunk every tile; only the zero chunk 9 is constant)
+      constexpr int F0 = N::PRODUCT ? (NIN + 7) / 8 * 8 : NIN;
 #pragma unroll
-      for (int f = NIN; f < T::ZF; f += 8) tc::store_chunk(xh, xl, R, tid, f / 8, f == NIN ? e1 : e0);
+      for (int f = F0; f < T::ZF; f += 8) tc::store_chunk(xh, xl, R, tid, f / 8, f == NIN ? e1 : e0);
     }
 #pragma unroll
     for (int k = 1; k < NL; ++k) {
@@ -816,6 +822,14 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
         hin[6] = __ldg(a.spdf + i);
         if (AH) hin[7] = __ldg(a.bsdf_pdf + i);   // C-A34
       }
+      // product conditioning (X0 features 32-64): part 0 w_o, part 1 n + roughness
+      float cv[4] = {0.f, 0.f, 1.f, 0.f};
+      if constexpr (N::PRODUCT) {
+        if (valid) {
+          if (part == 0) { cv[0] = __ldg(a.wox + i); cv[1] = __ldg(a.woy + i); cv[2] = __ldg(a.woz + i); }
+          else { cv[0] = __ldg(a.nx + i); cv[1] = __ldg(a.ny + i); cv[2] = __ldg(a.nz + i); cv[3] = __ldg(a.rough + i); }
+        }
+      }
       const uint32_t xh = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, xl = xh + (T::ZF / 8) * CHR;
       // all of this thread's levels in registers, then wait for the stage
       float gf[4 * LP];
@@ -839,6 +853,20 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
       NPM_WS_MSTAMP(kt, 2);
 #pragma unroll
       for (int j = 0; j < LP / 2; ++j) tc::store_chunk(xh, xl, R, row, part * (LP / 2) + j, gf + 8 * j);
+      if constexpr (N::PRODUCT) {   // [32, 48) SH4(w_o) by part 0; [48, 64) SH4(n), [64, 72) roughness + ones by part 1
+        float e16[16];
+        if (valid) sh4(cv[0], cv[1], cv[2], e16);
+        else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) e16[j] = 0.0f;
+        }
+        tc::store_chunk(xh, xl, R, row, 4 + 2 * part, e16);
+        tc::store_chunk(xh, xl, R, row, 5 + 2 * part, e16 + 8);
+        if (part == 1) {
+          const float ro[8] = {valid ? cv[3] : 0.0f, 1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          tc::store_chunk(xh, xl, R, row, 8, ro);
+        }
+      }
       if (part == 0) {
         float* rd = reinterpret_cast<float*>(smem + T::OFF_RD + (uint32_t)s * T::RD_BYTES);
         rd[3 * R + row] = valid ? 1.0f : 0.0f;

@@ -194,6 +194,30 @@ def test_train_gradient_and_stats(name, n, rgb):
     m.set(npm.BUF_GRADS, np.zeros(m.n_params, np.float32))
 
 
+@pytest.mark.parametrize("train_ws", ["1", "0"])
+def test_product_train_gradient_both_kernels(train_ws, monkeypatch):
+    """The product shape (c4, K = 16) trains in the warp-specialised kernel by
+    default; the r01 two-group kernel stays selectable (NPM_TRAIN_WS=0, read at
+    model creation).  Both against the oracle at 2 tiles + a ragged tail."""
+    monkeypatch.setenv("NPM_TRAIN_WS", train_ws)
+    m, ocfg, p = make_pair("c4", seed=11)
+    n = 2 * 128 * 148 + 77
+    b = synth.training_batch(n, seed=19, product=True, rgb=True, nan_rate=1e-3)
+    st = m.accumulate_grads(gq(m, b), b["wi"], b["target"], b["pdf"], n_global=n)
+    g = m.get(npm.BUF_GRADS).cpu().numpy().astype(np.float64)
+    og, ost = onpm.gradient(ocfg, p, oq(b, True), b["wi"].astype(np.float64), b["target"].astype(np.float64),
+                            b["pdf"].astype(np.float64), n)
+    assert rel_l2(g, og) <= 2e-3
+    for kind, a, e in grad_blocks(ocfg):
+        if np.linalg.norm(og[a:e]) > 0:
+            assert rel_l2(g[a:e], og[a:e]) <= 2e-3, (kind, a, e)
+    gz = og[ocfg.n_mlp:] == 0
+    assert np.all(g[ocfg.n_mlp:][gz] == 0)
+    assert abs(st["loss_proxy"] - ost["loss_proxy"]) <= 1e-4 * abs(ost["loss_proxy"])
+    for k in ("n_used", "n_zero_target", "n_dropped"):
+        assert st[k] == ost[k], k
+
+
 def test_adam_ema_from_identical_grads():
     m, ocfg, p = pair("c2")
     rng = np.random.default_rng(5)
