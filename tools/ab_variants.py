@@ -9,12 +9,13 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.environ.get("NPM_AB_SRC", ROOT)   # another source tree (e.g. a `git archive` of HEAD)
 
 
 def build(name, defs):
     tmp = tempfile.mkdtemp(prefix="npm_abv_")
-    shutil.copytree(os.path.join(ROOT, "paper_2504_04315_b200", "csrc"), os.path.join(tmp, "p", "csrc"))
-    shutil.copytree(os.path.join(ROOT, "include"), os.path.join(tmp, "include"))
+    shutil.copytree(os.path.join(SRC, "paper_2504_04315_b200", "csrc"), os.path.join(tmp, "p", "csrc"))
+    shutil.copytree(os.path.join(SRC, "include"), os.path.join(tmp, "include"))
     csrc = os.path.join(tmp, "p", "csrc")
     flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
              "--expt-relaxed-constexpr", "-I" + os.path.join(tmp, "include"), "-I" + csrc] + defs
