@@ -63,7 +63,16 @@ struct QW {
   static constexpr int TPR = 2;
 #endif
   static_assert(TPR == 1 || TPR == 2, "threads per row");
-  static constexpr int GROUPS = 2, GROUP_THREADS = TPR * R, CHAIN_THREADS = GROUPS * GROUP_THREADS;
+  // chain groups: two for the radiance shapes (one's MMA round trips and head
+  // overlap the other's); one for the product shape, whose 8-lobe head spills
+  // at the 80 registers of a 768-thread CTA and runs without spills at the 128
+  // of a 512-thread one (B200 c4 query 1.84 -> 1.59 ms)
+#ifdef NPM_QWS_PGROUPS   // measurement override for the product shape
+  static constexpr int GROUPS = N::PRODUCT ? NPM_QWS_PGROUPS : 2;
+#else
+  static constexpr int GROUPS = N::PRODUCT ? 1 : 2;
+#endif
+  static constexpr int GROUP_THREADS = TPR * R, CHAIN_THREADS = GROUPS * GROUP_THREADS;
   static constexpr int MEM_THREADS = MP * R;
   // MP = 4 register split (setmaxnreg moves registers only within the CTA's
   // launch allocation): TPR 1: 256 x 112 + 512 x 64 = 768 x 80; TPR 2:
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(Query
 #define QWS_STAMP(idx) do { } while (0)
 #endif
     int kt = g;
-    for (int64_t tile = blockIdx.x + (int64_t)g * tstride; tile < ntiles; tile += 2 * tstride, kt += 2) {
+    for (int64_t tile = blockIdx.x + (int64_t)g * tstride; tile < ntiles; tile += T::GROUPS * tstride, kt += T::GROUPS) {
       QWS_STAMP(0);
       const int s = kt % S;
       const uint32_t x0h = sb + T::OFF_X0 + (uint32_t)s * T::X0_BYTES, x0l = x0h + (KIN / 8) * CHR;

@@ -42,6 +42,22 @@ def run(name, n, ws):
     m.close()
 
 
+def objectives(n):
+    """f-4' learned selection probability (C-A34) and f-4 variance-aware target (C-A35)."""
+    from oracle import guide   # stand-in BSDF pdf of the records' directions (input data only)
+    os.environ["NPM_TRAIN_WS"] = "1"
+    b = synth.training_batch(n, seed=8, rgb=True, nan_rate=1e-3)
+    pb = guide.bsdf_pdf(b["nrm"].astype(np.float64), b["wi"].astype(np.float64)).astype(np.float32)
+    m = npm.Model(0, learn_alpha=1, **CONFIGS["c2"]["model"])
+    m.train_step(m.query(b["x"], bsdf_pdf=pb), b["wi"], b["target"], b["pdf"])
+    m.combined_sample(m.query(b["x"]), b["nrm"], alpha=0.5, seed=3)
+    m.close()
+    m = npm.Model(0, **dict(CONFIGS["c2"]["model"], divergence=2))
+    m.train_step(m.query(b["x"]), b["wi"], b["target"], b["pdf"])
+    print("objectives", n, "ok", flush=True)
+    m.close()
+
+
 def frame(n):
     import torch
     os.environ["NPM_TRAIN_WS"] = "1"
@@ -62,4 +78,6 @@ if __name__ == "__main__":
     run("c2", 70000, 1)
     run("c2", 70000, 0)
     run("c4", 20000, 0)
+    run("c4", 20000, 1)
+    objectives(20000)
     frame(140000)
