@@ -109,6 +109,7 @@ struct npm_model {
   int pipe_chunks = 3;     // NPM_PIPE_CHUNKS (c2 e2e: 2 -> 1.31, 3 -> 1.32, 4 -> 1.28, 8 -> 1.13 G/s)
   int query_groups = 1;    // NPM_QUERY_GROUPS
   int query_ws = 1;        // NPM_QUERY_WS
+  int qws_groups = 2;      // chain groups of query_ws_kernel's plain calls (NPM_QWS_GROUPS)
 };
 
 namespace {
@@ -361,6 +362,7 @@ void fill_query_args(const npm_model* m, const npm_query& d, int use_ema, QueryA
   a.log_kmax = logf(m->cfg.kappa_max);
   a.query_groups = m->query_groups;
   a.qws = m->query_ws;
+  a.qws_groups = m->qws_groups;
   a.alpha_w = m->n_alpha ? a.params + m->n_mlp + m->n_grid : nullptr;
 }
 
@@ -681,6 +683,11 @@ npm_status npm_create(const npm_config* cfg, int dev, npm_model** out) {
   // or slower (the binned scatter-adds collide on L2 lines).
   m->bin_train = m->n_grid * 4 > ((int64_t)64 << 20);
   if (const char* e = getenv("NPM_BIN_TRAIN")) m->bin_train = e[0] == '1';
+  // query_ws_kernel chain groups (B200, same box): two for L2-resident
+  // radiance tables (c2 205 vs 232 us with one), one for HBM-resident tables
+  // (c5 3.04 -> 2.34 ms) and the product shape (c4 1.84 -> 1.59 ms)
+  m->qws_groups = (c.mode == NPM_PRODUCT || m->n_grid * 4 > ((int64_t)64 << 20)) ? 1 : 2;
+  if (const char* e = getenv("NPM_QWS_GROUPS")) m->qws_groups = atoi(e) == 1 ? 1 : 2;
   // Training kernel per shape (B200 measurements): the warp-
   // specialised kernel for L2-resident tables (c2 612 vs 632 us; c3 equal);
   // the r01 two-group kernel for HBM-resident tables, whose binned,

@@ -49,6 +49,7 @@ struct QueryArgs {
   long long* dbg_clock;               // measurement builds (-DNPM_QUERY_STAMPS): [64 tiles][16] stamps of CTA 0
   const float* alpha_w;               // C-A34 selection head (a [W], c) of `params`, or NULL: use `alpha`
   int qws;                            // warp-specialised kernel for plain sample / pdf calls (NPM_QUERY_WS)
+  int qws_groups;                     // its chain groups for plain calls: 1 or 2 (NPM_QWS_GROUPS)
 };
 
 struct TrainArgs {

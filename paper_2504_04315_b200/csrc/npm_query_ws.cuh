@@ -37,7 +37,7 @@ namespace qws {
 // the chain at 112 via setmaxnreg -- no faster (the chain is the bound).
 // MODE 0: guide sampling / pdf; 1: combined BSDF / guide one-sample MIS (f-1);
 // 2: the mixture times the cosine lobe about the normal (f-2)
-template <class N, int MODE = 0>
+template <class N, int MODE = 0, int G = 2>
 struct QW {
   using B = TC<N>;
   static constexpr int NL = N::NL, W = N::W, NOUT = N::NOUT, NIN = N::NIN, L = N::L, K = N::K;
@@ -63,15 +63,14 @@ struct QW {
   static constexpr int TPR = 2;
 #endif
   static_assert(TPR == 1 || TPR == 2, "threads per row");
-  // chain groups: two for the radiance shapes (one's MMA round trips and head
-  // overlap the other's); one for the product shape, whose 8-lobe head spills
-  // at the 80 registers of a 768-thread CTA and runs without spills at the 128
-  // of a 512-thread one (B200 c4 query 1.84 -> 1.59 ms)
-#ifdef NPM_QWS_PGROUPS   // measurement override for the product shape
-  static constexpr int GROUPS = N::PRODUCT ? NPM_QWS_PGROUPS : 2;
-#else
-  static constexpr int GROUPS = N::PRODUCT ? 1 : 2;
-#endif
+  // G chain groups (chosen per model by the host, `QueryArgs::qws_groups`):
+  // two for L2-resident radiance tables (one group's MMA round trips and head
+  // overlap the other's: B200 c2 205 vs 232 us with one); one for the
+  // product shape, whose 8-lobe head spills at the 80 registers of a
+  // 768-thread CTA and runs without spills at the 128 of a 512-thread one
+  // (c4 1.84 -> 1.59 ms), and for HBM-resident tables (c5 3.04 -> 2.34 ms)
+  static_assert(G == 1 || G == 2, "chain groups");
+  static constexpr int GROUPS = G;
   static constexpr int GROUP_THREADS = TPR * R, CHAIN_THREADS = GROUPS * GROUP_THREADS;
   static constexpr int MEM_THREADS = MP * R;
   // MP = 4 register split (setmaxnreg moves registers only within the CTA's
@@ -113,9 +112,9 @@ struct QW {
   static_assert(W <= 64 && NOUT <= 64, "accumulator columns");
 };
 
-template <class N, int MODE>
-__global__ void __launch_bounds__(QW<N, MODE>::THREADS, 1) query_ws_kernel(QueryArgs a) {
-  using T = QW<N, MODE>;
+template <class N, int MODE, int G>
+__global__ void __launch_bounds__(QW<N, MODE, G>::THREADS, 1) query_ws_kernel(QueryArgs a) {
+  using T = QW<N, MODE, G>;
   constexpr bool COMBINED = MODE == 1, COSPROD = MODE == 2;
   using TB = TC<N>;
   constexpr int NL = N::NL, K = N::K, W = N::W, L = N::L, KIN = T::KIN;

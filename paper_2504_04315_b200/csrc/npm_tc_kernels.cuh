@@ -1150,28 +1150,33 @@ struct TcLaunch {
       // warp-specialised kernel for sample / pdf and combined-MIS calls (npm_query_ws.cuh)
       if (a.qws && !a.feat_in && !a.raw && !a.lambda && !a.kappa && !a.mu &&
           (!N::PRODUCT || (!a.combined && !a.cos_product))) {
-        auto go = [&](auto MC) -> int {
-          constexpr int MODE = decltype(MC)::value;
-          using Q = qws::QW<N, MODE>;
+        auto go = [&](auto MC, auto GC) -> int {
+          constexpr int MODE = decltype(MC)::value, G = decltype(GC)::value;
+          using Q = qws::QW<N, MODE, G>;
           if (Q::MP == 4) {   // the setmaxnreg split assumes the launch allocation (a hang otherwise)
             static int regs = -1;
             if (regs < 0) {
               cudaFuncAttributes fa;
-              regs = cudaFuncGetAttributes(&fa, qws::query_ws_kernel<N, MODE>) == cudaSuccess ? fa.numRegs : 0;
+              regs = cudaFuncGetAttributes(&fa, qws::query_ws_kernel<N, MODE, G>) == cudaSuccess ? fa.numRegs : 0;
             }
             if (regs != Q::LAUNCH_REGS) return -1;
           }
-          cudaFuncSetAttribute(qws::query_ws_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          cudaFuncSetAttribute(qws::query_ws_kernel<N, MODE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Q::SMEM);
           const int64_t ntiles = (a.n + Q::R - 1) / Q::R;
           const int blocks = (int)(ntiles < (int64_t)sms ? ntiles : (int64_t)sms);
-          qws::query_ws_kernel<N, MODE><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
+          qws::query_ws_kernel<N, MODE, G><<<blocks, Q::THREADS, Q::SMEM, st>>>(a);
           return 1;
         };
-        if constexpr (N::PRODUCT) return go(std::integral_constant<int, 0>{});
-        else return a.combined ? go(std::integral_constant<int, 1>{})
-                               : a.cos_product ? go(std::integral_constant<int, 2>{})
-                                               : go(std::integral_constant<int, 0>{});
+        using G1 = std::integral_constant<int, 1>;
+        using G2 = std::integral_constant<int, 2>;
+        // chain groups: the plain call takes the model's choice (qws_groups);
+        // the product shape always one, the f-1 / f-2 calls two
+        if constexpr (N::PRODUCT) return go(std::integral_constant<int, 0>{}, G1{});
+        else return a.combined ? go(std::integral_constant<int, 1>{}, G2{})
+                               : a.cos_product ? go(std::integral_constant<int, 2>{}, G2{})
+                                               : a.qws_groups == 1 ? go(std::integral_constant<int, 0>{}, G1{})
+                                                                   : go(std::integral_constant<int, 0>{}, G2{});
       }
     }
     // 2 threads per sample row, 256-thread CTAs, two CTAs per SM (their MMA

@@ -148,6 +148,29 @@ def test_sample_with_caller_uniforms_and_fused_pdf(name):
     assert (np.abs(pdf_q - opdf_q) / opdf_q).max() <= 1e-3
 
 
+@pytest.mark.parametrize("name,groups", [("c2", "1"), ("c5", "2")])
+def test_query_ws_chain_groups_override(name, groups, monkeypatch):
+    """query_ws_kernel's other chain-group count for a shape (the default is
+    two for L2-resident radiance tables, one for HBM-resident ones and the
+    product shape; NPM_QWS_GROUPS overrides at model creation), several tiles
+    per CTA and a ragged tail, against the oracle."""
+    monkeypatch.setenv("NPM_QWS_GROUPS", groups)
+    m, ocfg, p = make_pair(name, seed=13)
+    n = 4 * 128 * 148 + 45   # >= 65,536: the binned order bench.py times
+    b = synth.query_batch(n, seed=16)
+    u = np.random.default_rng(4).uniform(size=(3, n)).astype(np.float32)
+    wi, pdf, pdf_q = (t.cpu().numpy() for t in m.sample(gq(m, b), u=u, wq=b["wq"]))
+    sel = np.concatenate([np.random.default_rng(5).choice(n, 3000, replace=False), [0, n - 1]])
+    _, act = onpm.decode(ocfg, p, dict(x=np.ascontiguousarray(b["x"][:, sel])))
+    us = u[:, sel].astype(np.float64)
+    ow, opdf, _ = ovmf.sample(act, us, ocfg.n_lobes)
+    ok = ~_boundary_mask(act, us[0], ocfg.n_lobes)
+    assert np.abs(wi[:, sel][:, ok] - ow[:, ok]).max() <= 1e-4
+    assert (np.abs(pdf[sel][ok] - opdf[ok]) / opdf[ok]).max() <= 1e-3
+    opq = ovmf.mixture_pdf(b["wq"][:, sel].astype(np.float64), act)
+    assert (np.abs(pdf_q[sel] - opq) / opq).max() <= 1e-3
+
+
 def test_philox_sampling_matches_oracle_generator():
     m, ocfg, p = pair("c2")
     n = 3000
