@@ -521,25 +521,59 @@ __global__ void __launch_bounds__(WS<N, AH, VA>::THREADS, 1) train_ws_kernel(Tra
               A[m] = Bk[m] = Bx[m] = By[m] = Bz[m] = 0.0f;
               Ck[m] = cnorm(kap[m]) * 0.15915494f;   // C(k_i) 2 pi * C(k_j) 2 pi / (2 pi)
             }
+            // the other part's 4 lobes against this thread's 4 (16 pairs), then the
+            // own part's 10 unordered pairs once each (I_ij = I_ji: the pair core is
+            // symmetric, only the e-weights and the accumulators differ; B200 c2
+            // 833 -> 766 us against all 32 ordered pairs per thread)
+            // the pair core, symmetric in (i, j): S = C_i C_j / (2 pi) 2 pi (1 - e^{-2r}) / r e^{r - k_i - k_j}
+            auto pair_core = [&](float ki, float ix, float iy, float iz, float kj, float jx, float jy, float jz,
+                                 float cij, float& S, float& lx, float& d2) {
+              const float dx = ix - jx, dy = iy - jy, dz = iz - jz;
+              d2 = dx * dx + dy * dy + dz * dz;
+              const float sk = ki + kj, pk = ki * kj;
+              const float rr = fmaxf(sqrtf(fmaxf(sk * sk - pk * d2, 0.0f)), 1e-30f);
+              const float ex = -__fdividef(pk * d2, rr + sk);
+              const float om = one_minus_exp_neg(2.0f * rr);
+              const float inv_r = __fdividef(1.0f, rr);
+              S = cij * om * inv_r * __expf(ex);
+              lx = lox_from(rr, om, inv_r);
+            };
+            float cn[KH];
+#pragma unroll
+            for (int m = 0; m < KH; ++m) cn[m] = cnorm(kap[m]);
 #pragma unroll 2
-            for (int j = 0; j < K; ++j) {
+            for (int jj = 0; jj < KH; ++jj) {
+              const int j = (1 - h) * KH + jj;
               const float kj = vx[(5 * j) * R + r], jx = vx[(5 * j + 1) * R + r], jy = vx[(5 * j + 2) * R + r],
-                          jz = vx[(5 * j + 3) * R + r], ej = vx[(5 * j + 4) * R + r] * (j < KH ? c0 : c1);
+                          jz = vx[(5 * j + 3) * R + r], ej = vx[(5 * j + 4) * R + r] * (h ? c0 : c1);
               const float Cj = ej * cnorm(kj);
 #pragma unroll
               for (int m = 0; m < KH; ++m) {
-                const float dx = mx[m] - jx, dy = my[m] - jy, dz = mz[m] - jz;
-                const float d2 = dx * dx + dy * dy + dz * dz;
-                const float sk = kap[m] + kj, pk = kap[m] * kj;
-                const float rr = fmaxf(sqrtf(fmaxf(sk * sk - pk * d2, 0.0f)), 1e-30f);
-                const float ex = -__fdividef(pk * d2, rr + sk);
-                const float om = one_minus_exp_neg(2.0f * rr);
-                const float inv_r = __fdividef(1.0f, rr);
-                const float wI = Ck[m] * Cj * om * inv_r * __expf(ex);   // e_j I_ij
-                A[m] += wI;
-                const float q = wI * lox_from(rr, om, inv_r);
+                float S, lx, d2;
+                pair_core(kap[m], mx[m], my[m], mz[m], kj, jx, jy, jz, Ck[m] * Cj, S, lx, d2);
+                A[m] += S;
+                const float q = S * lx;
                 Bk[m] += q * (kap[m] + kj * (1.0f - 0.5f * d2));
                 Bx[m] += q * kj * jx; By[m] += q * kj * jy; Bz[m] += q * kj * jz;
+              }
+            }
+#pragma unroll
+            for (int m = 0; m < KH; ++m) {
+#pragma unroll
+              for (int m2 = m; m2 < KH; ++m2) {
+                float S, lx, d2;
+                pair_core(kap[m], mx[m], my[m], mz[m], kap[m2], mx[m2], my[m2], mz[m2], Ck[m] * cn[m2], S, lx, d2);
+                const float sl = S * lx;
+                A[m] += e[m2] * S;
+                const float q = e[m2] * sl;
+                Bk[m] += q * (kap[m] + kap[m2] * (1.0f - 0.5f * d2));
+                Bx[m] += q * kap[m2] * mx[m2]; By[m] += q * kap[m2] * my[m2]; Bz[m] += q * kap[m2] * mz[m2];
+                if (m2 != m) {
+                  A[m2] += e[m] * S;
+                  const float q2 = e[m] * sl;
+                  Bk[m2] += q2 * (kap[m2] + kap[m] * (1.0f - 0.5f * d2));
+                  Bx[m2] += q2 * kap[m] * mx[m]; By[m2] += q2 * kap[m] * my[m]; Bz[m2] += q2 * kap[m] * mz[m];
+                }
               }
             }
             float Zh = 0.0f;
