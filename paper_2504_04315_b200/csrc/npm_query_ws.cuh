@@ -89,7 +89,13 @@ struct QW {
   // between the weights and the X0 stages -- the compact layout measured
   // slower on B200 (c2 212 vs 206 us, c5 3164 vs 3032 us; a pad at the end of
   // the layout instead: 212 us), cause not identified
+  // (one-group layouts drop the gap: c4 query 1.59 -> 1.47 ms -- the layout
+  // then fits the 164 KB carve-out -- and c5 2.34 -> 2.29 ms)
+#if defined(NPM_QWS_SMEMA)
   static constexpr uint32_t H_BYTES = 2u * (W / 8) * CHR;
+#else
+  static constexpr uint32_t H_BYTES = G == 1 ? 0u : 2u * (W / 8) * CHR;
+#endif
   static constexpr uint32_t RD_BYTES = RDF * R * 4;
   static constexpr uint32_t a1k(uint32_t x) { return (x + 1023u) & ~1023u; }
   static constexpr uint32_t OFF_W = 0, OFF_B = B::WBYTES;
